@@ -1,0 +1,157 @@
+/*
+ * xbarsim_b200.h — C ABI of the B200-native crossbar-evaluation hot path.
+ *
+ * Drop-in boundary for xbarsim::nn::CrossbarCore
+ * (/root/reference/proj/core/include/xbarsim/layers.hpp:49-111).  Plain
+ * pointers and sizes only; no CUDA, torch or C++ types cross this line, and no
+ * exception crosses it: every entry point returns an xbs_status and leaves a
+ * thread-local message in xbs_last_error().  The C++ classes in
+ * include/xbarsim/ (and the Python mirror paper_2002_11151_b200.xbarsim) wrap
+ * these calls and rethrow the reference's exception types.
+ *
+ * Host matrices follow the reference's storage: Eigen::MatrixXd is
+ * column-major, so element (i, j) of an R x C matrix with leading dimension ld
+ * lives at p[j * ld + i].
+ *
+ * Every call on a core is synchronous at return (like the reference), except
+ * the *_device entry points, which enqueue on the core's CUDA stream and
+ * return immediately (xbs_core_synchronize waits).
+ */
+#ifndef XBARSIM_B200_H_
+#define XBARSIM_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XBS_ABI_VERSION 1
+
+/* Status codes: one per reference exception class (errors.hpp:10-47). */
+typedef enum xbs_status {
+  XBS_OK = 0,
+  XBS_INVALID_ARGUMENT = 1,        /* std::invalid_argument                 */
+  XBS_STATE_ERROR = 2,             /* xbarsim::StateError                    */
+  XBS_CONFIG_ERROR = 3,            /* xbarsim::ConfigError                   */
+  XBS_CONVERGENCE_ERROR = 4,       /* xbarsim::ConvergenceError              */
+  XBS_STALE_CACHE_ERROR = 5,       /* xbarsim::StaleCacheError               */
+  XBS_DEGENERATE_CIRCUIT_ERROR = 6,/* xbarsim::DegenerateCircuitError        */
+  XBS_UNSUPPORTED = 7,             /* valid reference config outside this
+                                      path's scope (e.g. FCM with parasitics,
+                                      ADC auto-calibration); maps to
+                                      ConfigError in the C++ wrapper         */
+  XBS_CUDA_ERROR = 8,              /* device fault; StateError + CUDA string */
+  XBS_INTERNAL = 9
+} xbs_status;
+
+/* EngineKind (engine.hpp:15-35). */
+enum { XBS_ENGINE_IDEAL = 0, XBS_ENGINE_ORACLE = 1, XBS_ENGINE_FCM = 2, XBS_ENGINE_AAM = 3,
+       XBS_ENGINE_INTERP_FCM = 4 };
+
+/* Flat POD mirroring CrossbarLayerOptions (layers.hpp:19-37) and the specs
+ * it aggregates.  xbs_options_init() fills the reference defaults. */
+typedef struct xbs_layer_options {
+  /* MappingSpec (mapping.hpp:14-25) */
+  int32_t weight_bits, device_bits, tile_rows, tile_cols;
+  double variation_sigma;
+  uint64_t variation_seed;
+  double w_max;
+  /* CrossbarConfig (crossbar.hpp:17-40) */
+  int32_t xbar_rows, xbar_cols;
+  double r_row, r_col, r_source, r_sense, g_min, g_max, v_fs;
+  /* DacSpec (converters.hpp:14-22) */
+  int32_t dac_bits, dac_stream_bits;
+  double dac_v_fs;
+  const double* dac_transfer; /* NULL: ideal linear */
+  int32_t dac_transfer_len;
+  /* AdcSpec (converters.hpp:37-45) */
+  int32_t adc_bits;
+  double adc_i_fs;
+  const double* adc_transfer; /* NULL: linear */
+  int32_t adc_transfer_len;
+  double adc_clip_percentile;
+  /* UpdateSpec (update.hpp:13-23) */
+  double upd_v, upd_gamma, upd_lr;
+  uint64_t upd_seed;
+  double upd_layer_scale;
+  /* CrossbarLayerOptions proper */
+  int32_t engine, interp_base, interp_interval;
+  double fcm_tol;
+  int32_t fcm_max_iter;
+  int32_t act_bits;
+  double act_full_scale;
+  int32_t error_bits, adc_cal_batches, threads;
+} xbs_layer_options;
+
+/* Reference statistics getters (layers.hpp:64-68) plus geometry. */
+typedef struct xbs_core_info {
+  int32_t in_features, out_features;          /* K, N                        */
+  int32_t grid_rows, grid_cols;               /* TiledLayerWeights grid      */
+  int32_t padded_rows, padded_cols;           /* Kp, Np                      */
+  int32_t num_slices;
+  int32_t snap_exponent;                      /* e of the 2^-e grid          */
+  double layer_scale, level_step;
+  int64_t refresh_count;                      /* refresh_count()             */
+  double conversion_seconds;                  /* conversion_seconds()        */
+  double weight_abs_max_seen;                 /* weight_abs_max_seen()       */
+  double grad_abs_max_seen;                   /* grad_abs_max_seen()         */
+  double forward_adc_full_scale;              /* forward_adc_full_scale()    */
+  int32_t fully_ideal;                        /* fully_ideal() fast path     */
+  int32_t kernel;                             /* 0 = tcgen05, 1 = SIMT check */
+} xbs_core_info;
+
+typedef struct xbs_core xbs_core;
+
+int32_t xbs_abi_version(void);
+const char* xbs_last_error(void);
+void xbs_options_init(xbs_layer_options* opt);
+
+/* CrossbarCore::CrossbarCore(W0, opt) — layers.cpp:68-83.  W0 is K x N,
+ * column-major with leading dimension ldw >= K. */
+int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, int64_t N, int64_t ldw,
+                    xbs_core** out);
+void xbs_core_destroy(xbs_core* core);
+
+/* CrossbarCore::forward(x, training) — layers.cpp:215-284.  x: M x K,
+ * y: M x N, column-major host buffers. */
+int xbs_core_forward(xbs_core* core, const double* x, int64_t M, int64_t ldx, int32_t training, double* y,
+                     int64_t ldy);
+/* CrossbarCore::backward(dy, grad_divisor) — layers.cpp:286-380.  dy: M x N,
+ * dx: M x K, column-major host buffers. */
+int xbs_core_backward(xbs_core* core, const double* dy, int64_t M, int64_t lddy, double grad_divisor,
+                      double* dx, int64_t lddx);
+/* CrossbarCore::apply_updates(iteration) — layers.cpp:382-391. */
+int xbs_core_apply_updates(xbs_core* core, uint64_t iteration);
+
+/* Device-resident variants (HBM pointers, column-major, ld = M): enqueue on
+ * the core's stream, return at once.  Same semantics as the host calls. */
+int xbs_core_forward_device(xbs_core* core, const double* d_x, int64_t M, int32_t training, double* d_y);
+int xbs_core_backward_device(xbs_core* core, const double* d_dy, int64_t M, double grad_divisor,
+                             double* d_dx);
+int xbs_core_apply_updates_device(xbs_core* core, uint64_t iteration);
+int xbs_core_synchronize(xbs_core* core);
+
+/* Accessors (layers.hpp:59-71).  Host copies. */
+int xbs_core_get_info(xbs_core* core, xbs_core_info* info);
+int xbs_core_gradient(xbs_core* core, double* dW, int64_t ld);             /* K x N */
+int xbs_core_set_gradient(xbs_core* core, const double* dW, int64_t ld);   /* feeds apply_update
+                                                                               (update.hpp:51-52) */
+int xbs_core_nonideal(xbs_core* core, int32_t slice, int32_t polarity, int32_t tile, double* g,
+                      int64_t ld);                                         /* tile_rows x tile_cols */
+int xbs_core_master(xbs_core* core, int32_t slice, double* u, int64_t ld);  /* Kp x Np */
+int xbs_core_set_master(xbs_core* core, int32_t slice, const double* u, int64_t ld);
+int xbs_core_implied_weights(xbs_core* core, double* w, int64_t ld);       /* K x N */
+
+/* Diagnostics for the parity harness: ADC conversions that took the exact
+ * fp64 boundary path in the last forward/backward, and total conversions. */
+int xbs_core_adc_counters(xbs_core* core, int64_t* exact_path, int64_t* conversions);
+/* Select the VMM kernel: 0 = tcgen05 (default), 1 = exact SIMT cross-check. */
+int xbs_core_select_kernel(xbs_core* core, int32_t kernel);
+/* CUDA stream (cudaStream_t) the core enqueues on, as an opaque pointer. */
+void* xbs_core_stream(xbs_core* core);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XBARSIM_B200_H_ */

@@ -1,0 +1,22 @@
+"""B200-native crossbar-evaluation hot path of TxSim (arxiv 2002.11151).
+
+The product is the C-ABI library ``_lib/libxbarsim_b200.so`` (include/xbarsim_b200.h)
+with its C++ drop-in classes (include/xbarsim/) and this Python mirror
+(:mod:`paper_2002_11151_b200.xbarsim`) of the reference's CrossbarCore API.
+"""
+from . import xbarsim  # noqa: F401
+from .xbarsim import (  # noqa: F401
+    AdcSpec,
+    ConfigError,
+    CrossbarConfig,
+    CrossbarCore,
+    CrossbarLayerOptions,
+    CrossbarLinear,
+    DacSpec,
+    EngineKind,
+    MappingSpec,
+    Polarity,
+    StateError,
+    Tensor,
+    UpdateSpec,
+)

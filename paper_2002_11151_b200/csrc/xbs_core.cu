@@ -1,0 +1,644 @@
+// C-ABI implementation: the CrossbarCore state machine (layers.cpp:68-391)
+// over device-resident state.  Host code validates exactly like the reference
+// (same order, same exception classes mapped to status codes), computes the
+// fp64 scale constants with the reference's expressions, and enqueues the
+// kernels on the core's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "xbs_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct XbsError : std::runtime_error {
+  int code;
+  XbsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw XbsError(code, m); }
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(XBS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return XBS_OK;
+  } catch (const XbsError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return XBS_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return XBS_INTERNAL;
+  }
+}
+
+bool is_pow2_double(double v) {
+  int e;
+  return v > 0 && std::frexp(v, &e) == 0.5;
+}
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// ---- validation, in the reference's order and with its exception classes
+void validate_crossbar(const xbs_layer_options& o) {  // crossbar.hpp:31-39
+  if (o.xbar_rows < 1 || o.xbar_cols < 1) fail(XBS_INVALID_ARGUMENT, "CrossbarConfig: rows and cols must be >= 1");
+  if (o.r_row < 0 || o.r_col < 0 || o.r_source < 0 || o.r_sense < 0)
+    fail(XBS_INVALID_ARGUMENT, "CrossbarConfig: resistances must be >= 0");
+  if (!(o.g_min > 0) || !(o.g_max > o.g_min)) fail(XBS_INVALID_ARGUMENT, "CrossbarConfig: need 0 < g_min < g_max");
+  if (!(o.v_fs > 0)) fail(XBS_INVALID_ARGUMENT, "CrossbarConfig: v_fs must be > 0");
+}
+void validate_mapping(const xbs_layer_options& o) {  // mapping.cpp:10-24
+  if (o.weight_bits < 1 || o.weight_bits > 24) fail(XBS_INVALID_ARGUMENT, "MappingSpec: weight_bits must be in [1, 24]");
+  if (o.device_bits < 1 || o.device_bits > o.weight_bits)
+    fail(XBS_INVALID_ARGUMENT, "MappingSpec: device_bits must be in [1, weight_bits]");
+  if (o.weight_bits % o.device_bits != 0)
+    fail(XBS_INVALID_ARGUMENT, "MappingSpec: weight_bits must be divisible by device_bits");
+  if (o.tile_rows < 1 || o.tile_cols < 1) fail(XBS_INVALID_ARGUMENT, "MappingSpec: tile dims must be >= 1");
+  if (o.tile_rows > o.xbar_rows || o.tile_cols > o.xbar_cols)
+    fail(XBS_INVALID_ARGUMENT, "MappingSpec: tile dims exceed crossbar dims");
+  if (o.variation_sigma < 0) fail(XBS_INVALID_ARGUMENT, "MappingSpec: variation_sigma must be >= 0");
+}
+void validate_options(const xbs_layer_options& o, const std::vector<double>& dac_tr,
+                      const std::vector<double>& adc_tr) {  // layers.cpp:17-47
+  validate_crossbar(o);
+  validate_mapping(o);
+  // DacSpec::validate (converters.cpp:11-26)
+  if (o.dac_bits < 1 || o.dac_bits > 32) fail(XBS_INVALID_ARGUMENT, "DacSpec: bits must be in [1, 32]");
+  if (!(o.dac_v_fs > 0)) fail(XBS_INVALID_ARGUMENT, "DacSpec: v_fs must be > 0");
+  if (o.dac_stream_bits < 1) fail(XBS_INVALID_ARGUMENT, "DacSpec: stream_bits must be >= 1");
+  if (!dac_tr.empty()) {
+    if (dac_tr.size() != (size_t{1} << o.dac_bits))
+      fail(XBS_INVALID_ARGUMENT, "DacSpec: transfer table must have 2^bits entries");
+    if (dac_tr.front() != 0.0) fail(XBS_INVALID_ARGUMENT, "DacSpec: transfer[0] must be 0");
+    if (dac_tr.back() > o.dac_v_fs) fail(XBS_INVALID_ARGUMENT, "DacSpec: transfer must not exceed v_fs");
+    if (!std::is_sorted(dac_tr.begin(), dac_tr.end()))
+      fail(XBS_INVALID_ARGUMENT, "DacSpec: transfer table must be monotone");
+  }
+  // AdcSpec::validate (converters.cpp:57-68)
+  if (o.adc_bits < 0 || o.adc_bits > 32) fail(XBS_INVALID_ARGUMENT, "AdcSpec: bits must be in [0, 32]");
+  if (!(o.adc_clip_percentile > 0.0) || o.adc_clip_percentile > 1.0)
+    fail(XBS_INVALID_ARGUMENT, "AdcSpec: clip_percentile must be in (0, 1]");
+  if (!adc_tr.empty()) {
+    if (o.adc_bits == 0) fail(XBS_INVALID_ARGUMENT, "AdcSpec: transfer table with pass-through ADC");
+    if (!std::is_sorted(adc_tr.begin(), adc_tr.end()))
+      fail(XBS_INVALID_ARGUMENT, "AdcSpec: transfer thresholds must be monotone");
+  }
+  // UpdateSpec::validate (update.cpp:10-14)
+  if (o.upd_v < 0) fail(XBS_INVALID_ARGUMENT, "UpdateSpec: v must be >= 0");
+  if (o.upd_gamma < 0) fail(XBS_INVALID_ARGUMENT, "UpdateSpec: gamma must be >= 0");
+  if (!(o.upd_lr > 0)) fail(XBS_INVALID_ARGUMENT, "UpdateSpec: lr must be > 0");
+  if (o.dac_bits != o.dac_stream_bits)
+    fail(XBS_CONFIG_ERROR, "dac.bits (" + std::to_string(o.dac_bits) + ") must equal dac.stream_bits (" +
+                               std::to_string(o.dac_stream_bits) + "): the streamed slice is the physical converter");
+  if (o.act_bits < 1 || o.act_bits > 24) fail(XBS_CONFIG_ERROR, "act_bits must be in [1, 24]");
+  if (o.error_bits < 1 || o.error_bits > 24) fail(XBS_CONFIG_ERROR, "error_bits must be in [1, 24]");
+  if (o.act_bits % o.dac_stream_bits != 0) fail(XBS_CONFIG_ERROR, "activation_bits must be divisible by dac.stream_bits");
+  if (o.error_bits % o.dac_stream_bits != 0) fail(XBS_CONFIG_ERROR, "error_bits must be divisible by dac.stream_bits");
+  if (!(o.act_full_scale > 0)) fail(XBS_CONFIG_ERROR, "act_full_scale must be > 0");
+  if (o.interp_interval < 1) fail(XBS_CONFIG_ERROR, "interp_interval must be >= 1");
+  if (o.engine == XBS_ENGINE_INTERP_FCM && o.interp_base != XBS_ENGINE_FCM && o.interp_base != XBS_ENGINE_AAM)
+    fail(XBS_CONFIG_ERROR, "interp_base must be fcm or aam");
+  if (o.adc_cal_batches < 1) fail(XBS_CONFIG_ERROR, "adc_cal_batches must be >= 1");
+  if (o.threads < 1) fail(XBS_CONFIG_ERROR, "threads must be >= 1");
+}
+
+// Path scope: valid reference configurations this
+// B200 path does not evaluate are refused loudly, never approximated.
+void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, const std::vector<double>& adc_tr) {
+  const bool zero_par = o.r_row == 0.0 && o.r_col == 0.0 && o.r_source == 0.0 && o.r_sense == 0.0;
+  if ((o.engine == XBS_ENGINE_FCM || o.engine == XBS_ENGINE_ORACLE || o.engine == XBS_ENGINE_INTERP_FCM) && !zero_par)
+    fail(XBS_UNSUPPORTED, "engine fcm/oracle/interp_fcm with parasitics is not on this path (SURVEY §8f-1)");
+  if (o.engine < 0 || o.engine > 4) fail(XBS_INVALID_ARGUMENT, "unknown engine");
+  if (o.adc_bits > 0 && adc_tr.empty() && !(o.adc_i_fs > 0))
+    fail(XBS_UNSUPPORTED, "ADC auto-calibration (adc.i_fs <= 0) is not on this path: pin adc.i_fs (SURVEY §8f-3)");
+  if (!adc_tr.empty()) fail(XBS_UNSUPPORTED, "ADC transfer tables are not on this path");
+  if (!dac_tr.empty()) fail(XBS_UNSUPPORTED, "DAC transfer tables are not on this path");
+  if (o.adc_bits > 16) fail(XBS_UNSUPPORTED, "adc.bits > 16 is not on this path");
+  if (o.dac_bits != 1) fail(XBS_UNSUPPORTED, "only the 1-bit DAC stream is on this path");
+  if (!is_pow2_double(o.dac_v_fs)) fail(XBS_UNSUPPORTED, "dac.v_fs must be a power of two (exact currents)");
+  if (o.act_bits > 16 || o.error_bits > 16) fail(XBS_UNSUPPORTED, "act_bits / error_bits > 16 are not on this path");
+  if (o.tile_rows > 256 || o.tile_cols > 256) fail(XBS_UNSUPPORTED, "tiles larger than 256 x 256 are not on this path");
+}
+
+int snap_exponent(double g_max) {  // largest e with g_max * 2^e <= Q_MAX
+  int e;
+  (void)std::frexp(xbs::kQMax / g_max, &e);
+  e += 2;
+  while (std::ldexp(g_max, e) > xbs::kQMax) --e;
+  return e;
+}
+
+void ensure_batch(xbs_core* c, int64_t M) {
+  if (M <= c->M_cap) return;
+  const int64_t cap = std::max<int64_t>(M, 2 * c->M_cap);
+  cudaFree(c->d_Af);
+  cudaFree(c->d_Ab);
+  cudaFree(c->d_xcodes);
+  cudaFree(c->d_ecodes);
+  c->d_Af = nullptr;
+  c->d_Ab = nullptr;
+  c->d_xcodes = nullptr;
+  c->d_ecodes = nullptr;
+  const int64_t rowsF = ((cap * c->g.TPi + 127) / 128) * 128;
+  const int64_t rowsB = ((cap * c->g.TPe * 2 + 127) / 128) * 128;
+  ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
+  ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NI), "cudaMalloc A_bwd");
+  ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
+  ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int16_t)), "cudaMalloc ecodes");
+  c->M_cap = cap;
+}
+
+void ensure_io(xbs_core* c, int64_t elems) {
+  if (elems <= c->io_cap) return;
+  cudaFree(c->d_io_in);
+  cudaFree(c->d_io_out);
+  c->d_io_in = c->d_io_out = nullptr;
+  ck(cudaMalloc(&c->d_io_in, size_t(elems) * 8), "cudaMalloc io_in");
+  ck(cudaMalloc(&c->d_io_out, size_t(elems) * 8), "cudaMalloc io_out");
+  c->io_cap = elems;
+}
+
+void sync(xbs_core* c) {
+  ck(cudaStreamSynchronize(c->stream), "kernel execution");
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+void regenerate_bookkeeping(xbs_core* c) {
+  if (c->opt.engine == XBS_ENGINE_IDEAL) xbs::launch_implied(c, c->d_wimp, c->stream);
+  if (c->opt.engine != XBS_ENGINE_IDEAL) ++c->refreshes;  // layers.cpp:176
+}
+
+// host col-major (ld) <-> device row-major (rows x cols)
+void h2d_colmajor_to_rowmajor(xbs_core* c, const double* h, int64_t rows, int64_t cols, int64_t ld, double* d) {
+  c->h_tmp.assign(size_t(rows * cols), 0.0);
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t i = 0; i < rows; ++i) c->h_tmp[size_t(i * cols + j)] = h[j * ld + i];
+  ck(cudaMemcpy(d, c->h_tmp.data(), size_t(rows * cols) * 8, cudaMemcpyHostToDevice), "H2D");
+}
+void d2h_rowmajor_to_colmajor(xbs_core* c, const double* d, int64_t rows, int64_t cols, double* h, int64_t ld) {
+  c->h_tmp.resize(size_t(rows * cols));
+  ck(cudaMemcpy(c->h_tmp.data(), d, size_t(rows * cols) * 8, cudaMemcpyDeviceToHost), "D2H");
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t i = 0; i < rows; ++i) h[j * ld + i] = c->h_tmp[size_t(i * cols + j)];
+}
+
+void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y) {
+  (void)training;  // training only feeds ADC auto-calibration (out of scope)
+  if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
+  ensure_batch(c, std::max<int64_t>(M, 1));
+  xbs::launch_prep_x(c, d_x, M, c->stream);
+  c->have_forward = true;
+  c->M_fwd = M;
+  if (M == 0) return;
+  if (c->fully_ideal) {
+    xbs::launch_fwd_ideal(c, M, d_y, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_fwd_tc(c, M, d_y, c->stream)) {
+    xbs::launch_fwd_simt(c, M, d_y, c->stream);
+  }
+}
+
+void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
+  if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
+  if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
+  xbs::launch_prep_dy(c, d_dy, M, c->stream);
+  xbs::launch_dw(c, M, gd, c->stream);
+  c->have_grad = true;
+  if (M == 0) return;
+  if (c->fully_ideal) {
+    xbs::launch_bwd_ideal(c, d_dy, M, d_dx, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_bwd_tc(c, M, d_dx, c->stream)) {
+    xbs::launch_bwd_simt(c, M, d_dx, c->stream);
+  }
+}
+
+void apply_updates_device(xbs_core* c, uint64_t iteration) {
+  if (!c->have_grad) return;  // layers.cpp:383
+  xbs::UpdP up{};
+  up.v = c->opt.upd_v;
+  up.gamma = c->opt.upd_gamma;
+  up.lr = c->opt.upd_lr;
+  const double ls = c->opt.upd_layer_scale == 0.0 ? c->layer_scale : c->opt.upd_layer_scale;  // update.cpp:52
+  up.factor = (c->opt.g_max - c->opt.g_min) / ls;
+  const double levels = double((uint64_t{1} << c->g.wb) - 1), sl = double((uint64_t{1} << c->g.db) - 1);
+  up.wfactor = (c->layer_scale / (c->opt.g_max - c->opt.g_min)) * (sl / levels);
+  up.seed = c->opt.upd_seed;
+  up.iteration = iteration;
+  up.linear = c->opt.upd_v == 0.0;
+  ck(cudaMemsetAsync(&c->d_sc->dwmax, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
+  ck(cudaMemsetAsync(&c->d_sc->err_flag, 0, sizeof(int), c->stream), "memset");
+  xbs::launch_update(c, up, c->stream);
+  regenerate_bookkeeping(c);
+  c->have_grad = false;
+  c->have_forward = false;
+}
+
+void finish_update_stats(xbs_core* c) {
+  ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+  if (c->h_sc->err_flag) fail(XBS_INVALID_ARGUMENT, "nonlinear_update: g outside device range");
+  c->dwmax_seen = std::max(c->dwmax_seen, __builtin_bit_cast(double, c->h_sc->dwmax));
+  c->wmax_seen = std::max(c->wmax_seen, __builtin_bit_cast(double, c->h_sc->wmax));
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t xbs_abi_version(void) { return XBS_ABI_VERSION; }
+const char* xbs_last_error(void) { return g_err.c_str(); }
+
+void xbs_options_init(xbs_layer_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->weight_bits = 8;  // MappingSpec defaults (mapping.hpp:15-21)
+  o->device_bits = 2;
+  o->tile_rows = 64;
+  o->tile_cols = 64;
+  o->variation_sigma = 0.0;
+  o->variation_seed = 0;
+  o->w_max = 0.0;
+  o->xbar_rows = 64;  // CrossbarConfig defaults (crossbar.hpp:18-26)
+  o->xbar_cols = 64;
+  o->r_row = 1.0;
+  o->r_col = 4.6;
+  o->r_source = 0.0;
+  o->r_sense = 0.0;
+  o->g_min = 1e-6;
+  o->g_max = 1e-5;
+  o->v_fs = 1.0;
+  o->dac_bits = 1;  // DacSpec (converters.hpp:15-18)
+  o->dac_stream_bits = 1;
+  o->dac_v_fs = 1.0;
+  o->adc_bits = 8;  // AdcSpec (converters.hpp:38-41)
+  o->adc_i_fs = 0.0;
+  o->adc_clip_percentile = 0.999;
+  o->upd_v = 0.0;  // UpdateSpec (update.hpp:14-20)
+  o->upd_gamma = 0.0;
+  o->upd_lr = 0.01;
+  o->upd_seed = 0;
+  o->upd_layer_scale = 0.0;
+  o->engine = XBS_ENGINE_FCM;  // CrossbarLayerOptions (layers.hpp:25-34)
+  o->interp_base = XBS_ENGINE_FCM;
+  o->interp_interval = 10;
+  o->fcm_tol = 1e-6;
+  o->fcm_max_iter = 1000;
+  o->act_bits = 8;
+  o->act_full_scale = 1.0;
+  o->error_bits = 8;
+  o->adc_cal_batches = 20;
+  o->threads = 1;
+}
+
+int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, int64_t N, int64_t ldw,
+                    xbs_core** out) {
+  return guard([&] {
+    if (!opt || !out) fail(XBS_INVALID_ARGUMENT, "xbs_core_create: null argument");
+    *out = nullptr;
+    auto c = std::make_unique<xbs_core>();
+    c->opt = *opt;
+    if (opt->dac_transfer && opt->dac_transfer_len > 0)
+      c->dac_tr.assign(opt->dac_transfer, opt->dac_transfer + opt->dac_transfer_len);
+    if (opt->adc_transfer && opt->adc_transfer_len > 0)
+      c->adc_tr.assign(opt->adc_transfer, opt->adc_transfer + opt->adc_transfer_len);
+    c->opt.dac_transfer = nullptr;
+    c->opt.adc_transfer = nullptr;
+    const xbs_layer_options& o = c->opt;
+    // map_weights validates first (layers.cpp:69 -> mapping.cpp:85-90)
+    validate_crossbar(o);
+    validate_mapping(o);
+    if (K == 0 || N == 0) fail(XBS_INVALID_ARGUMENT, "map_weights: empty weight matrix");
+    if (K < 0 || N < 0 || ldw < K || !W0) fail(XBS_INVALID_ARGUMENT, "map_weights: bad weight matrix");
+    double wabs = 0.0;
+    for (int64_t j = 0; j < N; ++j)
+      for (int64_t i = 0; i < K; ++i) {
+        const double w = W0[j * ldw + i];
+        if (!std::isfinite(w)) fail(XBS_INVALID_ARGUMENT, "map_weights: weights must be finite");
+        wabs = std::max(wabs, std::abs(w));
+      }
+    validate_options(o, c->dac_tr, c->adc_tr);  // layers.cpp:70
+    check_scope(o, c->dac_tr, c->adc_tr);
+
+    xbs::Geo& g = c->g;
+    g.K = int(K);
+    g.N = int(N);
+    g.tile_rows = o.tile_rows;
+    g.tile_cols = o.tile_cols;
+    g.GR = (g.K + o.tile_rows - 1) / o.tile_rows;
+    g.GC = (g.N + o.tile_cols - 1) / o.tile_cols;
+    g.Kp = g.GR * o.tile_rows;
+    g.Np = g.GC * o.tile_cols;
+    g.R = ((o.tile_rows + 127) / 128) * 128;
+    g.C = ((o.tile_cols + 127) / 128) * 128;
+    g.KI = g.GR * g.R;
+    g.NI = g.GC * g.C;
+    g.S = o.weight_bits / o.device_bits;
+    g.db = o.device_bits;
+    g.wb = o.weight_bits;
+    g.Ti = o.act_bits;
+    g.TPi = next_pow2(o.act_bits);
+    g.Te = o.error_bits;
+    g.TPe = next_pow2(o.error_bits);
+
+    double scale = o.w_max > 0 ? o.w_max : wabs;  // mapping.cpp:104-105
+    if (scale == 0.0) scale = 1.0;
+    c->layer_scale = scale;
+    c->level_step = (o.g_max - o.g_min) / double((uint64_t{1} << o.device_bits) - 1);
+
+    c->fully_ideal = o.engine == XBS_ENGINE_IDEAL && o.variation_sigma == 0.0 && c->dac_tr.empty() && o.adc_bits == 0;
+    const bool zero_par = o.r_row == 0.0 && o.r_col == 0.0 && o.r_source == 0.0 && o.r_sense == 0.0;
+    xbs::RegenP& rp = c->rp;
+    rp.g_min = o.g_min;
+    rp.g_max = o.g_max;
+    rp.range = o.g_max - o.g_min;
+    rp.sigma = o.variation_sigma;
+    rp.vseed = o.variation_seed;
+    rp.r_row = o.r_row;
+    rp.r_col = o.r_col;
+    rp.r_source = o.r_source;
+    rp.r_sense = o.r_sense;
+    rp.aam = (o.engine == XBS_ENGINE_AAM && !zero_par) ? 1 : 0;
+    rp.snap_e = snap_exponent(o.g_max);
+
+    // scale constants, same expressions as layers.cpp:272-281 / 369-377
+    const double vu = o.dac_v_fs / (std::pow(2.0, o.dac_bits) - 1.0);
+    const double sx = o.act_full_scale / (std::pow(2.0, o.act_bits) - 1.0);
+    const double levels = std::pow(2.0, o.weight_bits) - 1.0;
+    const double slice_levels = std::pow(2.0, o.device_bits) - 1.0;
+    const double F = (scale / (o.g_max - o.g_min)) * (slice_levels / levels);
+    c->vu = vu;
+    c->F = F;
+    c->sx = o.act_full_scale / double((1 << o.act_bits) - 1);  // tensor.cpp:29 (codes_to_values)
+    c->lev_e = std::pow(2.0, o.error_bits) - 1.0;
+    c->adc_scaled = o.adc_bits > 0 && c->adc_tr.empty();  // frozen or explicit (no auto-cal on this path)
+    c->ifs_fac = c->adc_scaled ? o.adc_i_fs / (std::pow(2.0, o.adc_bits) - 1.0) : 1.0;
+    double k_out = sx * F / vu;
+    if (c->adc_scaled) k_out *= c->ifs_fac;
+    c->k_out_fwd = k_out;
+
+    xbs::AdcP& a = c->adc;
+    a.passthrough = o.adc_bits == 0;
+    a.maxc = o.adc_bits > 0 ? int((1u << o.adc_bits) - 1) : 0;
+    a.maxc_d = double(a.maxc);
+    a.i_fs = o.adc_i_fs;
+    int lv;
+    (void)std::frexp(o.dac_v_fs, &lv);
+    a.sh = (lv - 1) - rp.snap_e;
+    if (a.passthrough && !c->fully_ideal) {
+      // pass-through totals must stay exact in fp64 (< 2^53 units of 2^-e)
+      const double qmax = std::ldexp(o.g_max, rp.snap_e), sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
+      const double fwd = double(g.GR) * o.tile_rows * qmax * (std::pow(2.0, g.Ti) - 1) * sw;
+      const double bwd = 2.0 * double(g.GC) * o.tile_cols * qmax * (std::pow(2.0, g.Te) - 1) * sw;
+      if (std::max(fwd, bwd) >= 9007199254740992.0)
+        fail(XBS_UNSUPPORTED, "pass-through ADC totals exceed 2^53 on this layer (inexact in the reference)");
+    }
+
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaMalloc(&c->d_master, size_t(g.S) * g.Kp * g.Np * 8), "cudaMalloc master");
+    ck(cudaMalloc(&c->d_digits, g.digits_bytes()), "cudaMalloc digits");
+    ck(cudaMemsetAsync(c->d_digits, 0, g.digits_bytes(), c->stream), "memset digits");
+    ck(cudaMalloc(&c->d_dW, size_t(g.K) * g.N * 8), "cudaMalloc dW");
+    ck(cudaMemsetAsync(c->d_dW, 0, size_t(g.K) * g.N * 8, c->stream), "memset dW");
+    if (o.engine == XBS_ENGINE_IDEAL) ck(cudaMalloc(&c->d_wimp, size_t(g.K) * g.N * 8), "cudaMalloc wimp");
+    ck(cudaMalloc(&c->d_sc, sizeof(xbs::DevScalars)), "cudaMalloc scalars");
+    ck(cudaMemsetAsync(c->d_sc, 0, sizeof(xbs::DevScalars), c->stream), "memset scalars");
+    ck(cudaMallocHost(&c->h_sc, sizeof(xbs::DevScalars)), "cudaMallocHost");
+
+    // W0 -> device (contiguous column-major K x N) -> master
+    double* d_W = nullptr;
+    ck(cudaMalloc(&d_W, size_t(K) * N * 8), "cudaMalloc W");
+    ck(cudaMemcpy2DAsync(d_W, size_t(K) * 8, W0, size_t(ldw) * 8, size_t(K) * 8, size_t(N), cudaMemcpyHostToDevice,
+                         c->stream),
+       "H2D W");
+    xbs::launch_map_weights(c.get(), d_W, c->stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!c->fully_ideal) xbs::launch_regen_all(c.get(), c->stream);
+    regenerate_bookkeeping(c.get());
+    sync(c.get());
+    c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    cudaFree(d_W);
+    *out = c.release();
+  });
+}
+
+void xbs_core_destroy(xbs_core* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_digits);
+  cudaFree(c->d_master);
+  cudaFree(c->d_dW);
+  cudaFree(c->d_wimp);
+  cudaFree(c->d_sc);
+  cudaFreeHost(c->h_sc);
+  cudaFree(c->d_Af);
+  cudaFree(c->d_Ab);
+  cudaFree(c->d_xcodes);
+  cudaFree(c->d_ecodes);
+  cudaFree(c->d_io_in);
+  cudaFree(c->d_io_out);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t ldx, int32_t training, double* y, int64_t ldy) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    if (M < 0 || (M > 0 && (ldx < M || ldy < M || !x || !y))) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: bad buffers");
+    ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
+    if (M > 0)
+      ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, x, size_t(ldx) * 8, size_t(M) * 8, size_t(c->g.K),
+                           cudaMemcpyHostToDevice, c->stream),
+         "H2D x");
+    forward_device(c, c->d_io_in, M, training != 0, c->d_io_out);
+    if (M > 0)
+      ck(cudaMemcpy2DAsync(y, size_t(ldy) * 8, c->d_io_out, size_t(M) * 8, size_t(M) * 8, size_t(c->g.N),
+                           cudaMemcpyDeviceToHost, c->stream),
+         "D2H y");
+    sync(c);
+  });
+}
+
+int xbs_core_backward(xbs_core* c, const double* dy, int64_t M, int64_t lddy, double gd, double* dx, int64_t lddx) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
+    if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
+    if (M > 0 && (lddy < M || lddx < M || !dy || !dx)) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: bad buffers");
+    ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
+    if (M > 0)
+      ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, dy, size_t(lddy) * 8, size_t(M) * 8, size_t(c->g.N),
+                           cudaMemcpyHostToDevice, c->stream),
+         "H2D dy");
+    backward_device(c, c->d_io_in, M, gd, c->d_io_out);
+    if (M > 0)
+      ck(cudaMemcpy2DAsync(dx, size_t(lddx) * 8, c->d_io_out, size_t(M) * 8, size_t(M) * 8, size_t(c->g.K),
+                           cudaMemcpyDeviceToHost, c->stream),
+         "D2H dx");
+    sync(c);
+  });
+}
+
+int xbs_core_apply_updates(xbs_core* c, uint64_t iteration) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    if (!c->have_grad) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    apply_updates_device(c, iteration);
+    sync(c);
+    c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    finish_update_stats(c);
+  });
+}
+
+int xbs_core_forward_device(xbs_core* c, const double* d_x, int64_t M, int32_t training, double* d_y) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    forward_device(c, d_x, M, training != 0, d_y);
+  });
+}
+int xbs_core_backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    backward_device(c, d_dy, M, gd, d_dx);
+  });
+}
+int xbs_core_apply_updates_device(xbs_core* c, uint64_t iteration) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    apply_updates_device(c, iteration);
+  });
+}
+int xbs_core_synchronize(xbs_core* c) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    sync(c);
+    finish_update_stats(c);
+  });
+}
+
+int xbs_core_get_info(xbs_core* c, xbs_core_info* info) {
+  return guard([&] {
+    if (!c || !info) fail(XBS_INVALID_ARGUMENT, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->in_features = c->g.K;
+    info->out_features = c->g.N;
+    info->grid_rows = c->g.GR;
+    info->grid_cols = c->g.GC;
+    info->padded_rows = c->g.Kp;
+    info->padded_cols = c->g.Np;
+    info->num_slices = c->g.S;
+    info->snap_exponent = c->rp.snap_e;
+    info->layer_scale = c->layer_scale;
+    info->level_step = c->level_step;
+    info->refresh_count = c->refreshes;
+    info->conversion_seconds = c->conversion_seconds;
+    info->weight_abs_max_seen = c->wmax_seen;
+    info->grad_abs_max_seen = c->dwmax_seen;
+    info->forward_adc_full_scale = c->opt.adc_i_fs;
+    info->fully_ideal = c->fully_ideal ? 1 : 0;
+    info->kernel = c->kernel;
+  });
+}
+
+int xbs_core_gradient(xbs_core* c, double* dW, int64_t ld) {
+  return guard([&] {
+    if (!c || !dW || ld < c->g.K) fail(XBS_INVALID_ARGUMENT, "bad gradient buffer");
+    sync(c);
+    d2h_rowmajor_to_colmajor(c, c->d_dW, c->g.K, c->g.N, dW, ld);
+  });
+}
+
+int xbs_core_set_gradient(xbs_core* c, const double* dW, int64_t ld) {
+  return guard([&] {
+    if (!c || !dW || ld < c->g.K) fail(XBS_INVALID_ARGUMENT, "bad gradient buffer");
+    sync(c);
+    h2d_colmajor_to_rowmajor(c, dW, c->g.K, c->g.N, ld, c->d_dW);
+    c->have_grad = true;
+  });
+}
+
+int xbs_core_nonideal(xbs_core* c, int32_t s, int32_t p, int32_t t, double* out, int64_t ld) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    if (c->fully_ideal) fail(XBS_STATE_ERROR, "CrossbarCore: no non-ideal state for the ideal fast path");
+    if (s < 0 || s >= c->g.S || p < 0 || p > 1 || t < 0 || t >= c->g.GR * c->g.GC)
+      fail(XBS_INVALID_ARGUMENT, "nonideal: index out of range");  // std::vector::at -> out_of_range
+    if (!out || ld < c->g.tile_rows) fail(XBS_INVALID_ARGUMENT, "bad output buffer");
+    const int n = c->g.tile_rows * c->g.tile_cols;
+    double* d = nullptr;
+    ck(cudaMalloc(&d, size_t(n) * 8), "cudaMalloc");
+    xbs::launch_digits_to_g(c, s, p, t / c->g.GC, t % c->g.GC, d, c->stream);
+    sync(c);
+    std::vector<double> h(static_cast<size_t>(n));
+    ck(cudaMemcpy(h.data(), d, size_t(n) * 8, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d);
+    for (int j = 0; j < c->g.tile_cols; ++j)
+      for (int i = 0; i < c->g.tile_rows; ++i) out[int64_t(j) * ld + i] = h[size_t(j) * c->g.tile_rows + i];
+  });
+}
+
+int xbs_core_master(xbs_core* c, int32_t s, double* u, int64_t ld) {
+  return guard([&] {
+    if (!c || s < 0 || s >= c->g.S || !u || ld < c->g.Kp) fail(XBS_INVALID_ARGUMENT, "master: bad arguments");
+    sync(c);
+    d2h_rowmajor_to_colmajor(c, c->d_master + size_t(s) * c->g.Kp * c->g.Np, c->g.Kp, c->g.Np, u, ld);
+  });
+}
+
+int xbs_core_set_master(xbs_core* c, int32_t s, const double* u, int64_t ld) {
+  return guard([&] {
+    if (!c || s < 0 || s >= c->g.S || !u || ld < c->g.Kp) fail(XBS_INVALID_ARGUMENT, "set_master: bad arguments");
+    sync(c);
+    h2d_colmajor_to_rowmajor(c, u, c->g.Kp, c->g.Np, ld, c->d_master + size_t(s) * c->g.Kp * c->g.Np);
+    if (!c->fully_ideal) xbs::launch_regen_all(c, c->stream);
+    if (c->opt.engine == XBS_ENGINE_IDEAL) xbs::launch_implied(c, c->d_wimp, c->stream);
+    sync(c);
+  });
+}
+
+int xbs_core_implied_weights(xbs_core* c, double* w, int64_t ld) {
+  return guard([&] {
+    if (!c || !w || ld < c->g.K) fail(XBS_INVALID_ARGUMENT, "implied_weights: bad arguments");
+    double* d = nullptr;
+    ck(cudaMalloc(&d, size_t(c->g.K) * c->g.N * 8), "cudaMalloc");
+    xbs::launch_implied(c, d, c->stream);
+    sync(c);
+    d2h_rowmajor_to_colmajor(c, d, c->g.K, c->g.N, w, ld);
+    cudaFree(d);
+  });
+}
+
+int xbs_core_adc_counters(xbs_core* c, int64_t* exact_path, int64_t* conversions) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    sync(c);
+    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    if (exact_path) *exact_path = int64_t(c->h_sc->exact_path);
+    if (conversions) *conversions = int64_t(c->h_sc->conversions);
+  });
+}
+
+int xbs_core_select_kernel(xbs_core* c, int32_t kernel) {
+  return guard([&] {
+    if (!c || kernel < 0 || kernel > 1) fail(XBS_INVALID_ARGUMENT, "select_kernel: 0 (tcgen05) or 1 (SIMT)");
+    c->kernel = kernel;
+  });
+}
+
+void* xbs_core_stream(xbs_core* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// Internal declarations shared by the C-ABI implementation and the kernels.
+//
+// HBM layout (all per core, sized once at create, batch buffers grow on
+// demand) — DESIGN.md §"Data layout in HBM":
+//   master  u[s][i][j]        fp64, S x Kp x Np, row-major (j fastest)
+//   digits  D[s][p][tr][tc][d][r][c]  u8 radix-255 digits of the snapped
+//           conductance q = (d0 + 255 d1) + 65025 (d2 + 255 d3); each digit
+//           plane is an R x C row-major tile (R, C = tile dims rounded up to
+//           128; the internal pad holds 0 and never conducts)
+//   A_fwd   [dh][b*TPi + k][KI] u8 {0,1} (dh=0) / {0,255} (dh=1) input
+//           bit-planes, feature i at column (i / tile_rows) * R + i % tile_rows
+//   A_bwd   [dh][(b*TPe + k)*2 + phi][NI] u8 error bit-planes, phi = sign
+//   xcodes  [b][i] u16 activation codes; ecodes [b][j] i16 signed error codes
+//   dW      [i][j] fp64 (row-major K x N)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/xbarsim_b200.h"
+
+namespace xbs {
+
+// Snapped exactness grid (radix-255 variant): q <= kQMax.
+constexpr double kQMax = 4228250624.0;  // 65025^2 - 1
+
+struct Geo {
+  int K = 0, N = 0;                 // logical in / out features
+  int tile_rows = 0, tile_cols = 0; // logical tile (MappingSpec)
+  int GR = 0, GC = 0;               // grid_rows, grid_cols
+  int Kp = 0, Np = 0;               // reference padded dims
+  int R = 0, C = 0;                 // device tile dims (multiples of 128)
+  int KI = 0, NI = 0;               // GR*R, GC*C
+  int S = 0, db = 0, wb = 0;        // slices, device_bits, weight_bits
+  int Ti = 0, TPi = 0;              // act_bits, padded to a power of two
+  int Te = 0, TPe = 0;              // error_bits, padded
+  __host__ __device__ size_t plane_bytes() const { return size_t(R) * C; }
+  __host__ __device__ size_t tile_digit_offset(int s, int p, int tr, int tc, int d) const {
+    return ((((size_t(s) * 2 + p) * GR + tr) * GC + tc) * 4 + d) * plane_bytes();
+  }
+  __host__ __device__ size_t digits_bytes() const { return size_t(S) * 2 * GR * GC * 4 * plane_bytes(); }
+};
+
+// Conversion / regeneration parameters (mapping.cpp:28-58, aam.cpp:5-31).
+struct RegenP {
+  double g_min, g_max, range, sigma;
+  uint64_t vseed;
+  double r_row, r_col, r_source, r_sense;
+  int aam;     // 1: AAM conversion, 0: identity (ideal / zero-parasitic fcm)
+  int snap_e;  // grid exponent e
+};
+
+// update.cpp:43-88 + implied weights (mapping.cpp:70-81)
+struct UpdP {
+  double v, gamma, lr, factor;  // factor = (g_max-g_min)/layer_scale
+  double wfactor;               // implied-weight factor
+  uint64_t seed, iteration;
+  int linear;
+};
+
+// ADC (converters.cpp:70-88) on the snapped grid: I = n * 2^sh exactly.
+struct AdcP {
+  int passthrough;  // adc.bits == 0
+  int maxc;         // 2^bits - 1
+  int sh;           // log2(v_fs) - e
+  double i_fs;
+  double maxc_d;
+};
+
+// Device scalars (one struct per core, in HBM).
+struct DevScalars {
+  double se;                 // max|dy|
+  unsigned long long dwmax;  // bits of max|dW| (non-negative doubles order as u64)
+  unsigned long long wmax;   // bits of max|implied W|
+  unsigned long long wmax_in;// bits of max|W0| (layer scale)
+  int err_flag;              // 1: nonlinear_update range violation
+  int pad;
+  unsigned long long exact_path, conversions;
+};
+
+}  // namespace xbs
+
+struct xbs_core {
+  xbs_layer_options opt{};
+  std::vector<double> dac_tr, adc_tr;
+  xbs::Geo g;
+  xbs::RegenP rp{};
+  xbs::AdcP adc{};
+  cudaStream_t stream = nullptr;
+  int kernel = 0;  // 0 tcgen05, 1 SIMT
+  bool fully_ideal = false;
+  bool adc_scaled = false;  // k_out includes i_fs/(2^bits-1)
+  double layer_scale = 1.0, level_step = 0.0;
+  double k_out_fwd = 0.0;     // layers.cpp:272-281
+  double kb_F_over_vu = 0.0;  // backward: k = step_e * F / vu (* ifs_fac)
+  double F = 0.0, vu = 0.0, ifs_fac = 1.0, sx = 0.0, lev_e = 0.0, lev_a = 0.0;
+  // device buffers
+  uint8_t* d_digits = nullptr;
+  double* d_master = nullptr;
+  double* d_dW = nullptr;
+  double* d_wimp = nullptr;  // implied weights (fully-ideal fast path), K x N row-major
+  xbs::DevScalars* d_sc = nullptr;
+  xbs::DevScalars* h_sc = nullptr;  // pinned mirror
+  // batch-dependent
+  int64_t M_cap = 0;
+  uint8_t* d_Af = nullptr;   // 2 * rowsF * KI
+  uint8_t* d_Ab = nullptr;   // 2 * rowsB * NI
+  uint16_t* d_xcodes = nullptr;
+  int16_t* d_ecodes = nullptr;
+  double* d_io_in = nullptr;   // host-API staging (M x max(K,N))
+  double* d_io_out = nullptr;
+  int64_t io_cap = 0;
+  // state
+  int64_t M_fwd = 0;
+  bool have_forward = false, have_grad = false;
+  int64_t refreshes = 0;
+  double conversion_seconds = 0.0;
+  double wmax_seen = 0.0, dwmax_seen = 0.0;
+  int64_t exact_path = 0, conversions = 0;
+  // host mirrors for readback
+  std::vector<double> h_tmp;
+};
+
+namespace xbs {
+// kernels (launchers), all enqueue on `st`
+void launch_map_weights(const xbs_core* c, const double* d_W, cudaStream_t st);
+void launch_absmax(const double* d_x, int64_t n, unsigned long long* out_bits, cudaStream_t st);
+void launch_regen_all(const xbs_core* c, cudaStream_t st);
+void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st);
+void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream_t st);
+void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
+void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
+void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
+void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* d_dx, cudaStream_t st);
+void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
+void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st);
+void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);
+void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double* d_out, cudaStream_t st);
+// tcgen05 kernels (xbs_vmm_tc.cu); return false if the shape is not covered
+bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
+bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
+}  // namespace xbs

@@ -1,0 +1,535 @@
+// Bandwidth-bound kernels of the hot path (SIMT, sm_100a):
+//   map_weights   mapping.cpp:83-131      W -> per-slice signed master
+//   regen/update  update.cpp:43-88 fused with mapping.cpp:28-58 (variation),
+//                 aam.cpp:14-31 (AAM), the 2^-e snap and radix-255 digit
+//                 emission, implied-weight / |dW| maxima (layers.cpp:384-386)
+//   prep_x/_dy    tensor.cpp:8-51 quantisers + DAC bit-planes (layers.cpp:236-241,
+//                 316-331)
+//   dw            layers.cpp:304 as the exact integer contract
+//   vmm_simt      exact SIMT forward/backward (cross-check kernel; also the
+//                 pass-through-ADC path, layers.cpp:202)
+//   ideal         fully-ideal fast path (layers.cpp:226, 307)
+// Compiled with --fmad=false: every fp64 expression rounds exactly as the
+// reference's x86-64 code does (no contraction).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "xbs_internal.cuh"
+
+namespace xbs {
+
+// ------------------------------------------------------------------ rng.hpp
+__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t v) {
+  h += 0x9e3779b97f4a7c15ull + v;
+  h = (h ^ (h >> 30)) * 0xbf58476d1ce4e5b9ull;
+  h = (h ^ (h >> 27)) * 0x94d049bb133111ebull;
+  return h ^ (h >> 31);
+}
+__device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return mix64(mix64(mix64(mix64(0x9e3779b97f4a7c15ull ^ seed, a), b), c), 0);
+}
+__device__ __forceinline__ double to_unit(uint64_t x) { return double(x >> 11) * 0x1.0p-53; }
+// rng.hpp:31-36 (draws 1 and 2 of the keyed stream)
+__device__ __forceinline__ double rng_gaussian(uint64_t key) {
+  double u1 = 1.0 - to_unit(mix64(key, 1));
+  double u2 = to_unit(mix64(key, 2));
+  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925287 * u2);
+}
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
+  atomicMax(p, (unsigned long long)__double_as_longlong(v));
+}
+
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ------------------------------------------------- conductance conversion
+// mapping.cpp:39-58 + aam.cpp:14-31 + snap: one device (s, p, global padded
+// i, j) from its master value u.
+__device__ __forceinline__ uint32_t convert_device(const RegenP& rp, const Geo& g, double u, int s, int p,
+                                                   int i, int j) {
+  double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
+  if (rp.sigma != 0.0) {
+    const int64_t idx = int64_t(i) * g.Np + j;
+    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, uint64_t(idx), 0));
+    m = m > 1e-12 ? m : 1e-12;
+    gv = fmin(gv * m, rp.g_max);
+  }
+  if (rp.aam) {
+    const int r = i % g.tile_rows, c = j % g.tile_cols;
+    const double rpth = rp.r_source + double(c + 1) * rp.r_row + double(g.tile_rows - r) * rp.r_col + rp.r_sense;
+    if (gv == 0.0) gv = 0.0;
+    else if (rpth != 0.0) gv = 1.0 / (1.0 / gv + rpth);
+  }
+  return uint32_t(rint(ldexp(gv, rp.snap_e)));  // nearbyint, ties-to-even
+}
+
+__device__ __forceinline__ void store_digits(uint8_t* digits, const Geo& g, int s, int p, int i, int j,
+                                             uint32_t q) {
+  const int tr = i / g.tile_rows, r = i % g.tile_rows, tc = j / g.tile_cols, c = j % g.tile_cols;
+  const uint32_t lo = q % 65025u, hi = q / 65025u;
+  const size_t off = size_t(r) * g.C + c;
+  digits[g.tile_digit_offset(s, p, tr, tc, 0) + off] = uint8_t(lo % 255u);
+  digits[g.tile_digit_offset(s, p, tr, tc, 1) + off] = uint8_t(lo / 255u);
+  digits[g.tile_digit_offset(s, p, tr, tc, 2) + off] = uint8_t(hi % 255u);
+  digits[g.tile_digit_offset(s, p, tr, tc, 3) + off] = uint8_t(hi / 255u);
+}
+
+__device__ __forceinline__ uint32_t load_q(const uint8_t* digits, const Geo& g, int s, int p, int tr, int tc,
+                                           int r, int c) {
+  const size_t off = size_t(r) * g.C + c;
+  const size_t base = g.tile_digit_offset(s, p, tr, tc, 0) + off, ps = g.plane_bytes();
+  const uint32_t d0 = digits[base], d1 = digits[base + ps], d2 = digits[base + 2 * ps], d3 = digits[base + 3 * ps];
+  return (d0 + 255u * d1) + 65025u * (d2 + 255u * d3);
+}
+
+// -------------------------------------------------------------- map_weights
+__global__ void k_absmax(const double* __restrict__ x, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, fabs(x[k]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(out, m);
+}
+
+void launch_absmax(const double* d_x, int64_t n, unsigned long long* out_bits, cudaStream_t st) {
+  int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  if (blocks < 1) blocks = 1;
+  k_absmax<<<blocks, 256, 0, st>>>(d_x, n, out_bits);
+}
+
+// mapping.cpp:104-129.  W col-major K x N (ld = K); writes every padded
+// master element (0 outside the logical region).
+__global__ void k_map_weights(const double* __restrict__ W, Geo g, double scale, uint64_t q_levels,
+                              uint64_t d_levels, double level_step, double* __restrict__ master) {
+  const int64_t n = int64_t(g.Kp) * g.Np;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / g.Np), j = int(t % g.Np);
+    uint64_t q = 0;
+    double sign = 1.0;
+    if (i < g.K && j < g.N) {
+      const double w = W[int64_t(j) * g.K + i];
+      const double mag = fabs(w) / scale * double(q_levels);
+      q = uint64_t(llround(mag));
+      if (q > q_levels) q = q_levels;
+      sign = w < 0 ? -1.0 : 1.0;
+    }
+    for (int s = 0; s < g.S; ++s) {
+      const uint64_t digit = (q >> (s * g.db)) & d_levels;
+      master[(size_t(s) * g.Kp + i) * g.Np + j] = digit != 0 ? sign * (double(digit) * level_step) : 0.0;
+    }
+  }
+}
+
+void launch_map_weights(const xbs_core* c, const double* d_W, cudaStream_t st) {
+  const int64_t n = int64_t(c->g.Kp) * c->g.Np;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 32));
+  k_map_weights<<<blocks, 256, 0, st>>>(d_W, c->g, c->layer_scale, (uint64_t{1} << c->g.wb) - 1,
+                                        (uint64_t{1} << c->g.db) - 1, c->level_step, c->d_master);
+}
+
+// regenerate() (layers.cpp:129-179) over every padded device, all slices and
+// polarities.
+__global__ void k_regen_all(Geo g, RegenP rp, const double* __restrict__ master, uint8_t* __restrict__ digits) {
+  const int64_t n = int64_t(g.Kp) * g.Np;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / g.Np), j = int(t % g.Np);
+    for (int s = 0; s < g.S; ++s) {
+      const double u = master[(size_t(s) * g.Kp + i) * g.Np + j];
+      for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_device(rp, g, u, s, p, i, j));
+    }
+  }
+}
+
+void launch_regen_all(const xbs_core* c, cudaStream_t st) {
+  const int64_t n = int64_t(c->g.Kp) * c->g.Np;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 32));
+  k_regen_all<<<blocks, 256, 0, st>>>(c->g, c->rp, c->d_master, c->d_digits);
+}
+
+// ----------------------------------------------------------- apply_updates
+// update.cpp:43-88 for every slice of one logical weight (i, j), then the
+// regeneration of both polarities of every slice (layers.cpp:388) and the
+// implied-weight Horner (mapping.cpp:70-81) for the |W| statistic.
+__global__ void k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW, double* __restrict__ master,
+                         uint8_t* __restrict__ digits, DevScalars* sc) {
+  const int64_t n = int64_t(g.K) * g.N;
+  double wmax = 0.0, dwmax = 0.0;
+  const double range = rp.range;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / g.N), j = int(t % g.N);
+    const double dw = dW[t];
+    dwmax = fmax(dwmax, fabs(dw));
+    const double dg = dw * up.factor;  // scale_gradient (update.cpp:16-24)
+    double acc = 0.0;
+    for (int s = g.S - 1; s >= 0; --s) {
+      double* up_ = &master[(size_t(s) * g.Kp + i) * g.Np + j];
+      const double ui = *up_;
+      double du = dg;
+      if (!up.linear && dg != 0.0) {
+        const bool pos_active = ui > 0.0 || (ui == 0.0 && dg < 0.0);
+        const double dev_arg = pos_active ? -dg : dg;
+        const double gg = rp.g_min + fabs(ui);
+        if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
+        const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
+        const double nl = dev_arg * exp(-up.v * x);
+        du = pos_active ? -nl : nl;
+      }
+      double noise = 0.0;
+      if (up.gamma != 0.0 && dg != 0.0) {
+        const double sigma = up.gamma * sqrt(range * fabs(dg));
+        if (sigma != 0.0)
+          noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s), uint64_t(t)));
+      }
+      double nu = ui - up.lr * (du + noise);
+      if (nu > range) nu = range;
+      if (nu < -range) nu = -range;
+      *up_ = nu;
+      for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_device(rp, g, nu, s, p, i, j));
+      acc = acc * double(1u << g.db) + nu;
+    }
+    wmax = fmax(wmax, fabs(up.wfactor * acc));
+  }
+  wmax = warp_max(wmax);
+  dwmax = warp_max(dwmax);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(&sc->wmax, wmax);
+    atomic_max_pos(&sc->dwmax, dwmax);
+  }
+}
+
+void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st) {
+  const int64_t n = int64_t(c->g.K) * c->g.N;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+  k_update<<<blocks, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
+}
+
+// implied_weights() (mapping.cpp:70-81) -> K x N row-major
+__global__ void k_implied(Geo g, double wfactor, const double* __restrict__ master, double* __restrict__ out) {
+  const int64_t n = int64_t(g.K) * g.N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / g.N), j = int(t % g.N);
+    double acc = 0.0;
+    for (int s = g.S - 1; s >= 0; --s) acc = acc * double(1u << g.db) + master[(size_t(s) * g.Kp + i) * g.Np + j];
+    out[t] = wfactor * acc;
+  }
+}
+
+void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st) {
+  const int64_t n = int64_t(c->g.K) * c->g.N;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+  const double levels = double((uint64_t{1} << c->g.wb) - 1), sl = double((uint64_t{1} << c->g.db) - 1);
+  const double wf = (c->layer_scale / (c->rp.g_max - c->rp.g_min)) * (sl / levels);
+  k_implied<<<blocks, 256, 0, st>>>(c->g, wf, c->d_master, d_out);
+}
+
+// non-ideal tile readback: snapped conductance q * 2^-e, tile_rows x tile_cols
+// column-major.
+__global__ void k_digits_to_g(Geo g, int e, const uint8_t* __restrict__ digits, int s, int p, int tr, int tc,
+                              double* out) {
+  const int n = g.tile_rows * g.tile_cols;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % g.tile_rows, c = t / g.tile_rows;
+    out[t] = ldexp(double(load_q(digits, g, s, p, tr, tc, r, c)), -e);
+  }
+}
+
+void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double* d_out, cudaStream_t st) {
+  k_digits_to_g<<<64, 256, 0, st>>>(c->g, c->rp.snap_e, c->d_digits, s, p, tr, tc, d_out);
+}
+
+// ------------------------------------------------------------------ prep_x
+// quantize_unsigned_codes (tensor.cpp:8-25) + DAC bit planes (layers.cpp:236-241)
+// x: M x K column-major (ld = M).  One thread per (b, 16-column chunk of the
+// device-padded K axis); writes codes and both A planes (bits, 255*bits).
+__global__ void k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF, double step, double levels,
+                         uint16_t* __restrict__ codes, uint8_t* __restrict__ A) {
+  const int chunks = g.KI / 16;
+  const int64_t n = M * chunks;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int ch = int(t / M);
+    uint32_t cv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int col = ch * 16 + q;
+      const int tr = col / g.R, r = col % g.R;
+      const int i = tr * g.tile_rows + r;
+      uint32_t code = 0;
+      if (r < g.tile_rows && i < g.K) {
+        double v = double(llround(x[int64_t(i) * M + b] / step));
+        if (v < 0) v = 0;
+        if (v > levels) v = levels;
+        code = uint32_t(v);
+        codes[b * g.K + i] = uint16_t(code);
+      }
+      cv[q] = code;
+    }
+    for (int k = 0; k < g.TPi; ++k) {
+      uint32_t w0[4], w1[4];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a |= ((cv[q4 * 4 + q] >> k) & 1u) << (8 * q);
+        w0[q4] = a;
+        w1[q4] = a * 255u;
+      }
+      const int64_t row = b * g.TPi + k;
+      uint4* p0 = reinterpret_cast<uint4*>(A + row * g.KI + ch * 16);
+      uint4* p1 = reinterpret_cast<uint4*>(A + (rowsF + row) * g.KI + ch * 16);
+      *p0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+      *p1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    }
+  }
+}
+
+void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st) {
+  const int64_t rowsF = ((M * c->g.TPi + 127) / 128) * 128;
+  // zero the M-padding rows once per call (rows [M*TPi, rowsF))
+  const int64_t pad0 = M * c->g.TPi;
+  if (rowsF > pad0) {
+    cudaMemsetAsync(c->d_Af + pad0 * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
+    cudaMemsetAsync(c->d_Af + (rowsF + pad0) * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
+  }
+  const int64_t n = M * (c->g.KI / 16);
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  const double levels = double((1 << c->opt.act_bits) - 1);
+  k_prep_x<<<blocks, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+                                    c->d_Af);
+}
+
+// ----------------------------------------------------------------- prep_dy
+// se = max|dy| (layers.cpp:298), quantize_signed_codes (tensor.cpp:33-51),
+// plus/minus planes (layers.cpp:316-331).  Row (b*TPe + k)*2 + phi, phi=0
+// plus, phi=1 minus.
+__global__ void k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB, double levels,
+                          const DevScalars* __restrict__ sc, int16_t* __restrict__ ecodes, uint8_t* __restrict__ A) {
+  const double se = sc->se;
+  const double step = se / levels;
+  const int chunks = g.NI / 16;
+  const int64_t n = M * chunks;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int ch = int(t / M);
+    uint32_t pv[16], mv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int col = ch * 16 + q;
+      const int tc = col / g.C, c = col % g.C;
+      const int j = tc * g.tile_cols + c;
+      int sm = 0;
+      if (c < g.tile_cols && j < g.N) {
+        if (se > 0) {
+          const double v = dy[int64_t(j) * M + b];
+          double qq = double(llround(fabs(v) / step));
+          if (qq > levels) qq = levels;
+          const int mag = int(qq);
+          sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
+        }
+        ecodes[b * g.N + j] = int16_t(sm);
+      }
+      pv[q] = sm > 0 ? uint32_t(sm) : 0u;
+      mv[q] = sm < 0 ? uint32_t(-sm) : 0u;
+    }
+    for (int k = 0; k < g.TPe; ++k)
+      for (int phi = 0; phi < 2; ++phi) {
+        const uint32_t* src = phi ? mv : pv;
+        uint32_t w0[4], w1[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint32_t a = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a |= ((src[q4 * 4 + q] >> k) & 1u) << (8 * q);
+          w0[q4] = a;
+          w1[q4] = a * 255u;
+        }
+        const int64_t row = (b * g.TPe + k) * 2 + phi;
+        *reinterpret_cast<uint4*>(A + row * g.NI + ch * 16) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(A + (rowsB + row) * g.NI + ch * 16) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+      }
+  }
+}
+
+__global__ void k_absmax_to_se(DevScalars* sc, const unsigned long long* bits) {
+  sc->se = __longlong_as_double((long long)*bits);
+}
+
+void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream_t st) {
+  cudaMemsetAsync(&c->d_sc->wmax_in, 0, sizeof(unsigned long long), st);
+  launch_absmax(d_dy, M * c->g.N, &c->d_sc->wmax_in, st);
+  k_absmax_to_se<<<1, 1, 0, st>>>(c->d_sc, &c->d_sc->wmax_in);
+  const int64_t rowsB = ((M * c->g.TPe * 2 + 127) / 128) * 128;
+  const int64_t pad0 = M * c->g.TPe * 2;
+  if (rowsB > pad0) {
+    cudaMemsetAsync(c->d_Ab + pad0 * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
+    cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
+  }
+  const int64_t n = M * (c->g.NI / 16);
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  k_prep_dy<<<blocks, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
+                                     c->d_ecodes, c->d_Ab);
+}
+
+// ---------------------------------------------------------------------- dW
+// Exact integer outer product: dW = ((S * sx) * step_e) / gd.
+__global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const uint16_t* __restrict__ xc,
+                     const int16_t* __restrict__ ec, const DevScalars* __restrict__ sc, double* __restrict__ dW) {
+  const double se = sc->se;
+  const double step_e = se > 0 ? se / lev_e : 0.0;
+  const int64_t n = int64_t(g.K) * g.N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / g.N), j = int(t % g.N);
+    int64_t S = 0;
+    for (int64_t b = 0; b < M; ++b) S += int64_t(xc[b * g.K + i]) * int64_t(ec[b * g.N + j]);
+    dW[t] = ((double(S) * sx) * step_e) / gd;
+  }
+}
+
+void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) {
+  const int64_t n = int64_t(c->g.K) * c->g.N;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+  k_dw<<<blocks, 256, 0, st>>>(c->g, M, c->sx, c->lev_e, grad_divisor, c->d_xcodes, c->d_ecodes, c->d_sc, c->d_dW);
+}
+
+// --------------------------------------------------------------- SIMT VMM
+__device__ __forceinline__ int64_t adc_apply(const AdcP& a, int64_t n, unsigned long long* conv) {
+  if (a.passthrough) return n;
+  const double I = ldexp(double(n), a.sh);
+  const double scaled = I / a.i_fs * a.maxc_d;
+  if (scaled >= a.maxc_d) return a.maxc;
+  return llround(scaled);
+}
+
+// forward (layers.cpp:246-283): one thread per (b, logical output column).
+__global__ void k_fwd_simt(Geo g, AdcP a, int64_t M, int64_t rowsF, const uint8_t* __restrict__ A,
+                           const uint8_t* __restrict__ digits, double k_out, double* __restrict__ y) {
+  const int64_t n = M * g.N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int col = int(t / M);
+    const int tc = col / g.tile_cols, c = col % g.tile_cols;
+    int64_t total = 0;
+    for (int k = 0; k < g.Ti; ++k) {
+      const uint8_t* arow = A + (b * g.TPi + k) * g.KI;
+      for (int tr = 0; tr < g.GR; ++tr)
+        for (int s = 0; s < g.S; ++s)
+          for (int p = 0; p < 2; ++p) {
+            int64_t nn = 0;
+            for (int r = 0; r < g.tile_rows; ++r)
+              if (arow[tr * g.R + r]) nn += load_q(digits, g, s, p, tr, tc, r, c);
+            const int64_t v = adc_apply(a, nn, nullptr);
+            const int64_t w = (v << (s * g.db)) << k;
+            total += p == 0 ? w : -w;
+          }
+    }
+    y[int64_t(col) * M + b] = a.passthrough ? ldexp(double(total), a.sh) * k_out : double(total) * k_out;
+  }
+}
+
+void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
+  const int64_t n = M * c->g.N;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  const int64_t rowsF = ((M * c->g.TPi + 127) / 128) * 128;
+  k_fwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, rowsF, c->d_Af, c->d_digits, c->k_out_fwd, d_y);
+}
+
+// backward (layers.cpp:339-379): one thread per (b, logical input row i).
+__global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__ A, const uint8_t* __restrict__ digits,
+                           double F_over_vu, double ifs_fac, int adc_scaled, double lev_e,
+                           const DevScalars* __restrict__ sc, double* __restrict__ dx) {
+  const double se = sc->se;
+  const double step_e = se > 0 ? se / lev_e : 0.0;
+  double k_out = step_e * F_over_vu;
+  if (adc_scaled) k_out *= ifs_fac;
+  const int64_t n = M * g.K;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int i = int(t / M);
+    const int tr = i / g.tile_rows, r = i % g.tile_rows;
+    int64_t total = 0;
+    if (se > 0)
+      for (int k = 0; k < g.Te; ++k) {
+        const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NI;
+        const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NI;
+        for (int tc = 0; tc < g.GC; ++tc)
+          for (int s = 0; s < g.S; ++s) {
+            int64_t pp = 0, mn = 0, pn = 0, mp = 0;
+            for (int c = 0; c < g.tile_cols; ++c) {
+              const int64_t qp = load_q(digits, g, s, 0, tr, tc, r, c), qn = load_q(digits, g, s, 1, tr, tc, r, c);
+              if (ap[tc * g.C + c]) { pp += qp; pn += qn; }
+              if (am[tc * g.C + c]) { mn += qn; mp += qp; }
+            }
+            const int64_t v = adc_apply(a, pp, nullptr) + adc_apply(a, mn, nullptr) - adc_apply(a, pn, nullptr) -
+                              adc_apply(a, mp, nullptr);
+            total += (v << (s * g.db)) << k;
+          }
+      }
+    dx[int64_t(i) * M + b] = a.passthrough ? ldexp(double(total), a.sh) * k_out : double(total) * k_out;
+  }
+}
+
+void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
+  const int64_t n = M * c->g.K;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  k_bwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, c->d_Ab, c->d_digits, c->F / c->vu, c->ifs_fac,
+                                      c->adc_scaled ? 1 : 0, c->lev_e, c->d_sc, d_dx);
+}
+
+// ------------------------------------------------------ fully-ideal path
+// y = x_values * wimp (layers.cpp:226), ascending k, unfused mul/add.
+__global__ void k_fwd_ideal(Geo g, int64_t M, double sx, const uint16_t* __restrict__ xc,
+                            const double* __restrict__ w, double* __restrict__ y) {
+  const int64_t n = M * g.N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int j = int(t / M);
+    double a = 0.0;
+    for (int k = 0; k < g.K; ++k) a = a + (double(xc[b * g.K + k]) * sx) * w[int64_t(k) * g.N + j];
+    y[int64_t(j) * M + b] = a;
+  }
+}
+
+void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
+  const int64_t n = M * c->g.N;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  k_fwd_ideal<<<blocks, 128, 0, st>>>(c->g, M, c->sx, c->d_xcodes, c->d_wimp, d_y);
+}
+
+// dx = dy_q * wimp^T (layers.cpp:307), dy_q = (sign*mag)*step_e (layers.cpp:301-302)
+__global__ void k_bwd_ideal(Geo g, int64_t M, double lev_e, const int16_t* __restrict__ ec,
+                            const DevScalars* __restrict__ sc, const double* __restrict__ w, double* __restrict__ dx) {
+  const double se = sc->se;
+  const double step_e = se > 0 ? se / lev_e : 0.0;
+  const int64_t n = M * g.K;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int i = int(t / M);
+    double a = 0.0;
+    for (int j = 0; j < g.N; ++j) {
+      const int e = ec[b * g.N + j];
+      const int sg = e > 0 ? 1 : (e < 0 ? -1 : 0);
+      const double dq = double(sg) * double(e < 0 ? -e : e) * step_e;
+      a = a + dq * w[int64_t(i) * g.N + j];
+    }
+    dx[int64_t(i) * M + b] = a;
+  }
+}
+
+void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* d_dx, cudaStream_t st) {
+  (void)d_dy;
+  const int64_t n = M * c->g.K;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  k_bwd_ideal<<<blocks, 128, 0, st>>>(c->g, M, c->lev_e, c->d_ecodes, c->d_sc, c->d_wimp, d_dx);
+}
+
+}  // namespace xbs

@@ -1,0 +1,464 @@
+"""Python mirror of the reference's crossbar-layer operator API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/xbarsim/layers.hpp:19-152 (CrossbarLayerOptions,
+CrossbarCore, Layer, CrossbarLinear) and the spec structs they aggregate
+(mapping.hpp:14-25, crossbar.hpp:17-40, converters.hpp:14-45, update.hpp:13-23).
+Matrices are numpy float64 arrays, logically (rows, cols) like Eigen::MatrixXd.
+
+Every compute call goes through ``libxbarsim_b200.so`` (include/xbarsim_b200.h):
+there is no CPU fallback; importing this module on a machine without the built
+library, or calling it without a GPU, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import enum
+import os
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libxbarsim_b200.so")
+
+
+# ----------------------------------------------------------------- errors.hpp
+class XbarsimError(RuntimeError):
+    pass
+
+
+class StateError(XbarsimError):
+    """errors.hpp:38-42"""
+
+
+class ConfigError(XbarsimError):
+    """errors.hpp:44-47 (also raised for configurations outside this path)"""
+
+
+class ConvergenceError(XbarsimError):
+    pass
+
+
+class StaleCacheError(XbarsimError):
+    pass
+
+
+class DegenerateCircuitError(XbarsimError):
+    pass
+
+
+class UnsupportedConfigError(ConfigError):
+    """A valid reference configuration this B200 path does not evaluate."""
+
+
+class CudaError(StateError):
+    pass
+
+
+_STATUS = {
+    1: ValueError,  # std::invalid_argument
+    2: StateError,
+    3: ConfigError,
+    4: ConvergenceError,
+    5: StaleCacheError,
+    6: DegenerateCircuitError,
+    7: UnsupportedConfigError,
+    8: CudaError,
+    9: XbarsimError,
+}
+
+
+class EngineKind(enum.IntEnum):
+    """engine.hpp:15-21"""
+
+    ideal = 0
+    oracle = 1
+    fcm = 2
+    aam = 3
+    interp_fcm = 4
+
+
+class Polarity(enum.IntEnum):
+    pos = 0
+    neg = 1
+
+
+# ------------------------------------------------------------- option specs
+@dataclasses.dataclass
+class MappingSpec:
+    weight_bits: int = 8
+    device_bits: int = 2
+    tile_rows: int = 64
+    tile_cols: int = 64
+    variation_sigma: float = 0.0
+    seed: int = 0
+    w_max: float = 0.0
+
+    def num_slices(self) -> int:
+        return self.weight_bits // self.device_bits
+
+
+@dataclasses.dataclass
+class CrossbarConfig:
+    rows: int = 64
+    cols: int = 64
+    r_row: float = 1.0
+    r_col: float = 4.6
+    r_source: float = 0.0
+    r_sense: float = 0.0
+    g_min: float = 1e-6
+    g_max: float = 1e-5
+    v_fs: float = 1.0
+
+
+@dataclasses.dataclass
+class DacSpec:
+    bits: int = 1
+    v_fs: float = 1.0
+    transfer: List[float] = dataclasses.field(default_factory=list)
+    stream_bits: int = 1
+
+
+@dataclasses.dataclass
+class AdcSpec:
+    bits: int = 8
+    i_fs: float = 0.0
+    transfer: List[float] = dataclasses.field(default_factory=list)
+    clip_percentile: float = 0.999
+
+
+@dataclasses.dataclass
+class UpdateSpec:
+    v: float = 0.0
+    gamma: float = 0.0
+    lr: float = 0.01
+    seed: int = 0
+    layer_scale: float = 0.0
+
+
+@dataclasses.dataclass
+class CrossbarLayerOptions:
+    map: MappingSpec = dataclasses.field(default_factory=MappingSpec)
+    crossbar: CrossbarConfig = dataclasses.field(default_factory=CrossbarConfig)
+    dac: DacSpec = dataclasses.field(default_factory=DacSpec)
+    adc: AdcSpec = dataclasses.field(default_factory=AdcSpec)
+    update: UpdateSpec = dataclasses.field(default_factory=UpdateSpec)
+    engine: EngineKind = EngineKind.fcm
+    interp_base: EngineKind = EngineKind.fcm
+    interp_interval: int = 10
+    fcm_tol: float = 1e-6
+    fcm_max_iter: int = 1000
+    act_bits: int = 8
+    act_full_scale: float = 1.0
+    error_bits: int = 8
+    adc_cal_batches: int = 20
+    threads: int = 1
+
+    def to_c(self) -> "CLayerOptions":
+        """Flat POD (include/xbarsim_b200.h xbs_layer_options)."""
+        o = CLayerOptions()
+        m, x, d, a, u = self.map, self.crossbar, self.dac, self.adc, self.update
+        o.weight_bits, o.device_bits, o.tile_rows, o.tile_cols = m.weight_bits, m.device_bits, m.tile_rows, m.tile_cols
+        o.variation_sigma, o.variation_seed, o.w_max = m.variation_sigma, m.seed, m.w_max
+        o.xbar_rows, o.xbar_cols = x.rows, x.cols
+        o.r_row, o.r_col, o.r_source, o.r_sense = x.r_row, x.r_col, x.r_source, x.r_sense
+        o.g_min, o.g_max, o.v_fs = x.g_min, x.g_max, x.v_fs
+        o.dac_bits, o.dac_stream_bits, o.dac_v_fs = d.bits, d.stream_bits, d.v_fs
+        o._keep = []
+        if d.transfer:
+            arr = (ctypes.c_double * len(d.transfer))(*d.transfer)
+            o._keep.append(arr)
+            o.dac_transfer, o.dac_transfer_len = ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)), len(d.transfer)
+        o.adc_bits, o.adc_i_fs, o.adc_clip_percentile = a.bits, a.i_fs, a.clip_percentile
+        if a.transfer:
+            arr = (ctypes.c_double * len(a.transfer))(*a.transfer)
+            o._keep.append(arr)
+            o.adc_transfer, o.adc_transfer_len = ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)), len(a.transfer)
+        o.upd_v, o.upd_gamma, o.upd_lr, o.upd_seed, o.upd_layer_scale = u.v, u.gamma, u.lr, u.seed, u.layer_scale
+        o.engine, o.interp_base, o.interp_interval = int(self.engine), int(self.interp_base), self.interp_interval
+        o.fcm_tol, o.fcm_max_iter = self.fcm_tol, self.fcm_max_iter
+        o.act_bits, o.act_full_scale, o.error_bits = self.act_bits, self.act_full_scale, self.error_bits
+        o.adc_cal_batches, o.threads = self.adc_cal_batches, self.threads
+        return o
+
+
+class CLayerOptions(ctypes.Structure):
+    _fields_ = [
+        ("weight_bits", ctypes.c_int32), ("device_bits", ctypes.c_int32),
+        ("tile_rows", ctypes.c_int32), ("tile_cols", ctypes.c_int32),
+        ("variation_sigma", ctypes.c_double), ("variation_seed", ctypes.c_uint64), ("w_max", ctypes.c_double),
+        ("xbar_rows", ctypes.c_int32), ("xbar_cols", ctypes.c_int32),
+        ("r_row", ctypes.c_double), ("r_col", ctypes.c_double), ("r_source", ctypes.c_double),
+        ("r_sense", ctypes.c_double), ("g_min", ctypes.c_double), ("g_max", ctypes.c_double),
+        ("v_fs", ctypes.c_double),
+        ("dac_bits", ctypes.c_int32), ("dac_stream_bits", ctypes.c_int32), ("dac_v_fs", ctypes.c_double),
+        ("dac_transfer", ctypes.POINTER(ctypes.c_double)), ("dac_transfer_len", ctypes.c_int32),
+        ("adc_bits", ctypes.c_int32), ("adc_i_fs", ctypes.c_double),
+        ("adc_transfer", ctypes.POINTER(ctypes.c_double)), ("adc_transfer_len", ctypes.c_int32),
+        ("adc_clip_percentile", ctypes.c_double),
+        ("upd_v", ctypes.c_double), ("upd_gamma", ctypes.c_double), ("upd_lr", ctypes.c_double),
+        ("upd_seed", ctypes.c_uint64), ("upd_layer_scale", ctypes.c_double),
+        ("engine", ctypes.c_int32), ("interp_base", ctypes.c_int32), ("interp_interval", ctypes.c_int32),
+        ("fcm_tol", ctypes.c_double), ("fcm_max_iter", ctypes.c_int32),
+        ("act_bits", ctypes.c_int32), ("act_full_scale", ctypes.c_double),
+        ("error_bits", ctypes.c_int32), ("adc_cal_batches", ctypes.c_int32), ("threads", ctypes.c_int32),
+    ]
+
+
+class CoreInfo(ctypes.Structure):
+    _fields_ = [
+        ("in_features", ctypes.c_int32), ("out_features", ctypes.c_int32),
+        ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
+        ("padded_rows", ctypes.c_int32), ("padded_cols", ctypes.c_int32),
+        ("num_slices", ctypes.c_int32), ("snap_exponent", ctypes.c_int32),
+        ("layer_scale", ctypes.c_double), ("level_step", ctypes.c_double),
+        ("refresh_count", ctypes.c_int64), ("conversion_seconds", ctypes.c_double),
+        ("weight_abs_max_seen", ctypes.c_double), ("grad_abs_max_seen", ctypes.c_double),
+        ("forward_adc_full_scale", ctypes.c_double), ("fully_ideal", ctypes.c_int32), ("kernel", ctypes.c_int32),
+    ]
+
+
+# Exported symbols (name -> (restype, argtypes)); tests check every one of
+# them against include/xbarsim_b200.h.
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+SYMBOLS = {
+    "xbs_abi_version": (ctypes.c_int32, []),
+    "xbs_last_error": (ctypes.c_char_p, []),
+    "xbs_options_init": (None, [ctypes.POINTER(CLayerOptions)]),
+    "xbs_core_create": (ctypes.c_int, [ctypes.POINTER(CLayerOptions), _D, _I64, _I64, _I64, ctypes.POINTER(_P)]),
+    "xbs_core_destroy": (None, [_P]),
+    "xbs_core_forward": (ctypes.c_int, [_P, _D, _I64, _I64, ctypes.c_int32, _D, _I64]),
+    "xbs_core_backward": (ctypes.c_int, [_P, _D, _I64, _I64, ctypes.c_double, _D, _I64]),
+    "xbs_core_apply_updates": (ctypes.c_int, [_P, ctypes.c_uint64]),
+    "xbs_core_forward_device": (ctypes.c_int, [_P, _P, _I64, ctypes.c_int32, _P]),
+    "xbs_core_backward_device": (ctypes.c_int, [_P, _P, _I64, ctypes.c_double, _P]),
+    "xbs_core_apply_updates_device": (ctypes.c_int, [_P, ctypes.c_uint64]),
+    "xbs_core_synchronize": (ctypes.c_int, [_P]),
+    "xbs_core_get_info": (ctypes.c_int, [_P, ctypes.POINTER(CoreInfo)]),
+    "xbs_core_gradient": (ctypes.c_int, [_P, _D, _I64]),
+    "xbs_core_set_gradient": (ctypes.c_int, [_P, _D, _I64]),
+    "xbs_core_nonideal": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _D, _I64]),
+    "xbs_core_master": (ctypes.c_int, [_P, ctypes.c_int32, _D, _I64]),
+    "xbs_core_set_master": (ctypes.c_int, [_P, ctypes.c_int32, _D, _I64]),
+    "xbs_core_implied_weights": (ctypes.c_int, [_P, _D, _I64]),
+    "xbs_core_adc_counters": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "xbs_core_select_kernel": (ctypes.c_int, [_P, ctypes.c_int32]),
+    "xbs_core_stream": (_P, [_P]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Loads the C-ABI library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"libxbarsim_b200.so not built ({path}); run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SYMBOLS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load_library().xbs_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, XbarsimError)(msg)
+
+
+def _fortran(a: np.ndarray) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+# --------------------------------------------------------------- operators
+class CrossbarCore:
+    """xbarsim::nn::CrossbarCore (layers.hpp:49-111) on one B200."""
+
+    def __init__(self, W0: np.ndarray, opt: CrossbarLayerOptions):
+        lib = load_library()
+        W = _fortran(W0)
+        if W.ndim != 2:
+            raise ValueError("CrossbarCore: W0 must be a matrix")
+        self._opt = opt
+        self._copt = opt.to_c()
+        h = ctypes.c_void_p()
+        _check(lib.xbs_core_create(ctypes.byref(self._copt), _ptr(W), W.shape[0], W.shape[1], max(1, W.shape[0]),
+                                   ctypes.byref(h)))
+        self._h = h
+        self._K, self._N = W.shape
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.xbs_core_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def forward(self, x: np.ndarray, training: bool) -> np.ndarray:
+        x = _fortran(x)
+        if x.ndim != 2 or x.shape[1] != self._K:
+            raise ValueError("CrossbarCore::forward: feature count mismatch")
+        M = x.shape[0]
+        y = np.zeros((M, self._N), dtype=np.float64, order="F")
+        _check(load_library().xbs_core_forward(self._h, _ptr(x), M, max(1, M), int(bool(training)), _ptr(y),
+                                               max(1, M)))
+        return y
+
+    def backward(self, dy: np.ndarray, grad_divisor: float) -> np.ndarray:
+        dy = _fortran(dy)
+        if dy.ndim != 2 or dy.shape[1] != self._N:
+            raise ValueError("CrossbarCore::backward: gradient shape mismatch")
+        M = dy.shape[0]
+        dx = np.zeros((M, self._K), dtype=np.float64, order="F")
+        _check(load_library().xbs_core_backward(self._h, _ptr(dy), M, max(1, M), float(grad_divisor), _ptr(dx),
+                                                max(1, M)))
+        return dx
+
+    def apply_updates(self, iteration: int) -> None:
+        _check(load_library().xbs_core_apply_updates(self._h, int(iteration)))
+
+    def in_features(self) -> int:
+        return self._K
+
+    def out_features(self) -> int:
+        return self._N
+
+    def info(self) -> CoreInfo:
+        inf = CoreInfo()
+        _check(load_library().xbs_core_get_info(self._h, ctypes.byref(inf)))
+        return inf
+
+    def gradient(self) -> np.ndarray:
+        g = np.zeros((self._K, self._N), order="F")
+        _check(load_library().xbs_core_gradient(self._h, _ptr(g), self._K))
+        return g
+
+    def set_gradient(self, dW: np.ndarray) -> None:
+        dW = _fortran(dW)
+        _check(load_library().xbs_core_set_gradient(self._h, _ptr(dW), self._K))
+
+    def refresh_count(self) -> int:
+        return int(self.info().refresh_count)
+
+    def conversion_seconds(self) -> float:
+        return float(self.info().conversion_seconds)
+
+    def weight_abs_max_seen(self) -> float:
+        return float(self.info().weight_abs_max_seen)
+
+    def grad_abs_max_seen(self) -> float:
+        return float(self.info().grad_abs_max_seen)
+
+    def forward_adc_full_scale(self) -> float:
+        return float(self.info().forward_adc_full_scale)
+
+    def nonideal(self, slice_: int, p: Polarity, tile: int) -> np.ndarray:
+        o = self._opt.map
+        g = np.zeros((o.tile_rows, o.tile_cols), order="F")
+        _check(load_library().xbs_core_nonideal(self._h, slice_, int(p), tile, _ptr(g), o.tile_rows))
+        return g
+
+    def master_diff(self, slice_: int) -> np.ndarray:
+        inf = self.info()
+        u = np.zeros((inf.padded_rows, inf.padded_cols), order="F")
+        _check(load_library().xbs_core_master(self._h, slice_, _ptr(u), inf.padded_rows))
+        return u
+
+    def set_master_diff(self, slice_: int, u: np.ndarray) -> None:
+        u = _fortran(u)
+        _check(load_library().xbs_core_set_master(self._h, slice_, _ptr(u), u.shape[0]))
+
+    def implied_weights(self) -> np.ndarray:
+        w = np.zeros((self._K, self._N), order="F")
+        _check(load_library().xbs_core_implied_weights(self._h, _ptr(w), self._K))
+        return w
+
+    def adc_counters(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(load_library().xbs_core_adc_counters(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def select_kernel(self, kernel: int) -> None:
+        _check(load_library().xbs_core_select_kernel(self._h, int(kernel)))
+
+    # device-resident entry points (pointers are CUDA device addresses)
+    def forward_device(self, d_x: int, M: int, training: bool, d_y: int) -> None:
+        _check(load_library().xbs_core_forward_device(self._h, d_x, M, int(bool(training)), d_y))
+
+    def backward_device(self, d_dy: int, M: int, grad_divisor: float, d_dx: int) -> None:
+        _check(load_library().xbs_core_backward_device(self._h, d_dy, M, float(grad_divisor), d_dx))
+
+    def apply_updates_device(self, iteration: int) -> None:
+        _check(load_library().xbs_core_apply_updates_device(self._h, int(iteration)))
+
+    def synchronize(self) -> None:
+        _check(load_library().xbs_core_synchronize(self._h))
+
+    def stream(self) -> int:
+        return load_library().xbs_core_stream(self._h) or 0
+
+
+@dataclasses.dataclass
+class Tensor:
+    """tensor.hpp:13-21"""
+
+    values: np.ndarray
+    dims: List[int] = dataclasses.field(default_factory=list)
+    bits: int = 0
+    full_scale: float = 0.0
+
+
+class Layer:
+    """layers.hpp:113-121"""
+
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        raise NotImplementedError
+
+    def backward(self, dy: Tensor) -> Tensor:
+        raise NotImplementedError
+
+    def apply_updates(self, iteration: int) -> None:
+        pass
+
+    def core(self) -> Optional[CrossbarCore]:
+        return None
+
+    def name(self) -> str:
+        raise NotImplementedError
+
+
+class CrossbarLinear(Layer):
+    """layers.cpp:393-413"""
+
+    def __init__(self, W0: np.ndarray, opt: CrossbarLayerOptions):
+        self._core = CrossbarCore(W0, opt)
+
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        return Tensor(self._core.forward(x.values, training), [self._core.out_features()])
+
+    def backward(self, dy: Tensor) -> Tensor:
+        return Tensor(self._core.backward(dy.values, 1.0), [self._core.in_features()])
+
+    def apply_updates(self, iteration: int) -> None:
+        self._core.apply_updates(iteration)
+
+    def core(self) -> CrossbarCore:
+        return self._core
+
+    def name(self) -> str:
+        return "linear"
