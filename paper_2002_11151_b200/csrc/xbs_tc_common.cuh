@@ -1,0 +1,168 @@
+// sm_100a building blocks for the tcgen05 crossbar kernels: mbarriers, TMA
+// (cp.async.bulk.tensor), UMMA shared-memory / instruction descriptors,
+// tcgen05.mma kind::i8, TMEM alloc / ld, and the fp32 ADC epilogue helpers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace xbs {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ------------------------------------------------------------- mbarriers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// ------------------------------------------------------------------- TMA
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// ------------------------------------------------------- UMMA descriptors
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start >> 4
+// [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46), version 1 [46,48), layout
+// [61,64): 2 = SWIZZLE_128B, 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(layout & 7u) << 61;
+  return d;
+}
+// Instruction descriptor, kind::i8: D s32, A/B u8, A K-major, B major as given.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool b_mn_major) {
+  return (2u << 4)                      /* c_format S32        */
+         | (0u << 7) | (0u << 10)       /* a, b: unsigned 8-bit */
+         | (0u << 15)                   /* a K-major           */
+         | (uint32_t(b_mn_major) << 16) /* b major             */
+         | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// ------------------------------------------------------------------ TMEM
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------- ADC epilogue math
+// A column current on the snapped grid is n = hi*65025 + lo units of
+// 2^sh amperes (hi, lo = the two radix-255 digit-pair accumulators, each an
+// exact s32 < 2^23 for 128 crossbar rows).  The fp32 fast path approximates
+// scaled = I / i_fs * maxc to within 5e-5 codes; conversions whose fraction
+// lies within kDelta of a rounding boundary are re-evaluated with the
+// reference's own fp64 expression (converters.cpp:85-87), so every code is
+// bit-exact.
+struct AdcConst {
+  float c_hi, c_lo, k_lo, maxc;
+  int sh;
+  int maxc_i;
+  double i_fs, maxc_d;
+};
+constexpr float kDelta = 1.0f / 4096.0f;
+constexpr float kMagic23 = 8388608.0f;     // 2^23
+constexpr float kRint = 12582912.0f;       // 1.5 * 2^23
+
+__device__ __noinline__ float adc_exact(uint32_t hi, uint32_t lo, double i_fs, double maxc_d, int sh) {
+  const long long n = (long long)hi * 65025ll + (long long)lo;
+  const double I = ldexp(double(n), sh);
+  const double scaled = I / i_fs * maxc_d;
+  if (scaled >= maxc_d) return float(maxc_d);
+  return float(llround(scaled));
+}
+
+// fp32 fast path for one conversion: returns rint(scaled) (clamped to maxc)
+// and sets bit `bit` of `near` when the fraction is within kDelta of a
+// rounding boundary.
+__device__ __forceinline__ float adc_fast(uint32_t hi, uint32_t lo, const AdcConst& k, uint32_t& near, uint32_t bit) {
+  const float hf = __fsub_rn(__int_as_float(int(hi | 0x4B000000u)), kMagic23);
+  const float lt = __fmaf_rn(__int_as_float(int(lo | 0x4B000000u)), k.c_lo, k.k_lo);
+  float x = __fmaf_rn(hf, k.c_hi, lt);
+  x = fminf(x, k.maxc);
+  const float t = __fsub_rn(__fadd_rn(x, kRint), kRint);
+  const float r = fabsf(__fsub_rn(x, t));
+  if (r > 0.5f - kDelta) near |= bit;
+  return t;
+}
+
+// 16 conversions: fast path for all, exact fp64 re-evaluation only for the
+// (rare) near-boundary ones; the warp takes the fix-up branch only when one
+// of its lanes needs it.
+__device__ __forceinline__ void adc_chunk16(const uint32_t (&hi)[16], const uint32_t (&lo)[16], const AdcConst& k,
+                                            float (&t)[16], uint32_t& exact_ctr) {
+  uint32_t near = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) t[j] = adc_fast(hi[j], lo[j], k, near, 1u << j);
+  if (__any_sync(0xffffffffu, near != 0)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if ((near >> j) & 1u) {
+        ++exact_ctr;
+        t[j] = adc_exact(hi[j], lo[j], k.i_fs, k.maxc_d, k.sh);
+      }
+  }
+}
+
+}  // namespace tc
+}  // namespace xbs

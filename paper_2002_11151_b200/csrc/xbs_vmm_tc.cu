@@ -1,7 +1,309 @@
-// tcgen05 crossbar VMM kernels (placeholder until the UMMA path lands).
+// tcgen05 crossbar VMM kernels (K1 forward, K2 backward) for sm_100a.
+//
+// K1 (layers.cpp:246-283).  One CTA-persistent unit = (128 input bit-plane
+// rows = 128/TPi batch rows x TPi planes, 128 device output columns of one
+// crossbar tile column).  For every crossbar row tile tr, slice s and
+// polarity p the MMA warp issues a K = 2*128 chain of tcgen05.mma kind::i8
+// (M=128, N=256, K=32):
+//     D[:, 0:128]   = A_bits . d0 + A_255 . d1   (lo digit pair of q)
+//     D[:, 128:256] = A_bits . d2 + A_255 . d3   (hi digit pair of q)
+// so the TMEM accumulator holds the exact column current of every
+// (row, bit plane, column) split as hi*65025 + lo.  The K-extent of one
+// accumulation is exactly one crossbar (128 rows): the epilogue then applies
+// the ADC (exact, see xbs_tc_common.cuh) and the signed shift-add
+// P += +-2^(s*db) * code in fp32 registers (exact integers < 2^24), double-
+// buffered against the next chain in TMEM.  After the last tile the TPi
+// bit-plane lanes of each batch row are combined as sum 2^k * P_k in int64
+// and scaled once by k_out (layers.cpp:272-283), so y is bit-identical to the
+// snapped oracle.
+//
+// Warp roles (320 threads, 1 CTA / SM): warp 0 TMA producer, warp 1 TMEM
+// allocator + single-thread MMA issuer, warps 2..9 epilogue (warp w reads
+// TMEM lanes 32*(w%4).. and column half (w-2)/4).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
 #include "xbs_internal.cuh"
+#include "xbs_tc_common.cuh"
 
 namespace xbs {
-bool launch_fwd_tc(xbs_core*, int64_t, double*, cudaStream_t) { return false; }
+namespace tc {
+
+constexpr int kThreads = 320;
+constexpr int kAStages = 2, kBStages = 2;
+constexpr int kPlane = 128 * 128;          // one 128x128 u8 digit / bit box
+constexpr int kAStage = 2 * kPlane;        // bits + 255*bits
+constexpr int kBStage = 4 * kPlane;        // d0 d2 | d1 d3
+constexpr int kSmem = kAStages * kAStage + kBStages * kBStage + 1024 + 256;
+
+struct FwdArgs {
+  int GR, GC, S, db, TPi, tile_cols, C, R, N;
+  int64_t M, rowsF;
+  int num_mb, num_units;
+  double k_out;
+  AdcConst adc;
+  double* y;
+  unsigned long long* ctr;  // [0] exact path, [1] conversions
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kAStages * kAStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kBStages * kBStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kAStages;
+  uint64_t* b_full = a_empty + kAStages;
+  uint64_t* b_empty = b_full + kBStages;
+  uint64_t* t_full = b_empty + kBStages;
+  uint64_t* t_empty = t_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 8);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nsplit = a.C / 128;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------- TMA producer
+      uint32_t as = 0, aph = 0, bs = 0, bph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        const int mb = u % a.num_mb, nb = u / a.num_mb;
+        const int tc = nb / nsplit, h = nb % nsplit;
+        for (int tr = 0; tr < a.GR; ++tr) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_expect_tx(&a_full[as], kAStage);
+          tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tr * a.R, mb * 128);
+          tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tr * a.R, int(a.rowsF) + mb * 128);
+          if (++as == kAStages) { as = 0; aph ^= 1; }
+          for (int s = 0; s < a.S; ++s)
+            for (int p = 0; p < 2; ++p) {
+              mbar_wait(&b_empty[bs], bph ^ 1);
+              mbar_expect_tx(&b_full[bs], kBStage);
+              const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R;
+              uint8_t* dst = sB + bs * kBStage;
+              tma_load_2d(dst + 0 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 0 * a.R);  // d0
+              tma_load_2d(dst + 1 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 2 * a.R);  // d2
+              tma_load_2d(dst + 2 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 1 * a.R);  // d1
+              tma_load_2d(dst + 3 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 3 * a.R);  // d3
+              if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_i8(128, 256, /*b_mn_major=*/true);
+      uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        for (int tr = 0; tr < a.GR; ++tr) {
+          mbar_wait(&a_full[as], aph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + as * kAStage);
+          for (int sp = 0; sp < 2 * a.S; ++sp) {
+            mbar_wait(&t_empty[ab], abph ^ 1);
+            mbar_wait(&b_full[bs], bph);
+            tc_fence_after();
+            const uint32_t b0 = smem_u32(sB + bs * kBStage);
+            const uint32_t td = tmem + ab * 256;
+#pragma unroll
+            for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
+                const uint64_t bd = sdesc(b0 + dh * 2 * kPlane + 4096 * ks, kPlane, 1024, 2);
+                umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
+              }
+            umma_commit(&b_empty[bs]);
+            if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            umma_commit(&t_full[ab]);
+            if (++ab == 2) { ab = 0; abph ^= 1; }
+          }
+          umma_commit(&a_empty[as]);
+          if (++as == kAStages) { as = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else {  // ---------------------------------------------------- epilogue
+    const int lg = warp & 3, ch = (warp - 2) >> 2;
+    const int ml = 32 * lg + lane;
+    uint32_t ab = 0, abph = 0, exact = 0;
+    const AdcConst k = a.adc;
+    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      const int mb = u % a.num_mb, nb = u / a.num_mb;
+      float P[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) P[j] = 0.f;
+      for (int tr = 0; tr < a.GR; ++tr)
+        for (int s = 0; s < a.S; ++s)
+          for (int p = 0; p < 2; ++p) {
+            const float w = p == 0 ? float(1 << (s * a.db)) : -float(1 << (s * a.db));
+            mbar_wait(&t_full[ab], abph);
+            tc_fence_after();
+            const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 64 * ch;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t lo[16], hi[16];
+              tmem_ld16(ta + 16 * q, lo);
+              tmem_ld16(ta + 128 + 16 * q, hi);
+              tmem_wait_ld();
+              if (q == 3) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t_empty[ab]);
+              }
+              float t[16];
+              adc_chunk16(hi, lo, k, t, exact);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) P[16 * q + j] = __fmaf_rn(t[j], w, P[16 * q + j]);
+            }
+            if (++ab == 2) { ab = 0; abph ^= 1; }
+          }
+      // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
+      const int kk = ml % a.TPi;
+      const int64_t b = int64_t(mb) * (128 / a.TPi) + ml / a.TPi;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        long long v = (long long)__float2ll_rn(P[j]) << kk;
+        for (int o = 1; o < a.TPi; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int col = nb * 128 + 64 * ch + j;
+        const int tc = col / a.C, c = col % a.C;
+        const int jg = tc * a.tile_cols + c;
+        if (kk == 0 && b < a.M && c < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v) * a.k_out;
+      }
+    }
+    if (a.ctr) {
+      atomicAdd(&a.ctr[0], (unsigned long long)exact);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D u8 tensor [outer][inner] with a 128 x 128 box, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                     uint32_t box_outer) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+AdcConst make_adc_const(const xbs_core* c) {
+  AdcConst k{};
+  const double cn = std::ldexp(1.0, c->adc.sh) / c->adc.i_fs * c->adc.maxc_d;  // codes per current unit
+  k.c_lo = float(cn);
+  k.c_hi = float(65025.0 * cn);
+  k.k_lo = -8388608.0f * k.c_lo;
+  k.maxc = float(c->adc.maxc);
+  k.sh = c->adc.sh;
+  k.maxc_i = c->adc.maxc;
+  k.i_fs = c->adc.i_fs;
+  k.maxc_d = c->adc.maxc_d;
+  return k;
+}
+
+}  // namespace tc
+
+bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
+  using namespace tc;
+  const Geo& g = c->g;
+  if (g.R != 128 || g.TPi > 16 || c->adc.passthrough) return false;
+  // fp32 P accumulators must stay exact: GR * maxc * sum_s 2^(s db) < 2^24
+  const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
+  if (double(g.GR) * c->adc.maxc * sw >= 16777216.0) return false;
+  const int64_t rowsF = ((M * g.TPi + 127) / 128) * 128;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, c->d_Af, uint64_t(g.KI), uint64_t(2 * rowsF), 128, 128)) return false;
+  if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 128)) return false;
+  FwdArgs a{};
+  a.GR = g.GR;
+  a.GC = g.GC;
+  a.S = g.S;
+  a.db = g.db;
+  a.TPi = g.TPi;
+  a.tile_cols = g.tile_cols;
+  a.C = g.C;
+  a.R = g.R;
+  a.N = g.N;
+  a.M = M;
+  a.rowsF = rowsF;
+  a.num_mb = int(rowsF / 128);
+  a.num_units = a.num_mb * (g.NI / 128);
+  a.k_out = c->k_out_fwd;
+  a.adc = make_adc_const(c);
+  a.y = d_y;
+  a.ctr = &c->d_sc->exact_path;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  const int grid = std::min(a.num_units, sm_count());
+  k_fwd_tc<<<grid, kThreads, kSmem, st>>>(mA, mB, a);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
 bool launch_bwd_tc(xbs_core*, int64_t, double*, cudaStream_t) { return false; }
+
 }  // namespace xbs
