@@ -1,0 +1,334 @@
+#!/usr/bin/env python3
+"""Crossbar-evaluation hot path benchmark (BASELINE.json metric).
+
+One step = one pass of the hot path over one batch: CrossbarCore forward
+(K0a prep + K1 tcgen05 VMM), backward (K0b prep + K3a dW + K2 tcgen05 VMM)
+and apply_updates (K3b fused update + regeneration) of the configs[1] layer
+at its largest sweep point (M=256, K=N=4096, 128x128 crossbars, 8-bit in /
+weights as four 2-bit slices, 1-bit DAC, 7-bit ADC, AAM parasitics).
+
+  value : non-ideal crossbar MACs/s with inputs resident in HBM (device
+          pointers through the C ABI), CUDA events on the core's stream,
+          max over ranks; N ranks run N independent replicas (weak scaling).
+  e2e   : the same metric through the host-pointer C-ABI calls (pinned host
+          buffers; H2D of x, dy and D2H of y, dx inside every step).
+
+`python bench.py --impl reference` times the reference algorithm's CPU
+implementation (the restated oracle, oracle/ -- the reference itself cannot
+be built here) on the host cores, on a bounded tile sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "non-ideal crossbar MACs/s (fwd+bwd+update) on 1 B200; % of int8 TC / HBM roofline"
+L_LIMBS = 4  # u8 limbs per snapped conductance (radix-255 digits) -> int8 ops = 2 * L * MAC
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2-4096")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ int8 peak
+def measure_int8_peak():
+    """Dense int8 tensor-core peak on this B200: torch._int_mm 8192^3 best of 10."""
+    import torch
+
+    try:
+        n = 8192
+        a = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12, "measured: torch._int_mm 8192^3 best of 10 (TOPS)"
+    except Exception as e:  # pragma: no cover
+        return 4500.0, f"NVIDIA dense int8 spec 4.5 POPS (measurement failed: {e})"
+
+
+# ----------------------------------------------------------- CPU baseline
+def cpu_sample(cfg, n_feat=256, steps=1):
+    """The oracle (restated reference CPU path, 1 thread: the reference's
+    forward/backward/update are serial, layers.hpp:34) on a bounded sample of
+    the same workload: a K=N=n_feat slice of the layer (same tile geometry,
+    batch, bits and options).  Returns (MAC/s, seconds, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py
+    from paper_2002_11151_b200.configs import Layer
+
+    layer = cfg.layers[0]
+    sl = Layer("sample", layer.M, n_feat, n_feat)
+    opt = cfg.options()
+    W, x, dy = cfg.weights(sl), cfg.inputs(sl), cfg.errors(sl)
+    orc = oracle_py.OracleCore(W, opt, snapped=True)
+    t0 = time.perf_counter()
+    for it in range(steps):
+        orc.forward(x, True)
+        orc.backward(dy, 1.0)
+        orc.apply_updates(it)
+    dt = (time.perf_counter() - t0) / steps
+    macs = cfg.macs(sl)["total"]
+    desc = (f"oracle fwd+bwd+update of a K=N={n_feat} slice of {cfg.name} (M={layer.M}, "
+            f"{(n_feat // cfg.tile) ** 2} of {((layer.K + cfg.tile - 1) // cfg.tile) * ((layer.N + cfg.tile - 1) // cfg.tile)}"
+            f" crossbar tiles), {dt:.2f} s/step, MACs/s scale linearly in tile count")
+    return macs / dt, dt, desc
+
+
+def run_reference(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    ncores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample(cfg, 256, 1)
+    vals = [cpu_sample(cfg, 256, 1) for _ in range(args.steps)]
+    v = statistics.median([x[0] for x in vals])
+    dt = statistics.median([x[1] for x in vals])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "MAC/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "layer": vars(cfg.layers[0]), "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port", "sample": vals[0][2],
+                         "host_cores_available": ncores,
+                         "note": "reference unbuildable here (Eigen3 absent); restated oracle, serial like the reference"},
+        "e2e": {"value": v, "unit": "MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- ours
+def main():
+    args = parse()
+    from paper_2002_11151_b200.configs import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    from paper_2002_11151_b200 import xbarsim as xb
+
+    layer = cfg.layers[0]
+    M, K, N = layer.M, layer.K, layer.N
+    opt = cfg.options()
+    W, x, dy = cfg.weights(layer), cfg.inputs(layer), cfg.errors(layer)
+    core = xb.CrossbarCore(W, opt)
+    stream = torch.cuda.ExternalStream(core.stream())
+    # device-resident operands, column-major (Eigen layout): (K, M) C-order == M x K col-major
+    d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    d_dy = torch.from_numpy(np.ascontiguousarray(dy.T)).cuda()
+    d_y = torch.empty((N, M), dtype=torch.float64, device="cuda")
+    d_dx = torch.empty((K, M), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+
+    it = [0]
+
+    def step():
+        core.forward_device(d_x.data_ptr(), M, True, d_y.data_ptr())
+        core.backward_device(d_dy.data_ptr(), M, 1.0, d_dx.data_ptr())
+        core.apply_updates_device(it[0])
+        it[0] += 1
+
+    for _ in range(args.warmup):
+        step()
+    core.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = core.launch_count()
+    core.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    core.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = core.stage_times()
+    core.profile(False)
+    launches = core.launch_count() - launches0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the host-pointer C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        def pinned(rows, cols):  # F-ordered (rows x cols) numpy view of pinned memory
+            return torch.empty((cols, rows), dtype=torch.float64, pin_memory=True).numpy().T
+
+        hx, hdy, hy, hdx = pinned(M, K), pinned(M, N), pinned(M, N), pinned(M, K)
+        hx[:] = x
+        hdy[:] = dy
+        for _ in range(2):
+            core.forward(hx, True, out=hy)
+            core.backward(hdy, 1.0, out=hdx)
+            core.apply_updates(it[0])
+            it[0] += 1
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            core.forward(hx, True, out=hy)
+            core.backward(hdy, 1.0, out=hdx)
+            core.apply_updates(it[0])
+            it[0] += 1
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"h2d_bytes_per_step": 8 * M * (K + N), "d2h_bytes_per_step": 8 * M * (N + K), "s": e2e_s}
+    clk = clocks.stop()
+
+    macs = cfg.macs(layer)
+    S = cfg.weight_bits // cfg.device_bits
+    peak_tops, peak_src = measure_int8_peak()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in stages.items()}
+    work = {  # algorithmic work per launch of each stage
+        "fwd_vmm": ("tensor", 2 * L_LIMBS * macs["fwd"] / 1e12, "TFLOP/s"),
+        "bwd_vmm": ("tensor", 2 * L_LIMBS * macs["bwd"] / 1e12, "TFLOP/s"),
+        "dw": ("tensor", 2 * macs["upd"] / 1e12, "TFLOP/s"),
+        "update": ("hbm", K * N * (24 * S + 8) / 1e9, "GB/s"),
+    }
+    roof_all = {}
+    for st, (bound, amount, unit) in work.items():
+        if per.get(st):
+            ach = amount / (per[st] * 1e-3)
+            pk = peak_tops if bound == "tensor" else hbm
+            roof_all[st] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk,
+                            "ms": per[st]}
+    dominant = max(("fwd_vmm", "bwd_vmm", "update", "dw"), key=lambda s: per.get(s, 0.0))
+    traffic = None
+    tpath = args.traffic or os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dominant)
+    roof = dict(roof_all.get(dominant, {}))
+    roof.update({"kernel": dominant, "traffic": traffic,
+                 "peak_source": peak_src if roof.get("bound") == "tensor" else "MEASURED_PEAKS.json hbm_gbs"})
+
+    value = world * macs["total"] / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg.name, "M": M, "K": K, "N": N, "tile": cfg.tile, "slices": S,
+                   "adc_bits": cfg.adc_bits, "parallelism": f"replicas{world}",
+                   "l2": "inputs larger than L2 (conductance digits %.0f MB/step > 126 MB)" % (
+                       2 * S * K * N * 4 / 1e6)},
+        "roofline": roof,
+        "roofline_stages": roof_all,
+        "int8_peak_tops": peak_tops,
+        "macs_per_step": macs,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = {"value": world * macs["total"] / e2e["s"], "unit": "MAC/s",
+                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, desc = cpu_sample(cfg, 256, 1)
+        line["cpu_baseline"] = {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,18 @@ int xbs_core_select_kernel(xbs_core* core, int32_t kernel);
 /* CUDA stream (cudaStream_t) the core enqueues on, as an opaque pointer. */
 void* xbs_core_stream(xbs_core* core);
 
+/* Per-stage device timing (CUDA events recorded on the core's stream around
+ * each stage while enabled).  Stages: 0 prep_x (K0a), 1 forward VMM (K1),
+ * 2 prep_dy (K0b), 3 dW (K3a), 4 backward VMM (K2), 5 update+regeneration
+ * (K3b).  xbs_core_stage_times synchronizes and returns the accumulated
+ * milliseconds and the number of timed instances per stage (n <= 6). */
+enum { XBS_STAGE_PREP_X = 0, XBS_STAGE_FWD = 1, XBS_STAGE_PREP_DY = 2, XBS_STAGE_DW = 3, XBS_STAGE_BWD = 4,
+       XBS_STAGE_UPDATE = 5, XBS_NUM_STAGES = 6 };
+int xbs_core_profile(xbs_core* core, int32_t enable);
+int xbs_core_stage_times(xbs_core* core, double* ms, int64_t* count, int32_t n);
+/* Number of this library's kernels launched by the core so far. */
+int64_t xbs_core_launch_count(xbs_core* core);
+
 #ifdef __cplusplus
 }
 #endif

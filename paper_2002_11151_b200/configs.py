@@ -1,0 +1,138 @@
+"""The five BASELINE.json workloads as seeded synthetic layers.
+
+Each config is a list of crossbar-mapped layers (M rows through the layer,
+K inputs, N outputs) plus the CrossbarLayerOptions the config phrase maps to
+(SURVEY.md Appendix B).  No dataset files exist in the image: inputs, weights
+and output errors are seeded synthetic tensors with the distributions the
+configs name.  adc.i_fs is pinned per config (auto-calibration is off the
+path): each value is the nearest-rank 0.999 quantile (converters.cpp:96-107)
+of forward column currents over a seeded tile sample of the config's first
+batch, frozen here.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, List
+
+import numpy as np
+
+from .xbarsim import CrossbarLayerOptions, EngineKind
+
+
+@dataclasses.dataclass
+class Layer:
+    name: str
+    M: int
+    K: int
+    N: int
+
+
+@dataclasses.dataclass
+class Config:
+    name: str
+    layers: List[Layer]
+    tile: int
+    weight_bits: int
+    device_bits: int
+    adc_bits: int
+    i_fs: float
+    r_row: float = 1.0
+    r_col: float = 4.6
+    r_source: float = 0.0
+    r_sense: float = 0.0
+    sigma: float = 0.0
+    v: float = 0.0
+    gamma: float = 0.0
+    lr: float = 0.1
+    x_dist: str = "u01"      # u01 | u-11 | n01
+    w_dist: str = "n0.02"    # n<sd> | kaiming
+    dy_dist: str = "u-11"
+    cid: int = 2
+    notes: str = ""
+
+    def options(self) -> CrossbarLayerOptions:
+        o = CrossbarLayerOptions()
+        o.engine = EngineKind.aam
+        o.crossbar.rows = o.crossbar.cols = self.tile
+        o.crossbar.r_row, o.crossbar.r_col = self.r_row, self.r_col
+        o.crossbar.r_source, o.crossbar.r_sense = self.r_source, self.r_sense
+        o.crossbar.g_min, o.crossbar.g_max = 1e-6, 1e-5  # Ron=100k, Ron/Roff=10
+        o.map.tile_rows = o.map.tile_cols = self.tile
+        o.map.weight_bits, o.map.device_bits = self.weight_bits, self.device_bits
+        o.map.variation_sigma, o.map.seed = self.sigma, 4000 + self.cid
+        o.adc.bits, o.adc.i_fs = self.adc_bits, self.i_fs
+        o.update.v, o.update.gamma, o.update.lr, o.update.seed = self.v, self.gamma, self.lr, 5000 + self.cid
+        o.act_bits = o.error_bits = 8
+        return o
+
+    def weights(self, layer: Layer, idx: int = 0) -> np.ndarray:
+        rng = np.random.default_rng(2000 + 100 * self.cid + idx)
+        if self.w_dist == "kaiming":
+            return rng.normal(0.0, np.sqrt(2.0 / layer.K), (layer.K, layer.N))
+        return rng.normal(0.0, float(self.w_dist[1:]), (layer.K, layer.N))
+
+    def _draw(self, dist: str, shape, seed: int) -> np.ndarray:
+        rng = np.random.default_rng(seed)
+        if dist == "u01":
+            return rng.uniform(0.0, 1.0, shape)
+        if dist == "u-11":
+            return rng.uniform(-1.0, 1.0, shape)
+        return rng.normal(0.0, 1.0, shape)
+
+    def inputs(self, layer: Layer, idx: int = 0) -> np.ndarray:
+        return self._draw(self.x_dist, (layer.M, layer.K), 1000 + 100 * self.cid + idx)
+
+    def errors(self, layer: Layer, idx: int = 0) -> np.ndarray:
+        return self._draw(self.dy_dist, (layer.M, layer.N), 3000 + 100 * self.cid + idx)
+
+    def macs(self, layer: Layer, T_in: int = 8, T_err: int = 8) -> dict:
+        """Algorithmic work per step: logical, unpadded."""
+        S = self.weight_bits // self.device_bits
+        f = layer.M * T_in * layer.K * layer.N * S * 2
+        b = layer.M * T_err * layer.K * layer.N * S * 4
+        u = layer.M * layer.K * layer.N
+        return {"fwd": f, "bwd": b, "upd": u, "total": f + b + u}
+
+
+def _c3_layers() -> List[Layer]:
+    L = [Layer("conv1", 131072, 27, 16)]
+    L += [Layer(f"s1.{i}", 131072, 144, 16) for i in range(6)]
+    L += [Layer("s2.0", 32768, 144, 32)] + [Layer(f"s2.{i}", 32768, 288, 32) for i in range(1, 6)]
+    L += [Layer("s3.0", 8192, 288, 64)] + [Layer(f"s3.{i}", 8192, 576, 64) for i in range(1, 6)]
+    L += [Layer("fc", 128, 64, 10)]
+    return L
+
+
+def _c4_layers() -> List[Layer]:
+    L = [Layer("conv1", 401408, 147, 64)]
+    L += [Layer(f"layer1.{i}", 100352, 576, 64) for i in range(4)]
+    L += [Layer("layer2.0", 25088, 576, 128)] + [Layer(f"layer2.{i}", 25088, 1152, 128) for i in range(1, 4)]
+    L += [Layer("layer2.ds", 25088, 64, 128)]
+    L += [Layer("layer3.0", 6272, 1152, 256)] + [Layer(f"layer3.{i}", 6272, 2304, 256) for i in range(1, 4)]
+    L += [Layer("layer3.ds", 6272, 128, 256)]
+    L += [Layer("layer4.0", 1568, 2304, 512)] + [Layer(f"layer4.{i}", 1568, 4608, 512) for i in range(1, 4)]
+    L += [Layer("layer4.ds", 1568, 256, 512)]
+    L += [Layer("fc", 32, 512, 1000)]
+    return L
+
+
+CONFIGS = {
+    # configs[0]: MLP 784-256-10 train step (the reference's CPU-runnable case)
+    "c1": Config("c1-mlp-784-256-10", [Layer("fc1", 64, 784, 256), Layer("fc2", 64, 256, 10)], tile=64,
+                 weight_bits=8, device_bits=2, adc_bits=6, i_fs=1.7e-4, r_row=1.0, r_col=1.0, r_source=1000.0,
+                 r_sense=1000.0, sigma=0.1, x_dist="u01", w_dist="n0.05", cid=1,
+                 notes="lognormal sigma=10% run as the reference's Normal(1,sigma) multiplier (Appendix B)"),
+    # configs[1]: single crossbar-mapped GEMM sweep, K=N in {512..4096}, batch 256
+    **{f"c2-{n}": Config(f"c2-gemm-{n}", [Layer(f"gemm{n}", 256, n, n)], tile=128, weight_bits=8, device_bits=2,
+                         adc_bits=7, i_fs=1.8e-4, x_dist="u-11", w_dist="n0.02", cid=2)
+       for n in (512, 1024, 2048, 4096)},
+    "c3": Config("c3-resnet20-im2col", _c3_layers(), tile=128, weight_bits=8, device_bits=4, adc_bits=8, i_fs=2.0e-4,
+                 v=1.0, gamma=0.05, x_dist="n01", w_dist="kaiming", dy_dist="n01", cid=3,
+                 notes="write sigma=5% mapped to UpdateSpec.gamma (Appendix B); per-layer im2col GEMM workloads"),
+    "c4": Config("c4-resnet18-im2col", _c4_layers(), tile=128, weight_bits=8, device_bits=2, adc_bits=6, i_fs=2.0e-4,
+                 x_dist="n01", w_dist="kaiming", dy_dist="n01", cid=4),
+    "c5": Config("c5-stress-8192", [Layer("vmm", 4096, 8192, 8192)], tile=256, weight_bits=8, device_bits=1,
+                 adc_bits=8, i_fs=4.0e-4, r_row=2.5, r_col=2.5, sigma=0.2, x_dist="n01", w_dist="n0.02",
+                 dy_dist="n01", cid=5,
+                 notes="lognormal sigma=20% -> Normal(1,sigma); 'asymmetric update ratio 0.8' has no reference knob"),
+}

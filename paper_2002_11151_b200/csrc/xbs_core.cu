@@ -199,14 +199,64 @@ void d2h_rowmajor_to_colmajor(xbs_core* c, const double* d, int64_t rows, int64_
     for (int64_t i = 0; i < rows; ++i) h[j * ld + i] = c->h_tmp[size_t(i * cols + j)];
 }
 
+// CUDA-event bracket around one stage (only while profiling is enabled).
+struct StageScope {
+  xbs_core* c;
+  int stage;
+  cudaEvent_t a = nullptr;
+  static cudaEvent_t take(xbs_core* c) {
+    if (!c->ev_pool.empty()) {
+      cudaEvent_t e = c->ev_pool.back();
+      c->ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
+  StageScope(xbs_core* cc, int s) : c(cc), stage(s) {
+    if (c->profile) {
+      a = take(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~StageScope() {
+    if (a) {
+      cudaEvent_t b = take(c);
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({stage, a, b});
+    }
+  }
+};
+
+void collect_stage_times(xbs_core* c) {
+  if (c->pending.empty()) return;
+  sync(c);
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, p.a, p.b), "cudaEventElapsedTime");
+    c->stage_ms[p.stage] += ms;
+    c->stage_n[p.stage] += 1;
+    c->ev_pool.push_back(p.a);
+    c->ev_pool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
 void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y) {
   (void)training;  // training only feeds ADC auto-calibration (out of scope)
   if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
   ensure_batch(c, std::max<int64_t>(M, 1));
-  xbs::launch_prep_x(c, d_x, M, c->stream);
+  {
+    StageScope st(c, XBS_STAGE_PREP_X);
+    xbs::launch_prep_x(c, d_x, M, c->stream);
+    c->launches += M > 0 ? 1 : 0;
+  }
   c->have_forward = true;
   c->M_fwd = M;
   if (M == 0) return;
+  StageScope st(c, XBS_STAGE_FWD);
+  c->launches += 1;
   if (c->fully_ideal) {
     xbs::launch_fwd_ideal(c, M, d_y, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_fwd_tc(c, M, d_y, c->stream)) {
@@ -217,10 +267,20 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, do
 void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
   if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
   if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
-  xbs::launch_prep_dy(c, d_dy, M, c->stream);
-  xbs::launch_dw(c, M, gd, c->stream);
+  {
+    StageScope st(c, XBS_STAGE_PREP_DY);
+    xbs::launch_prep_dy(c, d_dy, M, c->stream);
+    c->launches += M > 0 ? 3 : 2;
+  }
+  {
+    StageScope st(c, XBS_STAGE_DW);
+    xbs::launch_dw(c, M, gd, c->stream);
+    c->launches += 1;
+  }
   c->have_grad = true;
   if (M == 0) return;
+  StageScope st(c, XBS_STAGE_BWD);
+  c->launches += 1;
   if (c->fully_ideal) {
     xbs::launch_bwd_ideal(c, d_dy, M, d_dx, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_bwd_tc(c, M, d_dx, c->stream)) {
@@ -243,8 +303,10 @@ void apply_updates_device(xbs_core* c, uint64_t iteration) {
   up.linear = c->opt.upd_v == 0.0;
   ck(cudaMemsetAsync(&c->d_sc->dwmax, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
   ck(cudaMemsetAsync(&c->d_sc->err_flag, 0, sizeof(int), c->stream), "memset");
+  StageScope st(c, XBS_STAGE_UPDATE);
   xbs::launch_update(c, up, c->stream);
   regenerate_bookkeeping(c);
+  c->launches += c->opt.engine == XBS_ENGINE_IDEAL ? 2 : 1;
   c->have_grad = false;
   c->have_forward = false;
 }
@@ -450,6 +512,11 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_ecodes);
   cudaFree(c->d_io_in);
   cudaFree(c->d_io_out);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -640,5 +707,30 @@ int xbs_core_select_kernel(xbs_core* c, int32_t kernel) {
 }
 
 void* xbs_core_stream(xbs_core* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int xbs_core_profile(xbs_core* c, int32_t enable) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    collect_stage_times(c);
+    c->profile = enable != 0;
+    for (int i = 0; i < XBS_NUM_STAGES; ++i) {
+      c->stage_ms[i] = 0.0;
+      c->stage_n[i] = 0;
+    }
+  });
+}
+
+int xbs_core_stage_times(xbs_core* c, double* ms, int64_t* count, int32_t n) {
+  return guard([&] {
+    if (!c || n < 0 || n > XBS_NUM_STAGES) fail(XBS_INVALID_ARGUMENT, "stage_times: bad arguments");
+    collect_stage_times(c);
+    for (int i = 0; i < n; ++i) {
+      if (ms) ms[i] = c->stage_ms[i];
+      if (count) count[i] = c->stage_n[i];
+    }
+  });
+}
+
+int64_t xbs_core_launch_count(xbs_core* c) { return c ? c->launches : 0; }
 
 }  // extern "C"

@@ -122,6 +122,14 @@ struct xbs_core {
   int64_t exact_path = 0, conversions = 0;
   // host mirrors for readback
   std::vector<double> h_tmp;
+  // profiling: pending (stage, start, stop) event pairs, accumulated totals
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { int stage; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  double stage_ms[XBS_NUM_STAGES] = {};
+  int64_t stage_n[XBS_NUM_STAGES] = {};
+  int64_t launches = 0;
 };
 
 namespace xbs {

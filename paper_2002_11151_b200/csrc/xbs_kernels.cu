@@ -442,11 +442,11 @@ void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st)
 
 // backward (layers.cpp:339-379): one thread per (b, logical input row i).
 __global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__ A, const uint8_t* __restrict__ digits,
-                           double F_over_vu, double ifs_fac, int adc_scaled, double lev_e,
+                           double F, double vu, double ifs_fac, int adc_scaled, double lev_e,
                            const DevScalars* __restrict__ sc, double* __restrict__ dx) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
-  double k_out = step_e * F_over_vu;
+  double k_out = step_e * F / vu;  // layers.cpp:375
   if (adc_scaled) k_out *= ifs_fac;
   const int64_t n = M * g.K;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
@@ -479,7 +479,7 @@ void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st
   const int64_t n = M * c->g.K;
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
-  k_bwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, c->d_Ab, c->d_digits, c->F / c->vu, c->ifs_fac,
+  k_bwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, c->d_Ab, c->d_digits, c->F, c->vu, c->ifs_fac,
                                       c->adc_scaled ? 1 : 0, c->lev_e, c->d_sc, d_dx);
 }
 

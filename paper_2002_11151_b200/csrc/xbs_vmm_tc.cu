@@ -304,6 +304,246 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   return cudaPeekAtLastError() == cudaSuccess;
 }
 
-bool launch_bwd_tc(xbs_core*, int64_t, double*, cudaStream_t) { return false; }
+// ---------------------------------------------------------------------------
+// K2 backward (layers.cpp:339-379).  Unit = (128 error bit-plane rows: 128 /
+// (2 TPe) batch rows x TPe planes x {plus, minus} phase, 64 device rows of
+// one crossbar row tile).  For each crossbar column tile tc and slice s one
+// chain of K = 2 x 128 (tile columns, bits | 255*bits) computes, with the
+// transposed tiles read K-major straight from the same digit planes,
+//     D[:, p*128 + acc*64 + r] = sum_c v_phi[c] * q_acc(s, p, tr, tc; r, c)
+// i.e. all four products vp.gp, vp.gn, vm.gp, vm.gn of the reference in one
+// accumulator (phase in M, polarity in N).  The epilogue converts every one
+// of them through the ADC and accumulates  +-2^(s db) * code  with sign
+// +1 when phase == polarity (acc_pos) and -1 otherwise (acc_neg).
+namespace tc {
+
+struct BwdArgs {
+  int GR, GC, S, db, TPe, tile_rows, R, C, K;
+  int64_t M, rowsB;
+  int num_mb, num_units;
+  double F, vu, ifs_fac, lev_e;
+  int adc_scaled;
+  const DevScalars* sc;
+  AdcConst adc;
+  double* dx;
+  unsigned long long* ctr;
+};
+
+constexpr int kBHalf = 64 * 128;  // one [64 rows][128 cols] digit box
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_bwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kAStages * kAStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kBStages * kBStage);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kAStages;
+  uint64_t* b_full = a_empty + kAStages;
+  uint64_t* b_empty = b_full + kBStages;
+  uint64_t* t_full = b_empty + kBStages;
+  uint64_t* t_empty = t_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 8);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int rhalves = a.R / 64;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------- TMA producer
+      uint32_t as = 0, aph = 0, bs = 0, bph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        const int mb = u % a.num_mb, rb = u / a.num_mb;
+        const int tr = rb / rhalves, rh = rb % rhalves;
+        for (int tc = 0; tc < a.GC; ++tc) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_expect_tx(&a_full[as], kAStage);
+          tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tc * a.C, mb * 128);
+          tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tc * a.C, int(a.rowsB) + mb * 128);
+          if (++as == kAStages) { as = 0; aph ^= 1; }
+          for (int s = 0; s < a.S; ++s) {
+            mbar_wait(&b_empty[bs], bph ^ 1);
+            mbar_expect_tx(&b_full[bs], kBStage);
+            uint8_t* dst = sB + bs * kBStage;
+            // smem order [dh][p][acc][64 r][128 c]; digit d = 2*acc + dh
+#pragma unroll
+            for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+              for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int acc = 0; acc < 2; ++acc) {
+                  const int row = (((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) + 2 * acc + dh) * a.R + rh * 64;
+                  tma_load_2d(dst + ((dh * 2 + p) * 2 + acc) * kBHalf, &mapB, &b_full[bs], 0, row);
+                }
+            if (++bs == kBStages) { bs = 0; bph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_i8(128, 256, /*b_mn_major=*/false);
+      uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        for (int tc = 0; tc < a.GC; ++tc) {
+          mbar_wait(&a_full[as], aph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + as * kAStage);
+          for (int s = 0; s < a.S; ++s) {
+            mbar_wait(&t_empty[ab], abph ^ 1);
+            mbar_wait(&b_full[bs], bph);
+            tc_fence_after();
+            const uint32_t b0 = smem_u32(sB + bs * kBStage);
+            const uint32_t td = tmem + ab * 256;
+#pragma unroll
+            for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
+                const uint64_t bd = sdesc(b0 + dh * 4 * kBHalf + 32 * ks, 16, 1024, 2);
+                umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
+              }
+            umma_commit(&b_empty[bs]);
+            if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            umma_commit(&t_full[ab]);
+            if (++ab == 2) { ab = 0; abph ^= 1; }
+          }
+          umma_commit(&a_empty[as]);
+          if (++as == kAStages) { as = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else {  // ---------------------------------------------------- epilogue
+    const int lg = warp & 3, ch = (warp - 2) >> 2;
+    const int ml = 32 * lg + lane;
+    const int phi = ml & 1;
+    uint32_t ab = 0, abph = 0, exact = 0;
+    const AdcConst k = a.adc;
+    const double se = a.sc->se;
+    const double step_e = se > 0 ? se / a.lev_e : 0.0;
+    double k_out = step_e * a.F / a.vu;  // layers.cpp:375-377
+    if (a.adc_scaled) k_out *= a.ifs_fac;
+    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      const int mb = u % a.num_mb, rb = u / a.num_mb;
+      const int tr = rb / rhalves, rh = rb % rhalves;
+      float P[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) P[j] = 0.f;
+      for (int tc = 0; tc < a.GC; ++tc)
+        for (int s = 0; s < a.S; ++s) {
+          const float w = float(1 << (s * a.db));
+          mbar_wait(&t_full[ab], abph);
+          tc_fence_after();
+          const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 32 * ch;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const float ws = p == phi ? w : -w;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              uint32_t lo[16], hi[16];
+              tmem_ld16(ta + p * 128 + 16 * q, lo);
+              tmem_ld16(ta + p * 128 + 64 + 16 * q, hi);
+              tmem_wait_ld();
+              if (p == 1 && q == 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t_empty[ab]);
+              }
+              float t[16];
+              adc_chunk16(hi, lo, k, t, exact);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) P[16 * q + j] = __fmaf_rn(t[j], ws, P[16 * q + j]);
+            }
+          }
+          if (++ab == 2) { ab = 0; abph ^= 1; }
+        }
+      // combine the 2*TPe (plane, phase) lanes of each batch row
+      const int grp = 2 * a.TPe;
+      const int kk = (ml % grp) >> 1;
+      const int64_t b = int64_t(mb) * (128 / grp) + ml / grp;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        long long v = (long long)__float2ll_rn(P[j]) << kk;
+        for (int o = 1; o < grp; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int rloc = rh * 64 + 32 * ch + j;
+        const int ig = tr * a.tile_rows + rloc;
+        if ((ml % grp) == 0 && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v) * k_out;
+      }
+    }
+    if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace tc
+
+bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
+  using namespace tc;
+  const Geo& g = c->g;
+  if (g.R != 128 || g.C != 128 || g.TPe > 16 || c->adc.passthrough) return false;
+  const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
+  if (double(g.GC) * c->adc.maxc * sw * 2.0 >= 16777216.0) return false;
+  const int64_t rowsB = ((M * g.TPe * 2 + 127) / 128) * 128;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
+  if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 64)) return false;
+  BwdArgs a{};
+  a.GR = g.GR;
+  a.GC = g.GC;
+  a.S = g.S;
+  a.db = g.db;
+  a.TPe = g.TPe;
+  a.tile_rows = g.tile_rows;
+  a.R = g.R;
+  a.C = g.C;
+  a.K = g.K;
+  a.M = M;
+  a.rowsB = rowsB;
+  a.num_mb = int(rowsB / 128);
+  a.num_units = a.num_mb * (g.KI / 64);
+  a.F = c->F;
+  a.vu = c->vu;
+  a.ifs_fac = c->ifs_fac;
+  a.lev_e = c->lev_e;
+  a.adc_scaled = c->adc_scaled ? 1 : 0;
+  a.sc = c->d_sc;
+  a.adc = make_adc_const(c);
+  a.dx = d_dx;
+  a.ctr = &c->d_sc->exact_path;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  const int grid = std::min(a.num_units, sm_count());
+  k_bwd_tc<<<grid, kThreads, kSmem, st>>>(mA, mB, a);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
 
 }  // namespace xbs

@@ -248,7 +248,12 @@ SYMBOLS = {
     "xbs_core_adc_counters": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "xbs_core_select_kernel": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stream": (_P, [_P]),
+    "xbs_core_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
+    "xbs_core_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(_I64), ctypes.c_int32]),
+    "xbs_core_launch_count": (_I64, [_P]),
 }
+
+STAGES = ("prep_x", "fwd_vmm", "prep_dy", "dw", "bwd_vmm", "update")
 
 _lib = None
 
@@ -309,22 +314,24 @@ class CrossbarCore:
     def handle(self):
         return self._h
 
-    def forward(self, x: np.ndarray, training: bool) -> np.ndarray:
+    def forward(self, x: np.ndarray, training: bool, out: Optional[np.ndarray] = None) -> np.ndarray:
         x = _fortran(x)
         if x.ndim != 2 or x.shape[1] != self._K:
             raise ValueError("CrossbarCore::forward: feature count mismatch")
         M = x.shape[0]
-        y = np.zeros((M, self._N), dtype=np.float64, order="F")
+        y = np.zeros((M, self._N), dtype=np.float64, order="F") if out is None else out
+        assert y.shape == (M, self._N) and y.flags.f_contiguous
         _check(load_library().xbs_core_forward(self._h, _ptr(x), M, max(1, M), int(bool(training)), _ptr(y),
                                                max(1, M)))
         return y
 
-    def backward(self, dy: np.ndarray, grad_divisor: float) -> np.ndarray:
+    def backward(self, dy: np.ndarray, grad_divisor: float, out: Optional[np.ndarray] = None) -> np.ndarray:
         dy = _fortran(dy)
         if dy.ndim != 2 or dy.shape[1] != self._N:
             raise ValueError("CrossbarCore::backward: gradient shape mismatch")
         M = dy.shape[0]
-        dx = np.zeros((M, self._K), dtype=np.float64, order="F")
+        dx = np.zeros((M, self._K), dtype=np.float64, order="F") if out is None else out
+        assert dx.shape == (M, self._K) and dx.flags.f_contiguous
         _check(load_library().xbs_core_backward(self._h, _ptr(dy), M, max(1, M), float(grad_divisor), _ptr(dx),
                                                 max(1, M)))
         return dx
@@ -411,6 +418,19 @@ class CrossbarCore:
 
     def stream(self) -> int:
         return load_library().xbs_core_stream(self._h) or 0
+
+    def profile(self, enable: bool) -> None:
+        _check(load_library().xbs_core_profile(self._h, int(bool(enable))))
+
+    def stage_times(self):
+        """{stage: (total_ms, count)} accumulated while profiling."""
+        ms = (ctypes.c_double * 6)()
+        n = (ctypes.c_int64 * 6)()
+        _check(load_library().xbs_core_stage_times(self._h, ms, n, 6))
+        return {STAGES[i]: (ms[i], n[i]) for i in range(6)}
+
+    def launch_count(self) -> int:
+        return int(load_library().xbs_core_launch_count(self._h))
 
 
 @dataclasses.dataclass
