@@ -162,6 +162,18 @@ void ensure_batch(xbs_core* c, int64_t M) {
   ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NI), "cudaMalloc A_bwd");
   ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
   ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int16_t)), "cudaMalloc ecodes");
+  cudaFree(c->d_xc8);
+  cudaFree(c->d_e8);
+  c->d_xc8 = c->d_e8 = nullptr;
+  if (c->opt.act_bits <= 8 && c->opt.error_bits <= 8) {
+    c->KA = ((c->g.K + 127) / 128) * 128;
+    c->NA = ((c->g.N + 127) / 128) * 128;
+    c->M_cap8 = ((cap + 127) / 128) * 128;
+    ck(cudaMalloc(&c->d_xc8, size_t(c->M_cap8) * c->KA), "cudaMalloc xc8");
+    ck(cudaMalloc(&c->d_e8, 2 * size_t(c->M_cap8) * c->NA), "cudaMalloc e8");
+    ck(cudaMemsetAsync(c->d_xc8, 0, size_t(c->M_cap8) * c->KA, c->stream), "memset");
+    ck(cudaMemsetAsync(c->d_e8, 0, 2 * size_t(c->M_cap8) * c->NA, c->stream), "memset");
+  }
   c->M_cap = cap;
 }
 
@@ -274,7 +286,7 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, doub
   }
   {
     StageScope st(c, XBS_STAGE_DW);
-    xbs::launch_dw(c, M, gd, c->stream);
+    if (c->kernel == 1 || !xbs::launch_dw_tc(c, M, gd, c->stream)) xbs::launch_dw(c, M, gd, c->stream);
     c->launches += 1;
   }
   c->have_grad = true;
@@ -510,6 +522,8 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_Ab);
   cudaFree(c->d_xcodes);
   cudaFree(c->d_ecodes);
+  cudaFree(c->d_xc8);
+  cudaFree(c->d_e8);
   cudaFree(c->d_io_in);
   cudaFree(c->d_io_out);
   for (auto& p : c->pending) {

@@ -1,0 +1,182 @@
+// K3a: the digital weight gradient dW = x_values^T dy_q / grad_divisor
+// (layers.cpp:304) as an exact integer outer product on tcgen05 kind::i8:
+//     S[i, j] = sum_b xcode[b, i] * (plus[b, j] - minus[b, j])
+// with the u8 activation codes as A (MN-major) and the u8 plus / minus error
+// magnitudes side by side in N (MN-major), s32 accumulation in TMEM (exact
+// for batch <= 33025), then dW = ((S * sx) * step_e) / grad_divisor in fp64
+// (the snapped-mode contract), written row-major [i][j].
+//
+// Unit = 128 rows i x 128 columns j; K loop over 128-row batch blocks.
+// Warp roles as in the VMM kernels (TMA producer, MMA issuer, 8 epilogue
+// warps); the TMEM accumulator is double buffered so the epilogue's stores
+// overlap the next unit's MMAs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "xbs_internal.cuh"
+#include "xbs_tc_common.cuh"
+
+namespace xbs {
+namespace tc {
+
+namespace dw {
+constexpr int kThreads = 320;
+constexpr int kStages = 4;
+constexpr int kBox = 128 * 128;
+constexpr int kStage = 3 * kBox;  // A | plus | minus
+constexpr int kSmem = kStages * kStage + 1024 + 256;
+}  // namespace dw
+
+struct DwArgs {
+  int K, N, num_ib, num_units, kblocks;
+  int64_t Mcap8;
+  double sx, lev_e, gd;
+  const DevScalars* sc;
+  double* dW;
+};
+
+__global__ void __launch_bounds__(dw::kThreads, 1)
+    k_dw_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapE, const DwArgs a) {
+  using namespace dw;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* t_full = empty + kStages;
+  uint64_t* t_empty = t_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 8);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      uint32_t st = 0, ph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        const int ib = u % a.num_ib, jb = u / a.num_ib;
+        for (int kb = 0; kb < a.kblocks; ++kb) {
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_expect_tx(&full[st], kStage);
+          uint8_t* dst = smem + st * kStage;
+          tma_load_2d(dst, &mapA, &full[st], ib * 128, kb * 128);
+          tma_load_2d(dst + kBox, &mapE, &full[st], jb * 128, kb * 128);
+          tma_load_2d(dst + 2 * kBox, &mapE, &full[st], jb * 128, int(a.Mcap8) + kb * 128);
+          if (++st == kStages) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: A MN-major (i), B MN-major (plus | minus)
+      constexpr uint32_t idesc = idesc_i8(128, 256, true) | (1u << 15);
+      uint32_t st = 0, ph = 0, ab = 0, abph = 0;
+      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+        mbar_wait(&t_empty[ab], abph ^ 1);
+        tc_fence_after();
+        const uint32_t td = tmem + ab * 256;
+        for (int kb = 0; kb < a.kblocks; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t s0 = smem_u32(smem + st * kStage);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ad = sdesc(s0 + 4096 * ks, kBox, 1024, 2);
+            const uint64_t bd = sdesc(s0 + kBox + 4096 * ks, kBox, 1024, 2);
+            umma_i8(td, ad, bd, idesc, (kb | ks) != 0);
+          }
+          umma_commit(&empty[st]);
+          if (++st == kStages) { st = 0; ph ^= 1; }
+        }
+        umma_commit(&t_full[ab]);
+        if (++ab == 2) { ab = 0; abph ^= 1; }
+      }
+    }
+  } else {  // epilogue
+    const int lg = warp & 3, ch = (warp - 2) >> 2;
+    const double se = a.sc->se;
+    const double step_e = se > 0 ? se / a.lev_e : 0.0;
+    uint32_t ab = 0, abph = 0;
+    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      const int ib = u % a.num_ib, jb = u / a.num_ib;
+      const int i = ib * 128 + 32 * lg + lane;
+      mbar_wait(&t_full[ab], abph);
+      tc_fence_after();
+      const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 64 * ch;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pv[16], mv[16];
+        tmem_ld16(ta + 16 * q, pv);
+        tmem_ld16(ta + 128 + 16 * q, mv);
+        tmem_wait_ld();
+        if (q == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[ab]);
+        }
+        const int j0 = jb * 128 + 64 * ch + 16 * q;
+        if (i < a.K) {
+          double* row = a.dW + int64_t(i) * a.N;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int S = int(pv[jj]) - int(mv[jj]);
+            if (j0 + jj < a.N) row[j0 + jj] = ((double(S) * a.sx) * step_e) / a.gd;
+          }
+        }
+      }
+      if (++ab == 2) { ab = 0; abph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo);
+int num_sms();
+
+}  // namespace tc
+
+bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) {
+  using namespace tc;
+  if (!c->d_xc8 || !c->d_e8 || M > 32768 || M == 0) return false;
+  const int64_t Mp = ((M + 127) / 128) * 128;
+  CUtensorMap mA, mE;
+  if (!make_map_u8(&mA, c->d_xc8, uint64_t(c->KA), uint64_t(Mp), 128, 128)) return false;
+  if (!make_map_u8(&mE, c->d_e8, uint64_t(c->NA), uint64_t(2 * c->M_cap8), 128, 128)) return false;
+  DwArgs a{};
+  a.K = c->g.K;
+  a.N = c->g.N;
+  a.num_ib = c->KA / 128;
+  a.num_units = a.num_ib * (c->NA / 128);
+  a.kblocks = int(Mp / 128);
+  a.Mcap8 = c->M_cap8;
+  a.sx = c->sx;
+  a.lev_e = c->lev_e;
+  a.gd = grad_divisor;
+  a.sc = c->d_sc;
+  a.dW = c->d_dW;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, dw::kSmem);
+    attr = true;
+  }
+  const int grid = std::min(a.num_units, num_sms());
+  k_dw_tc<<<grid, dw::kThreads, dw::kSmem, st>>>(mA, mE, a);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+}  // namespace xbs

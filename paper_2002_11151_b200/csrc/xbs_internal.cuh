@@ -110,6 +110,13 @@ struct xbs_core {
   uint8_t* d_Ab = nullptr;   // 2 * rowsB * NI
   uint16_t* d_xcodes = nullptr;
   int16_t* d_ecodes = nullptr;
+  // u8 operands of the tcgen05 dW GEMM (act/error bits <= 8): x codes
+  // [Mcap8][KA], error magnitudes [plus | minus][Mcap8][NA]; K, N padded to
+  // 128 (zero), batch padded to 128 (rows >= M zeroed per call)
+  uint8_t* d_xc8 = nullptr;
+  uint8_t* d_e8 = nullptr;
+  int KA = 0, NA = 0;
+  int64_t M_cap8 = 0;
   double* d_io_in = nullptr;   // host-API staging (M x max(K,N))
   double* d_io_out = nullptr;
   int64_t io_cap = 0;
@@ -150,4 +157,5 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 // tcgen05 kernels (xbs_vmm_tc.cu); return false if the shape is not covered
 bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
 bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
+bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
 }  // namespace xbs

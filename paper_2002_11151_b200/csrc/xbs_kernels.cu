@@ -49,6 +49,23 @@ __device__ __forceinline__ T warp_max(T v) {
 // ------------------------------------------------- conductance conversion
 // mapping.cpp:39-58 + aam.cpp:14-31 + snap: one device (s, p, global padded
 // i, j) from its master value u.
+__device__ __forceinline__ uint32_t convert_device_rc(const RegenP& rp, const Geo& g, double u, int s, int p,
+                                                      int i, int j, int r, int c) {
+  double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
+  if (rp.sigma != 0.0) {
+    const int64_t idx = int64_t(i) * g.Np + j;
+    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, uint64_t(idx), 0));
+    m = m > 1e-12 ? m : 1e-12;
+    gv = fmin(gv * m, rp.g_max);
+  }
+  if (rp.aam) {
+    const double rpth = rp.r_source + double(c + 1) * rp.r_row + double(g.tile_rows - r) * rp.r_col + rp.r_sense;
+    if (gv == 0.0) gv = 0.0;
+    else if (rpth != 0.0) gv = 1.0 / (1.0 / gv + rpth);
+  }
+  return uint32_t(rint(ldexp(gv, rp.snap_e)));
+}
+
 __device__ __forceinline__ uint32_t convert_device(const RegenP& rp, const Geo& g, double u, int s, int p,
                                                    int i, int j) {
   double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
@@ -201,10 +218,113 @@ __global__ void k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ d
   }
 }
 
+// Same arithmetic as k_update, laid out for HBM: blockIdx.y = weight row i,
+// each thread owns 4 consecutive columns j (coalesced fp64 dW / master
+// read-modify-write) and emits each digit plane row segment as one packed
+// 32-bit store.  Per weight it moves 8 B dW + 16 B x S master + 8 B x S
+// conductance digits (both polarities) -- the K3b roofline bytes.
+__global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
+                                                 double* __restrict__ master, uint8_t* __restrict__ digits,
+                                                 DevScalars* sc) {
+  const double range = rp.range;
+  double wmax = 0.0, dwmax = 0.0;
+  const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
+    if (j0 >= g.N) break;
+    const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
+    int tcj[4], cj[4];
+    {
+      int tc = j0 / g.tile_cols, c = j0 - tc * g.tile_cols;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        tcj[jj] = tc;
+        cj[jj] = c;
+        if (++c == g.tile_cols) { c = 0; ++tc; }
+      }
+    }
+    const bool vec = (g.tile_cols % 4 == 0) && (j0 + 3 < g.N);
+    const int nj = min(4, g.N - j0);
+    double dg[4], acc[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const double dw = jj < nj ? dW[int64_t(i) * g.N + j0 + jj] : 0.0;
+      dwmax = fmax(dwmax, fabs(dw));
+      dg[jj] = dw * up.factor;  // scale_gradient (update.cpp:16-24)
+      acc[jj] = 0.0;
+    }
+    for (int s = g.S - 1; s >= 0; --s) {
+      double* urow = &master[(size_t(s) * g.Kp + i) * g.Np + j0];
+      uint32_t q[2][4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        if (jj >= nj) {
+          q[0][jj] = q[1][jj] = 0;
+          continue;
+        }
+        const double ui = urow[jj];
+        double du = dg[jj];
+        if (!up.linear && dg[jj] != 0.0) {
+          const bool pos_active = ui > 0.0 || (ui == 0.0 && dg[jj] < 0.0);
+          const double dev_arg = pos_active ? -dg[jj] : dg[jj];
+          const double gg = rp.g_min + fabs(ui);
+          if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
+          const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
+          const double nl = dev_arg * exp(-up.v * x);
+          du = pos_active ? -nl : nl;
+        }
+        double noise = 0.0;
+        if (up.gamma != 0.0 && dg[jj] != 0.0) {
+          const double sigma = up.gamma * sqrt(range * fabs(dg[jj]));
+          if (sigma != 0.0)
+            noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s),
+                                                 uint64_t(int64_t(i) * g.N + j0 + jj)));
+        }
+        double nu = ui - up.lr * (du + noise);
+        if (nu > range) nu = range;
+        if (nu < -range) nu = -range;
+        urow[jj] = nu;
+        acc[jj] = acc[jj] * double(1u << g.db) + nu;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) q[p][jj] = convert_device_rc(rp, g, nu, s, p, i, j0 + jj, r, cj[jj]);
+      }
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        if (vec) {
+          uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const uint32_t lo = q[p][jj] % 65025u, hi = q[p][jj] / 65025u;
+            w[0] |= (lo % 255u) << (8 * jj);
+            w[1] |= (lo / 255u) << (8 * jj);
+            w[2] |= (hi % 255u) << (8 * jj);
+            w[3] |= (hi / 255u) << (8 * jj);
+          }
+          const size_t off = size_t(r) * g.C + cj[0];
+#pragma unroll
+          for (int d = 0; d < 4; ++d)
+            *reinterpret_cast<uint32_t*>(digits + g.tile_digit_offset(s, p, tr, tcj[0], d) + off) = w[d];
+        } else {
+          for (int jj = 0; jj < nj; ++jj) store_digits(digits, g, s, p, i, j0 + jj, q[p][jj]);
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (jj < nj) wmax = fmax(wmax, fabs(up.wfactor * acc[jj]));
+  }
+  wmax = warp_max(wmax);
+  dwmax = warp_max(dwmax);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(&sc->wmax, wmax);
+    atomic_max_pos(&sc->dwmax, dwmax);
+  }
+}
+
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st) {
-  const int64_t n = int64_t(c->g.K) * c->g.N;
-  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
-  k_update<<<blocks, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
+  const int bx = (c->g.N + 4 * 256 - 1) / (4 * 256);
+  const int by = std::min(c->g.K, 65535);
+  k_update4<<<dim3(bx, by), 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
+  (void)k_update;
 }
 
 // implied_weights() (mapping.cpp:70-81) -> K x N row-major
@@ -246,7 +366,8 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 // x: M x K column-major (ld = M).  One thread per (b, 16-column chunk of the
 // device-padded K axis); writes codes and both A planes (bits, 255*bits).
 __global__ void k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF, double step, double levels,
-                         uint16_t* __restrict__ codes, uint8_t* __restrict__ A) {
+                         uint16_t* __restrict__ codes, uint8_t* __restrict__ A, uint8_t* __restrict__ c8,
+                         int ld8) {
   const int chunks = g.KI / 16;
   const int64_t n = M * chunks;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
@@ -265,6 +386,7 @@ __global__ void k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t
         if (v > levels) v = levels;
         code = uint32_t(v);
         codes[b * g.K + i] = uint16_t(code);
+        if (c8) c8[b * ld8 + i] = uint8_t(code);
       }
       cv[q] = code;
     }
@@ -299,8 +421,12 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
   const double levels = double((1 << c->opt.act_bits) - 1);
+  if (c->d_xc8) {  // u8 code plane for the tcgen05 dW: rows [M, Mpad) must read 0
+    const int64_t Mp = ((M + 127) / 128) * 128;
+    if (Mp > M) cudaMemsetAsync(c->d_xc8 + M * c->KA, 0, size_t(Mp - M) * c->KA, st);
+  }
   k_prep_x<<<blocks, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
-                                    c->d_Af);
+                                    c->d_Af, c->d_xc8, c->KA);
 }
 
 // ----------------------------------------------------------------- prep_dy
@@ -308,7 +434,8 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
 // plus/minus planes (layers.cpp:316-331).  Row (b*TPe + k)*2 + phi, phi=0
 // plus, phi=1 minus.
 __global__ void k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB, double levels,
-                          const DevScalars* __restrict__ sc, int16_t* __restrict__ ecodes, uint8_t* __restrict__ A) {
+                          const DevScalars* __restrict__ sc, int16_t* __restrict__ ecodes, uint8_t* __restrict__ A,
+                          uint8_t* __restrict__ e8, int64_t plane8, int ld8) {
   const double se = sc->se;
   const double step = se / levels;
   const int chunks = g.NI / 16;
@@ -332,6 +459,10 @@ __global__ void k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64
           sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
         }
         ecodes[b * g.N + j] = int16_t(sm);
+        if (e8) {
+          e8[b * ld8 + j] = uint8_t(sm > 0 ? sm : 0);
+          e8[plane8 + b * ld8 + j] = uint8_t(sm < 0 ? -sm : 0);
+        }
       }
       pv[q] = sm > 0 ? uint32_t(sm) : 0u;
       mv[q] = sm < 0 ? uint32_t(-sm) : 0u;
@@ -372,8 +503,16 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
   const int64_t n = M * (c->g.NI / 16);
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  const int64_t plane8 = c->M_cap8 * c->NA;
+  if (c->d_e8) {
+    const int64_t Mp = ((M + 127) / 128) * 128;
+    if (Mp > M) {
+      cudaMemsetAsync(c->d_e8 + M * c->NA, 0, size_t(Mp - M) * c->NA, st);
+      cudaMemsetAsync(c->d_e8 + plane8 + M * c->NA, 0, size_t(Mp - M) * c->NA, st);
+    }
+  }
   k_prep_dy<<<blocks, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
-                                     c->d_ecodes, c->d_Ab);
+                                     c->d_ecodes, c->d_Ab, c->d_e8, plane8, c->NA);
 }
 
 // ---------------------------------------------------------------------- dW

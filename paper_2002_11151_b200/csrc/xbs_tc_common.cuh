@@ -38,6 +38,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Wait for the single-thread roles (TMA producer, MMA issuer): the thread is
+// suspended in hardware for up to ~0.5 us per try instead of spinning, so
+// its warp does not steal issue slots from the epilogue warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(500)
+        : "memory");
+  } while (!done);
+}
 
 // ------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
@@ -105,6 +121,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 
 // ------------------------------------------------------- ADC epilogue math
 // A column current on the snapped grid is n = hi*65025 + lo units of
@@ -124,7 +145,7 @@ constexpr float kDelta = 1.0f / 4096.0f;
 constexpr float kMagic23 = 8388608.0f;     // 2^23
 constexpr float kRint = 12582912.0f;       // 1.5 * 2^23
 
-__device__ __noinline__ float adc_exact(uint32_t hi, uint32_t lo, double i_fs, double maxc_d, int sh) {
+static __device__ __noinline__ float adc_exact(uint32_t hi, uint32_t lo, double i_fs, double maxc_d, int sh) {
   const long long n = (long long)hi * 65025ll + (long long)lo;
   const double I = ldexp(double(n), sh);
   const double scaled = I / i_fs * maxc_d;
@@ -144,6 +165,74 @@ __device__ __forceinline__ float adc_fast(uint32_t hi, uint32_t lo, const AdcCon
   const float r = fabsf(__fsub_rn(x, t));
   if (r > 0.5f - kDelta) near |= bit;
   return t;
+}
+
+// fp32 fast path without per-element boundary bookkeeping: returns the
+// rounded code and folds |fraction - rint| into a running max `m`.
+__device__ __forceinline__ float adc_fast_m(uint32_t hi, uint32_t lo, const AdcConst& k, float& m) {
+  const float hf = __fsub_rn(__int_as_float(int(hi | 0x4B000000u)), kMagic23);
+  const float lt = __fmaf_rn(__int_as_float(int(lo | 0x4B000000u)), k.c_lo, k.k_lo);
+  float x = __fmaf_rn(hf, k.c_hi, lt);
+  x = fminf(x, k.maxc);
+  const float t = __fsub_rn(__fadd_rn(x, kRint), kRint);
+  m = fmaxf(m, fabsf(__fsub_rn(x, t)));
+  return t;
+}
+
+// One 8-column chunk of a chain: TMEM -> registers, ADC, P[base+j] += w*code.
+// If any lane of the warp saw a fraction within kDelta of 1/2 the whole
+// chunk is re-checked element by element and the near-boundary codes are
+// replaced by the exact fp64 evaluation (P += w * (exact - fast)).
+template <int kN>
+__device__ __forceinline__ void adc_chunk8(uint32_t ta_lo, uint32_t ta_hi, const AdcConst& k, float w,
+                                           float (&P)[kN], int base, uint32_t& exact_ctr, uint64_t* release) {
+  uint32_t lo[8], hi[8];
+  tmem_ld8(ta_lo, lo);
+  tmem_ld8(ta_hi, hi);
+  tmem_wait_ld();
+  if (release) {  // last TMEM read of this accumulator buffer by this warp
+    tc_fence_before();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(release);
+  }
+  float m = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) P[base + j] = __fmaf_rn(adc_fast_m(hi[j], lo[j], k, m), w, P[base + j]);
+  if (__any_sync(0xffffffffu, m > 0.5f - kDelta)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t near = 0;
+      const float fast = adc_fast(hi[j], lo[j], k, near, 1u);
+      if (near) {
+        ++exact_ctr;
+        const float ex = adc_exact(hi[j], lo[j], k.i_fs, k.maxc_d, k.sh);
+        P[base + j] = __fmaf_rn(__fsub_rn(ex, fast), w, P[base + j]);
+      }
+    }
+  }
+}
+
+// 16 conversions accumulated straight into P[j] += w * code: fast path for
+// all, then for the (rare) near-boundary ones the exact fp64 code replaces
+// the fast one (P += w * (exact - fast); all operands are exact integers).
+// The warp takes the fix-up branch only when one of its lanes needs it.
+template <int kN>
+__device__ __forceinline__ void adc_accum16(const uint32_t (&hi)[16], const uint32_t (&lo)[16], const AdcConst& k,
+                                            float w, float (&P)[kN], int base, uint32_t& exact_ctr) {
+  uint32_t near = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) P[base + j] = __fmaf_rn(adc_fast(hi[j], lo[j], k, near, 1u << j), w, P[base + j]);
+  if (__any_sync(0xffffffffu, near != 0)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if ((near >> j) & 1u) {
+        ++exact_ctr;
+        uint32_t dummy = 0;
+        const float fast = adc_fast(hi[j], lo[j], k, dummy, 1u);
+        const float ex = adc_exact(hi[j], lo[j], k.i_fs, k.maxc_d, k.sh);
+        P[base + j] = __fmaf_rn(__fsub_rn(ex, fast), w, P[base + j]);
+      }
+  }
 }
 
 // 16 conversions: fast path for all, exact fp64 re-evaluation only for the

@@ -31,7 +31,8 @@
 namespace xbs {
 namespace tc {
 
-constexpr int kThreads = 320;
+constexpr int kEpiWarps = 16;                 // 4 per SM sub-partition
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer, MMA issuer
 constexpr int kAStages = 2, kBStages = 2;
 constexpr int kPlane = 128 * 128;          // one 128x128 u8 digit / bit box
 constexpr int kAStage = 2 * kPlane;        // bits + 255*bits
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 8);
+      mbar_init(&t_empty[i], kEpiWarps);
     }
     mbar_fence_init();
   }
@@ -97,14 +98,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mb = u % a.num_mb, nb = u / a.num_mb;
         const int tc = nb / nsplit, h = nb % nsplit;
         for (int tr = 0; tr < a.GR; ++tr) {
-          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_wait_sleep(&a_empty[as], aph ^ 1);
           mbar_expect_tx(&a_full[as], kAStage);
           tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tr * a.R, mb * 128);
           tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tr * a.R, int(a.rowsF) + mb * 128);
           if (++as == kAStages) { as = 0; aph ^= 1; }
           for (int s = 0; s < a.S; ++s)
             for (int p = 0; p < 2; ++p) {
-              mbar_wait(&b_empty[bs], bph ^ 1);
+              mbar_wait_sleep(&b_empty[bs], bph ^ 1);
               mbar_expect_tx(&b_full[bs], kBStage);
               const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R;
               uint8_t* dst = sB + bs * kBStage;
@@ -123,12 +124,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
         for (int tr = 0; tr < a.GR; ++tr) {
-          mbar_wait(&a_full[as], aph);
+          mbar_wait_sleep(&a_full[as], aph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + as * kAStage);
           for (int sp = 0; sp < 2 * a.S; ++sp) {
-            mbar_wait(&t_empty[ab], abph ^ 1);
-            mbar_wait(&b_full[bs], bph);
+            mbar_wait_sleep(&t_empty[ab], abph ^ 1);
+            mbar_wait_sleep(&b_full[bs], bph);
             tc_fence_after();
             const uint32_t b0 = smem_u32(sB + bs * kBStage);
             const uint32_t td = tmem + ab * 256;
@@ -151,48 +152,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
+    constexpr int kCols = 128 / (kEpiWarps / 4);  // output columns per epilogue warp
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int mb = u % a.num_mb, nb = u / a.num_mb;
-      float P[64];
+      float P[kCols];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) P[j] = 0.f;
+      for (int j = 0; j < kCols; ++j) P[j] = 0.f;
       for (int tr = 0; tr < a.GR; ++tr)
         for (int s = 0; s < a.S; ++s)
           for (int p = 0; p < 2; ++p) {
             const float w = p == 0 ? float(1 << (s * a.db)) : -float(1 << (s * a.db));
             mbar_wait(&t_full[ab], abph);
             tc_fence_after();
-            const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 64 * ch;
+            const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kCols * ch;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t lo[16], hi[16];
-              tmem_ld16(ta + 16 * q, lo);
-              tmem_ld16(ta + 128 + 16 * q, hi);
-              tmem_wait_ld();
-              if (q == 3) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&t_empty[ab]);
-              }
-              float t[16];
-              adc_chunk16(hi, lo, k, t, exact);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) P[16 * q + j] = __fmaf_rn(t[j], w, P[16 * q + j]);
-            }
+            for (int q = 0; q < kCols / 8; ++q)
+              adc_chunk8(ta + 8 * q, ta + 128 + 8 * q, k, w, P, 8 * q, exact,
+                         q == kCols / 8 - 1 ? &t_empty[ab] : nullptr);
             if (++ab == 2) { ab = 0; abph ^= 1; }
           }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
       const int kk = ml % a.TPi;
       const int64_t b = int64_t(mb) * (128 / a.TPi) + ml / a.TPi;
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
+      for (int j = 0; j < kCols; ++j) {
         long long v = (long long)__float2ll_rn(P[j]) << kk;
         for (int o = 1; o < a.TPi; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int col = nb * 128 + 64 * ch + j;
+        const int col = nb * 128 + kCols * ch + j;
         const int tc = col / a.C, c = col % a.C;
         const int jg = tc * a.tile_cols + c;
         if (kk == 0 && b < a.M && c < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v) * a.k_out;
@@ -248,6 +238,11 @@ static int sm_count() {
   }
   return n;
 }
+
+bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+  return make_map(m, base, inner, outer, bi, bo);
+}
+int num_sms() { return sm_count(); }
 
 AdcConst make_adc_const(const xbs_core* c) {
   AdcConst k{};
@@ -358,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 8);
+      mbar_init(&t_empty[i], kEpiWarps);
     }
     mbar_fence_init();
   }
@@ -380,13 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mb = u % a.num_mb, rb = u / a.num_mb;
         const int tr = rb / rhalves, rh = rb % rhalves;
         for (int tc = 0; tc < a.GC; ++tc) {
-          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_wait_sleep(&a_empty[as], aph ^ 1);
           mbar_expect_tx(&a_full[as], kAStage);
           tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tc * a.C, mb * 128);
           tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tc * a.C, int(a.rowsB) + mb * 128);
           if (++as == kAStages) { as = 0; aph ^= 1; }
           for (int s = 0; s < a.S; ++s) {
-            mbar_wait(&b_empty[bs], bph ^ 1);
+            mbar_wait_sleep(&b_empty[bs], bph ^ 1);
             mbar_expect_tx(&b_full[bs], kBStage);
             uint8_t* dst = sB + bs * kBStage;
             // smem order [dh][p][acc][64 r][128 c]; digit d = 2*acc + dh
@@ -410,12 +405,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
         for (int tc = 0; tc < a.GC; ++tc) {
-          mbar_wait(&a_full[as], aph);
+          mbar_wait_sleep(&a_full[as], aph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + as * kAStage);
           for (int s = 0; s < a.S; ++s) {
-            mbar_wait(&t_empty[ab], abph ^ 1);
-            mbar_wait(&b_full[bs], bph);
+            mbar_wait_sleep(&t_empty[ab], abph ^ 1);
+            mbar_wait_sleep(&b_full[bs], bph);
             tc_fence_after();
             const uint32_t b0 = smem_u32(sB + bs * kBStage);
             const uint32_t td = tmem + ab * 256;
@@ -438,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
+    constexpr int kRows = 64 / (kEpiWarps / 4);  // output rows per epilogue warp
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
     const int phi = ml & 1;
@@ -450,34 +446,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int mb = u % a.num_mb, rb = u / a.num_mb;
       const int tr = rb / rhalves, rh = rb % rhalves;
-      float P[32];
+      float P[kRows];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) P[j] = 0.f;
+      for (int j = 0; j < kRows; ++j) P[j] = 0.f;
       for (int tc = 0; tc < a.GC; ++tc)
         for (int s = 0; s < a.S; ++s) {
           const float w = float(1 << (s * a.db));
           mbar_wait(&t_full[ab], abph);
           tc_fence_after();
-          const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 32 * ch;
+          const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kRows * ch;
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
             const float ws = p == phi ? w : -w;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              uint32_t lo[16], hi[16];
-              tmem_ld16(ta + p * 128 + 16 * q, lo);
-              tmem_ld16(ta + p * 128 + 64 + 16 * q, hi);
-              tmem_wait_ld();
-              if (p == 1 && q == 1) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&t_empty[ab]);
-              }
-              float t[16];
-              adc_chunk16(hi, lo, k, t, exact);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) P[16 * q + j] = __fmaf_rn(t[j], ws, P[16 * q + j]);
-            }
+            for (int q = 0; q < kRows / 8; ++q)
+              adc_chunk8(ta + p * 128 + 8 * q, ta + p * 128 + 64 + 8 * q, k, ws, P, 8 * q, exact,
+                         (p == 1 && q == kRows / 8 - 1) ? &t_empty[ab] : nullptr);
           }
           if (++ab == 2) { ab = 0; abph ^= 1; }
         }
@@ -486,10 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kk = (ml % grp) >> 1;
       const int64_t b = int64_t(mb) * (128 / grp) + ml / grp;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < kRows; ++j) {
         long long v = (long long)__float2ll_rn(P[j]) << kk;
         for (int o = 1; o < grp; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int rloc = rh * 64 + 32 * ch + j;
+        const int rloc = rh * 64 + kRows * ch + j;
         const int ig = tr * a.tile_rows + rloc;
         if ((ml % grp) == 0 && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v) * k_out;
       }
