@@ -1,2 +1,2 @@
 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_fwd_tc|k_bwd_tc|k_dw_tc|k_update4" -s 4 -c 4 -o gpurun_out/prof_all python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1; tail -2 gpurun_out/ncu_full.log
+ncu --set full --clock-control none --import-source on -k regex:"k_fwd_tc" -s 1 -c 1 -o gpurun_out/prof_fwd python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "xbs_internal.cuh"
@@ -47,8 +48,10 @@ struct FwdArgs {
   AdcConst adc;
   double* y;
   unsigned long long* ctr;  // [0] exact path, [1] conversions
+  int dbg;                  // perf experiments: 1 skip ADC math, 2 skip MMAs
 };
 
+template <int DBG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -133,14 +136,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t b0 = smem_u32(sB + bs * kBStage);
             const uint32_t td = tmem + ab * 256;
+            if (!(a.dbg & 2)) {
 #pragma unroll
-            for (int dh = 0; dh < 2; ++dh)
+              for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {
-                const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
-                const uint64_t bd = sdesc(b0 + dh * 2 * kPlane + 4096 * ks, kPlane, 1024, 2);
-                umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
-              }
+                for (int ks = 0; ks < 4; ++ks) {
+                  const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
+                  const uint64_t bd = sdesc(b0 + dh * 2 * kPlane + 4096 * ks, kPlane, 1024, 2);
+                  umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
+                }
+            }
             umma_commit(&b_empty[bs]);
             if (++bs == kBStages) { bs = 0; bph ^= 1; }
             umma_commit(&t_full[ab]);
@@ -157,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ml = 32 * lg + lane;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
+    const AdcConst2 c2 = make_const2(k);
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int mb = u % a.num_mb, nb = u / a.num_mb;
       float P[kCols];
@@ -166,13 +172,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < a.S; ++s)
           for (int p = 0; p < 2; ++p) {
             const float w = p == 0 ? float(1 << (s * a.db)) : -float(1 << (s * a.db));
-            mbar_wait(&t_full[ab], abph);
+            mbar_wait_sleep(&t_full[ab], abph);
             tc_fence_after();
             const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kCols * ch;
+            if constexpr (DBG == 1) {
+              adc_pipeline<kCols / 8, kCols / 2, 1>([&](int q) { return ta + 8 * q; },
+                                                    [&](int q) { return ta + 128 + 8 * q; },
+                                                    [](int q) { return 4 * q; }, [&](int) { return 0ull; }, k, c2,
+                                                    *reinterpret_cast<uint64_t(*)[kCols / 2]>(P), exact,
+                                                    &t_empty[ab]);
+            } else {
 #pragma unroll
-            for (int q = 0; q < kCols / 8; ++q)
-              adc_chunk8(ta + 8 * q, ta + 128 + 8 * q, k, w, P, 8 * q, exact,
-                         q == kCols / 8 - 1 ? &t_empty[ab] : nullptr);
+              for (int q = 0; q < kCols / 8; ++q)
+                adc_chunk8s(ta + 8 * q, ta + 128 + 8 * q, k, w, P, 8 * q, exact,
+                            q == kCols / 8 - 1 ? &t_empty[ab] : nullptr);
+            }
             if (++ab == 2) { ab = 0; abph ^= 1; }
           }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
@@ -250,6 +264,16 @@ AdcConst make_adc_const(const xbs_core* c) {
   k.c_lo = float(cn);
   k.c_hi = float(65025.0 * cn);
   k.k_lo = -8388608.0f * k.c_lo;
+  k.k2 = float(-8388608.0 * (double(k.c_lo) + double(k.c_hi)));
+  // Error bound of the fast x (in code units): rounding of k2 and of the
+  // inner FFMA (each <= 2^23 (c_hi + c_lo) 2^-24), of x itself (<= 2^-24 x,
+  // x < 2 maxc before the saturation check) plus the float constants'
+  // relative error on n (2 * 2^-24 x).  delta = 4x that bound, >= 2^-12.
+  const double maxc = double(c->adc.maxc);
+  const double err = 3.0 * 0x1p-24 * (maxc + 1.0);  // fast-x error on the unclamped range
+  const double delta = std::max(0x1p-12, 4.0 * err);
+  k.thr = float(0.5 - delta);
+  k.sat = float(maxc - 0.5 - delta);
   k.maxc = float(c->adc.maxc);
   k.sh = c->adc.sh;
   k.maxc_i = c->adc.maxc;
@@ -289,13 +313,16 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.adc = make_adc_const(c);
   a.y = d_y;
   a.ctr = &c->d_sc->exact_path;
+  a.dbg = getenv("XBS_DBG_FWD") ? atoi(getenv("XBS_DBG_FWD")) : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_fwd_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   const int grid = std::min(a.num_units, sm_count());
-  k_fwd_tc<<<grid, kThreads, kSmem, st>>>(mA, mB, a);
+  if (a.dbg & 1) k_fwd_tc<1><<<grid, kThreads, kSmem, st>>>(mA, mB, a);
+  else k_fwd_tc<0><<<grid, kThreads, kSmem, st>>>(mA, mB, a);
   return cudaPeekAtLastError() == cudaSuccess;
 }
 
@@ -439,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int phi = ml & 1;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
+    const AdcConst2 c2 = make_const2(k);
     const double se = a.sc->se;
     const double step_e = se > 0 ? se / a.lev_e : 0.0;
     double k_out = step_e * a.F / a.vu;  // layers.cpp:375-377
@@ -452,17 +480,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int tc = 0; tc < a.GC; ++tc)
         for (int s = 0; s < a.S; ++s) {
           const float w = float(1 << (s * a.db));
-          mbar_wait(&t_full[ab], abph);
+          const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
+          const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
+          mbar_wait_sleep(&t_full[ab], abph);
           tc_fence_after();
           const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kRows * ch;
+          constexpr int QP = kRows / 8;  // chunks per polarity
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            const float ws = p == phi ? w : -w;
-#pragma unroll
-            for (int q = 0; q < kRows / 8; ++q)
-              adc_chunk8(ta + p * 128 + 8 * q, ta + p * 128 + 64 + 8 * q, k, ws, P, 8 * q, exact,
-                         (p == 1 && q == kRows / 8 - 1) ? &t_empty[ab] : nullptr);
-          }
+          for (int q = 0; q < 2 * QP; ++q)
+            adc_chunk8s(ta + (q / QP) * 128 + 8 * (q % QP), ta + (q / QP) * 128 + 64 + 8 * (q % QP), k,
+                        q < QP ? wpos : wneg, P, 8 * (q % QP), exact, q == 2 * QP - 1 ? &t_empty[ab] : nullptr);
           if (++ab == 2) { ab = 0; abph ^= 1; }
         }
       // combine the 2*TPe (plane, phase) lanes of each batch row

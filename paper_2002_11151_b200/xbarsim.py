@@ -21,7 +21,7 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libxbarsim_b200.so")
+LIB_PATH = os.environ.get("XBS_LIB_PATH") or os.path.join(_HERE, "_lib", "libxbarsim_b200.so")
 
 
 # ----------------------------------------------------------------- errors.hpp
