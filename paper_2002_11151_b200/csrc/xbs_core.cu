@@ -156,8 +156,8 @@ void ensure_batch(xbs_core* c, int64_t M) {
   c->d_Ab = nullptr;
   c->d_xcodes = nullptr;
   c->d_ecodes = nullptr;
-  const int64_t rowsF = ((cap * c->g.TPi + 127) / 128) * 128;
-  const int64_t rowsB = ((cap * c->g.TPe * 2 + 127) / 128) * 128;
+  const int64_t rowsF = xbs::rows_fwd(cap, c->g.TPi);
+  const int64_t rowsB = xbs::rows_bwd(cap, c->g.TPe);
   ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
   ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NI), "cudaMalloc A_bwd");
   ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");

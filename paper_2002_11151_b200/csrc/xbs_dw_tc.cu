@@ -145,9 +145,6 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo);
-int num_sms();
-
 }  // namespace tc
 
 bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) {

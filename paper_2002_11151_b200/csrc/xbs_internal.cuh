@@ -27,6 +27,11 @@ namespace xbs {
 // Snapped exactness grid (radix-255 variant): q <= kQMax.
 constexpr double kQMax = 4228250624.0;  // 65025^2 - 1
 
+// Rows of the forward / backward bit-plane operands, padded to whole
+// 256-row MMA unit pairs (rows beyond M*TP are zero).
+inline int64_t rows_fwd(int64_t M, int TPi) { return ((M * TPi + 255) / 256) * 256; }
+inline int64_t rows_bwd(int64_t M, int TPe) { return ((M * TPe * 2 + 255) / 256) * 256; }
+
 struct Geo {
   int K = 0, N = 0;                 // logical in / out features
   int tile_rows = 0, tile_cols = 0; // logical tile (MappingSpec)

@@ -410,7 +410,7 @@ __global__ void k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t
 }
 
 void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st) {
-  const int64_t rowsF = ((M * c->g.TPi + 127) / 128) * 128;
+  const int64_t rowsF = rows_fwd(M, c->g.TPi);
   // zero the M-padding rows once per call (rows [M*TPi, rowsF))
   const int64_t pad0 = M * c->g.TPi;
   if (rowsF > pad0) {
@@ -494,7 +494,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
   cudaMemsetAsync(&c->d_sc->wmax_in, 0, sizeof(unsigned long long), st);
   launch_absmax(d_dy, M * c->g.N, &c->d_sc->wmax_in, st);
   k_absmax_to_se<<<1, 1, 0, st>>>(c->d_sc, &c->d_sc->wmax_in);
-  const int64_t rowsB = ((M * c->g.TPe * 2 + 127) / 128) * 128;
+  const int64_t rowsB = rows_bwd(M, c->g.TPe);
   const int64_t pad0 = M * c->g.TPe * 2;
   if (rowsB > pad0) {
     cudaMemsetAsync(c->d_Ab + pad0 * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
@@ -575,7 +575,7 @@ void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st)
   const int64_t n = M * c->g.N;
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
-  const int64_t rowsF = ((M * c->g.TPi + 127) / 128) * 128;
+  const int64_t rowsF = rows_fwd(M, c->g.TPi);
   k_fwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, rowsF, c->d_Af, c->d_digits, c->k_out_fwd, d_y);
 }
 

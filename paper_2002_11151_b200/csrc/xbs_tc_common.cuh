@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+struct xbs_core;
 namespace xbs {
 namespace tc {
 
@@ -492,6 +493,12 @@ __device__ __forceinline__ void adc_chunk16(const uint32_t (&hi)[16], const uint
       }
   }
 }
+
+// host helpers (xbs_vmm_tc.cu)
+bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
+                 int swizzle_bytes = 128);
+int num_sms();
+AdcConst make_adc_const(const xbs_core* c);
 
 }  // namespace tc
 }  // namespace xbs

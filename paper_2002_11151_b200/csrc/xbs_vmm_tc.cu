@@ -40,177 +40,6 @@ constexpr int kAStage = 2 * kPlane;        // bits + 255*bits
 constexpr int kBStage = 4 * kPlane;        // d0 d2 | d1 d3
 constexpr int kSmem = kAStages * kAStage + kBStages * kBStage + 1024 + 256;
 
-struct FwdArgs {
-  int GR, GC, S, db, TPi, tile_cols, C, R, N;
-  int64_t M, rowsF;
-  int num_mb, num_units;
-  double k_out;
-  AdcConst adc;
-  double* y;
-  unsigned long long* ctr;  // [0] exact path, [1] conversions
-  int dbg;                  // perf experiments: 1 skip ADC math, 2 skip MMAs
-};
-
-template <int DBG>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kAStages * kAStage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kBStages * kBStage);
-  uint64_t* a_full = bars;
-  uint64_t* a_empty = a_full + kAStages;
-  uint64_t* b_full = a_empty + kAStages;
-  uint64_t* b_empty = b_full + kBStages;
-  uint64_t* t_full = b_empty + kBStages;
-  uint64_t* t_empty = t_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kAStages; ++i) {
-      mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], 1);
-    }
-    for (int i = 0; i < kBStages; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], kEpiWarps);
-    }
-    mbar_fence_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mapA);
-    tma_prefetch(&mapB);
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int nsplit = a.C / 128;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------------------------------- TMA producer
-      uint32_t as = 0, aph = 0, bs = 0, bph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        const int mb = u % a.num_mb, nb = u / a.num_mb;
-        const int tc = nb / nsplit, h = nb % nsplit;
-        for (int tr = 0; tr < a.GR; ++tr) {
-          mbar_wait_sleep(&a_empty[as], aph ^ 1);
-          mbar_expect_tx(&a_full[as], kAStage);
-          tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tr * a.R, mb * 128);
-          tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tr * a.R, int(a.rowsF) + mb * 128);
-          if (++as == kAStages) { as = 0; aph ^= 1; }
-          for (int s = 0; s < a.S; ++s)
-            for (int p = 0; p < 2; ++p) {
-              mbar_wait_sleep(&b_empty[bs], bph ^ 1);
-              mbar_expect_tx(&b_full[bs], kBStage);
-              const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R;
-              uint8_t* dst = sB + bs * kBStage;
-              tma_load_2d(dst + 0 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 0 * a.R);  // d0
-              tma_load_2d(dst + 1 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 2 * a.R);  // d2
-              tma_load_2d(dst + 2 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 1 * a.R);  // d1
-              tma_load_2d(dst + 3 * kPlane, &mapB, &b_full[bs], h * 128, row0 + 3 * a.R);  // d3
-              if (++bs == kBStages) { bs = 0; bph ^= 1; }
-            }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_i8(128, 256, /*b_mn_major=*/true);
-      uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        for (int tr = 0; tr < a.GR; ++tr) {
-          mbar_wait_sleep(&a_full[as], aph);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + as * kAStage);
-          for (int sp = 0; sp < 2 * a.S; ++sp) {
-            mbar_wait_sleep(&t_empty[ab], abph ^ 1);
-            mbar_wait_sleep(&b_full[bs], bph);
-            tc_fence_after();
-            const uint32_t b0 = smem_u32(sB + bs * kBStage);
-            const uint32_t td = tmem + ab * 256;
-            if (!(a.dbg & 2)) {
-#pragma unroll
-              for (int dh = 0; dh < 2; ++dh)
-#pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
-                  const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
-                  const uint64_t bd = sdesc(b0 + dh * 2 * kPlane + 4096 * ks, kPlane, 1024, 2);
-                  umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
-                }
-            }
-            umma_commit(&b_empty[bs]);
-            if (++bs == kBStages) { bs = 0; bph ^= 1; }
-            umma_commit(&t_full[ab]);
-            if (++ab == 2) { ab = 0; abph ^= 1; }
-          }
-          umma_commit(&a_empty[as]);
-          if (++as == kAStages) { as = 0; aph ^= 1; }
-        }
-      }
-    }
-  } else {  // ---------------------------------------------------- epilogue
-    constexpr int kCols = 128 / (kEpiWarps / 4);  // output columns per epilogue warp
-    const int lg = warp & 3, ch = (warp - 2) >> 2;
-    const int ml = 32 * lg + lane;
-    uint32_t ab = 0, abph = 0, exact = 0;
-    const AdcConst k = a.adc;
-    const AdcConst2 c2 = make_const2(k);
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int mb = u % a.num_mb, nb = u / a.num_mb;
-      float P[kCols];
-#pragma unroll
-      for (int j = 0; j < kCols; ++j) P[j] = 0.f;
-      for (int tr = 0; tr < a.GR; ++tr)
-        for (int s = 0; s < a.S; ++s)
-          for (int p = 0; p < 2; ++p) {
-            const float w = p == 0 ? float(1 << (s * a.db)) : -float(1 << (s * a.db));
-            mbar_wait_sleep(&t_full[ab], abph);
-            tc_fence_after();
-            const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kCols * ch;
-            if constexpr (DBG == 1) {
-              adc_pipeline<kCols / 8, kCols / 2, 1>([&](int q) { return ta + 8 * q; },
-                                                    [&](int q) { return ta + 128 + 8 * q; },
-                                                    [](int q) { return 4 * q; }, [&](int) { return 0ull; }, k, c2,
-                                                    *reinterpret_cast<uint64_t(*)[kCols / 2]>(P), exact,
-                                                    &t_empty[ab]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < kCols / 8; ++q)
-                adc_chunk8s(ta + 8 * q, ta + 128 + 8 * q, k, w, P, 8 * q, exact,
-                            q == kCols / 8 - 1 ? &t_empty[ab] : nullptr);
-            }
-            if (++ab == 2) { ab = 0; abph ^= 1; }
-          }
-      // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
-      const int kk = ml % a.TPi;
-      const int64_t b = int64_t(mb) * (128 / a.TPi) + ml / a.TPi;
-#pragma unroll
-      for (int j = 0; j < kCols; ++j) {
-        long long v = (long long)__float2ll_rn(P[j]) << kk;
-        for (int o = 1; o < a.TPi; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int col = nb * 128 + kCols * ch + j;
-        const int tc = col / a.C, c = col % a.C;
-        const int jg = tc * a.tile_cols + c;
-        if (kk == 0 && b < a.M && c < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v) * a.k_out;
-      }
-    }
-    if (a.ctr) {
-      atomicAdd(&a.ctr[0], (unsigned long long)exact);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
 // ------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -229,9 +58,10 @@ static EncodeFn encode_fn() {
   return fn;
 }
 
-// 2-D u8 tensor [outer][inner] with a 128 x 128 box, 128B swizzle.
+// 2-D u8 tensor [outer][inner], box box_inner x box_outer, 128B (default)
+// or 64B swizzle.
 static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                     uint32_t box_outer) {
+                     uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -239,7 +69,7 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -253,8 +83,10 @@ static int sm_count() {
   return n;
 }
 
-bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
-  return make_map(m, base, inner, outer, bi, bo);
+bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
+                 int swizzle_bytes) {
+  return make_map(m, base, inner, outer, bi, bo,
+                  swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 int num_sms() { return sm_count(); }
 
@@ -283,48 +115,6 @@ AdcConst make_adc_const(const xbs_core* c) {
 }
 
 }  // namespace tc
-
-bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
-  using namespace tc;
-  const Geo& g = c->g;
-  if (g.R != 128 || g.TPi > 16 || c->adc.passthrough) return false;
-  // fp32 P accumulators must stay exact: GR * maxc * sum_s 2^(s db) < 2^24
-  const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
-  if (double(g.GR) * c->adc.maxc * sw >= 16777216.0) return false;
-  const int64_t rowsF = ((M * g.TPi + 127) / 128) * 128;
-  CUtensorMap mA, mB;
-  if (!make_map(&mA, c->d_Af, uint64_t(g.KI), uint64_t(2 * rowsF), 128, 128)) return false;
-  if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 128)) return false;
-  FwdArgs a{};
-  a.GR = g.GR;
-  a.GC = g.GC;
-  a.S = g.S;
-  a.db = g.db;
-  a.TPi = g.TPi;
-  a.tile_cols = g.tile_cols;
-  a.C = g.C;
-  a.R = g.R;
-  a.N = g.N;
-  a.M = M;
-  a.rowsF = rowsF;
-  a.num_mb = int(rowsF / 128);
-  a.num_units = a.num_mb * (g.NI / 128);
-  a.k_out = c->k_out_fwd;
-  a.adc = make_adc_const(c);
-  a.y = d_y;
-  a.ctr = &c->d_sc->exact_path;
-  a.dbg = getenv("XBS_DBG_FWD") ? atoi(getenv("XBS_DBG_FWD")) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fwd_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    attr = true;
-  }
-  const int grid = std::min(a.num_units, sm_count());
-  if (a.dbg & 1) k_fwd_tc<1><<<grid, kThreads, kSmem, st>>>(mA, mB, a);
-  else k_fwd_tc<0><<<grid, kThreads, kSmem, st>>>(mA, mB, a);
-  return cudaPeekAtLastError() == cudaSuccess;
-}
 
 // ---------------------------------------------------------------------------
 // K2 backward (layers.cpp:339-379).  Unit = (128 error bit-plane rows: 128 /
@@ -520,7 +310,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   if (g.R != 128 || g.C != 128 || g.TPe > 16 || c->adc.passthrough) return false;
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   if (double(g.GC) * c->adc.maxc * sw * 2.0 >= 16777216.0) return false;
-  const int64_t rowsB = ((M * g.TPe * 2 + 127) / 128) * 128;
+  const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
   if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
   if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 64)) return false;
