@@ -1,2 +1,2 @@
 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_fwd_tc" -s 1 -c 1 -o gpurun_out/prof_fwd python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+ncu --set full --clock-control none --import-source on -k regex:"k_update1" -s 1 -c 1 -o gpurun_out/prof_fwd python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log

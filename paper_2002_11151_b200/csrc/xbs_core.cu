@@ -499,6 +499,10 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
                          c->stream),
        "H2D W");
     xbs::launch_map_weights(c.get(), d_W, c->stream);
+    if (o.variation_sigma == 0.0 && !c->fully_ideal) {
+      ck(cudaMalloc(&c->d_qmin, size_t(o.tile_rows) * o.tile_cols * sizeof(uint32_t)), "cudaMalloc qmin");
+      xbs::launch_qmin(c.get(), c->stream);
+    }
     const auto t0 = std::chrono::steady_clock::now();
     if (!c->fully_ideal) xbs::launch_regen_all(c.get(), c->stream);
     regenerate_bookkeeping(c.get());
@@ -513,6 +517,7 @@ void xbs_core_destroy(xbs_core* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_digits);
+  cudaFree(c->d_qmin);
   cudaFree(c->d_master);
   cudaFree(c->d_dW);
   cudaFree(c->d_wimp);

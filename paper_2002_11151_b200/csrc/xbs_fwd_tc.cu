@@ -184,6 +184,13 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
             mbar_wait(&t_full[ab * 2 + mb], abph);
             tc_fence_after();
             const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + mb * 128 + 32 * ch;
+            if (a.dbg & 1) {  // perf experiment: no ADC work, just hand the buffer back
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&t_empty[ab * 2 + mb]);
+              if (++ab == 2) { ab = 0; abph ^= 1; }
+              continue;
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               adc_chunk8s(ta + 8 * q, ta + 64 + 8 * q, k, w, P, 8 * q, exact,

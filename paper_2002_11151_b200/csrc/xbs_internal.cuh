@@ -104,6 +104,7 @@ struct xbs_core {
   double F = 0.0, vu = 0.0, ifs_fac = 1.0, sx = 0.0, lev_e = 0.0, lev_a = 0.0;
   // device buffers
   uint8_t* d_digits = nullptr;
+  uint32_t* d_qmin = nullptr;  // sigma == 0: snapped q of g_min per tile position
   double* d_master = nullptr;
   double* d_dW = nullptr;
   double* d_wimp = nullptr;  // implied weights (fully-ideal fast path), K x N row-major
@@ -157,6 +158,7 @@ void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st
 void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* d_dx, cudaStream_t st);
 void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st);
+void launch_qmin(const xbs_core* c, cudaStream_t st);
 void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);
 void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double* d_out, cudaStream_t st);
 // tcgen05 kernels (xbs_vmm_tc.cu); return false if the shape is not covered

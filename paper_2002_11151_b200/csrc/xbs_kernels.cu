@@ -225,7 +225,7 @@ __global__ void k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ d
 // conductance digits (both polarities) -- the K3b roofline bytes.
 __global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
                                                  double* __restrict__ master, uint8_t* __restrict__ digits,
-                                                 DevScalars* sc) {
+                                                 DevScalars* sc, const uint32_t* __restrict__ qmin) {
   const double range = rp.range;
   double wmax = 0.0, dwmax = 0.0;
   const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -284,8 +284,18 @@ __global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, cons
         if (nu < -range) nu = -range;
         urow[jj] = nu;
         acc[jj] = acc[jj] * double(1u << g.db) + nu;
+        if (qmin) {
+          // sigma == 0: the inactive polarity sits exactly at g_min (mapping.cpp:39-45),
+          // whose snapped non-ideal value depends only on the tile position.
+          const int pa = nu > 0.0 ? 0 : 1;
+          const uint32_t qa = convert_device_rc(rp, g, nu, s, pa, i, j0 + jj, r, cj[jj]);
+          const uint32_t qi = qmin[r * g.tile_cols + cj[jj]];
+          q[0][jj] = pa == 0 ? qa : qi;
+          q[1][jj] = pa == 0 ? qi : qa;
+        } else {
 #pragma unroll
-        for (int p = 0; p < 2; ++p) q[p][jj] = convert_device_rc(rp, g, nu, s, p, i, j0 + jj, r, cj[jj]);
+          for (int p = 0; p < 2; ++p) q[p][jj] = convert_device_rc(rp, g, nu, s, p, i, j0 + jj, r, cj[jj]);
+        }
       }
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -323,8 +333,21 @@ __global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, cons
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st) {
   const int bx = (c->g.N + 4 * 256 - 1) / (4 * 256);
   const int by = std::min(c->g.K, 65535);
-  k_update4<<<dim3(bx, by), 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
+  k_update4<<<dim3(bx, by), 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
   (void)k_update;
+}
+
+// q(g_min) per tile position (sigma == 0 only): tile_rows x tile_cols
+__global__ void k_qmin(Geo g, RegenP rp, uint32_t* qmin) {
+  const int n = g.tile_rows * g.tile_cols;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t / g.tile_cols, c = t % g.tile_cols;
+    qmin[t] = convert_device_rc(rp, g, 0.0, 0, 0, r, c, r, c);
+  }
+}
+
+void launch_qmin(const xbs_core* c, cudaStream_t st) {
+  k_qmin<<<64, 256, 0, st>>>(c->g, c->rp, c->d_qmin);
 }
 
 // implied_weights() (mapping.cpp:70-81) -> K x N row-major

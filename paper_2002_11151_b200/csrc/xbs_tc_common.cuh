@@ -263,11 +263,9 @@ __device__ __forceinline__ uint64_t adc_fast2(uint32_t hi0, uint32_t hi1, uint32
 // saturation) or whose max |r| exceeds k.thr (near a rounding boundary) is
 // re-evaluated element by element with the reference's fp64 expression.
 __device__ __forceinline__ float adc_x(uint32_t hi, uint32_t lo, const AdcConst& k) {
-  // hi converted exactly (magic OR + subtract); lo's magic offset folded
-  // into k_lo (exact).  |x - scaled| <= 3 2^-24 x  (<< kDelta).
-  const float hf = __fsub_rn(__int_as_float(int(hi | 0x4B000000u)), kMagic23);
-  const float lt = __fmaf_rn(__int_as_float(int(lo | 0x4B000000u)), k.c_lo, k.k_lo);
-  return __fmaf_rn(hf, k.c_hi, lt);
+  // hi, lo < 2^24 (<= 256 crossbar rows) convert exactly (I2FP, ALU pipe);
+  // |x - scaled| <= 3 2^-24 x  (<< kDelta).
+  return __fmaf_rn(__uint2float_rn(hi), k.c_hi, __fmul_rn(__uint2float_rn(lo), k.c_lo));
 }
 __device__ __forceinline__ float rint_magic(float x) { return __fsub_rn(__fadd_rn(x, kRint), kRint); }
 

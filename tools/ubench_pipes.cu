@@ -70,7 +70,7 @@ void run(const char* name, int warps) {
   cudaFree(d);
 }
 
-int main() {
+int main_pipes() {
   for (int w : {8, 16, 32}) {
     run<0>("FFMA reg", w);
     run<6>("FFMA imm", w);
@@ -82,3 +82,28 @@ int main() {
   }
   return 0;
 }
+// (appended) I2F throughput probe
+__global__ void k_i2f(float* out, int s0) {
+  int u[8]; float v[8];
+  for (int i = 0; i < 8; ++i) { u[i] = threadIdx.x * 7 + i; v[i] = 0.f; }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { v[i] += __int2float_rn(u[i]); u[i] += s0; }
+  }
+  float acc = 0; for (int i = 0; i < 8; ++i) acc += v[i];
+  if (acc == 12345.f) out[0] = acc;
+}
+int main2() {
+  float* d; cudaMalloc(&d, 4);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int warps : {16, 32}) {
+    k_i2f<<<sms, 32 * warps>>>(d, 3);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a); k_i2f<<<sms, 32 * warps>>>(d, 3); cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    double instr = double(warps) * ITERS * 8;  // I2F per SM (plus same count of FADD and IADD)
+    printf("I2F(+FADD+IADD) warps/SM=%d %.3f ms  %.2f I2F/clk/SM\n", warps, ms, instr / (ms * 1e-3 * 1.965e9));
+  }
+  return 0;
+}
+int main() { main_pipes(); return main2(); }
