@@ -36,12 +36,14 @@ namespace tc {
 namespace fw {
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kABox = 128 * 128;  // 128 rows x 128 B, SW128
-constexpr int kAStage = 4 * kABox;
+constexpr int kABox = 128 * 128;  // 128 rows x 128 B (one k-block), SW128
 constexpr int kBBox = 128 * 64;   // 128 crossbar rows x 64 columns, SW64
-constexpr int kBStage = 4 * kBBox;
-constexpr int kAStages = 2, kBStages = 3;
-constexpr int kSmem = kAStages * kAStage + kBStages * kBStage + 1024 + 256;
+constexpr int kBStage = 4 * kBBox;  // one k-block of the 4 digit planes
+constexpr int kBStages = 3;
+// KB = 128-row k-blocks per crossbar (1: 128-row tiles, 2: 256-row tiles)
+template <int KB> constexpr int kAStage = 4 * KB * kABox;  // [mb][dh][kb]
+template <int KB> constexpr int kAStages = KB == 1 ? 2 : 1;
+template <int KB> constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages * kBStage + 1024 + 256;
 }  // namespace fw
 
 struct FwdArgs {
@@ -55,9 +57,11 @@ struct FwdArgs {
   int dbg;  // perf experiments: 2 = skip MMAs
 };
 
+template <int KB>
 __global__ void __launch_bounds__(fw::kThreads, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
   using namespace fw;
+  constexpr int kAStage = fw::kAStage<KB>, kAStages = fw::kAStages<KB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -111,21 +115,25 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
           for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
             for (int dh = 0; dh < 2; ++dh)
-              tma_load_2d(sA + as * kAStage + (mb * 2 + dh) * kABox, &mapA, &a_full[as], tr * a.R,
-                          int(dh * a.rowsF) + (2 * mbp + mb) * 128);
+#pragma unroll
+              for (int kb = 0; kb < KB; ++kb)
+                tma_load_2d(sA + as * kAStage + ((mb * 2 + dh) * KB + kb) * kABox, &mapA, &a_full[as],
+                            tr * a.R + kb * 128, int(dh * a.rowsF) + (2 * mbp + mb) * 128);
           if (++as == kAStages) { as = 0; aph ^= 1; }
           for (int s = 0; s < a.S; ++s)
-            for (int p = 0; p < 2; ++p) {
-              mbar_wait(&b_empty[bs], bph ^ 1);
-              mbar_expect_tx(&b_full[bs], kBStage);
-              const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R;
-              uint8_t* dst = sB + bs * kBStage;  // [dh][acc]: d0 d2 | d1 d3
-              tma_load_2d(dst + 0 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 0 * a.R);
-              tma_load_2d(dst + 1 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 2 * a.R);
-              tma_load_2d(dst + 2 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 1 * a.R);
-              tma_load_2d(dst + 3 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 3 * a.R);
-              if (++bs == kBStages) { bs = 0; bph ^= 1; }
-            }
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+              for (int kb = 0; kb < KB; ++kb) {
+                mbar_wait(&b_empty[bs], bph ^ 1);
+                mbar_expect_tx(&b_full[bs], kBStage);
+                const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R + kb * 128;
+                uint8_t* dst = sB + bs * kBStage;  // [dh][acc]: d0 d2 | d1 d3
+                tma_load_2d(dst + 0 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 0 * a.R);
+                tma_load_2d(dst + 1 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 2 * a.R);
+                tma_load_2d(dst + 2 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 1 * a.R);
+                tma_load_2d(dst + 3 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 3 * a.R);
+                if (++bs == kBStages) { bs = 0; bph ^= 1; }
+              }
         }
       }
     }
@@ -139,26 +147,29 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + as * kAStage);
           for (int sp = 0; sp < 2 * a.S; ++sp) {
-            mbar_wait(&b_full[bs], bph);
-            const uint32_t b0 = smem_u32(sB + bs * kBStage);
 #pragma unroll
-            for (int mb = 0; mb < 2; ++mb) {
-              mbar_wait(&t_empty[ab * 2 + mb], abph ^ 1);
-              tc_fence_after();
-              if (!(a.dbg & 2)) {
+            for (int kb = 0; kb < KB; ++kb) {
+              mbar_wait(&b_full[bs], bph);
+              const uint32_t b0 = smem_u32(sB + bs * kBStage);
 #pragma unroll
-                for (int dh = 0; dh < 2; ++dh)
+              for (int mb = 0; mb < 2; ++mb) {
+                if (kb == 0) mbar_wait(&t_empty[ab * 2 + mb], abph ^ 1);
+                tc_fence_after();
+                if (!(a.dbg & 2)) {
 #pragma unroll
-                  for (int ks = 0; ks < 4; ++ks) {
-                    const uint64_t ad = sdesc(a0 + (mb * 2 + dh) * kABox + 32 * ks, 16, 1024, 2);
-                    const uint64_t bd = sdesc(b0 + dh * 2 * kBBox + 2048 * ks, kBBox, 512, 4);
-                    umma_i8(tmem + ab * 256 + mb * 128, ad, bd, idesc, (dh | ks) != 0);
-                  }
+                  for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                      const uint64_t ad = sdesc(a0 + ((mb * 2 + dh) * KB + kb) * kABox + 32 * ks, 16, 1024, 2);
+                      const uint64_t bd = sdesc(b0 + dh * 2 * kBBox + 2048 * ks, kBBox, 512, 4);
+                      umma_i8(tmem + ab * 256 + mb * 128, ad, bd, idesc, (kb | dh | ks) != 0);
+                    }
+                }
+                if (kb == KB - 1) umma_commit(&t_full[ab * 2 + mb]);
               }
-              umma_commit(&t_full[ab * 2 + mb]);
+              umma_commit(&b_empty[bs]);
+              if (++bs == kBStages) { bs = 0; bph ^= 1; }
             }
-            umma_commit(&b_empty[bs]);
-            if (++bs == kBStages) { bs = 0; bph ^= 1; }
             if (++ab == 2) { ab = 0; abph ^= 1; }
           }
           umma_commit(&a_empty[as]);
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
 bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   using namespace tc;
   const Geo& g = c->g;
-  if (g.R != 128 || g.TPi > 16 || c->adc.passthrough) return false;
+  if ((g.R != 128 && g.R != 256) || g.TPi > 16 || c->adc.passthrough) return false;
   // fp32 P accumulators must stay exact: GR * maxc * sum_s 2^(s db) < 2^24
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   if (double(g.GR) * c->adc.maxc * sw >= 16777216.0) return false;
@@ -251,11 +262,13 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.dbg = getenv("XBS_DBG_FWD") ? atoi(getenv("XBS_DBG_FWD")) : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem);
+    cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
+    cudaFuncSetAttribute(k_fwd_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
     attr = true;
   }
   const int grid = std::min(a.num_units, num_sms());
-  k_fwd_tc<<<grid, fw::kThreads, fw::kSmem, st>>>(mA, mB, a);
+  if (g.R == 128) k_fwd_tc<1><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
+  else k_fwd_tc<2><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
   return cudaPeekAtLastError() == cudaSuccess;
 }
 

@@ -34,11 +34,13 @@ namespace tc {
 
 constexpr int kEpiWarps = 16;                 // 4 per SM sub-partition
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer, MMA issuer
-constexpr int kAStages = 2, kBStages = 2;
+constexpr int kBStages = 2;
 constexpr int kPlane = 128 * 128;          // one 128x128 u8 digit / bit box
-constexpr int kAStage = 2 * kPlane;        // bits + 255*bits
-constexpr int kBStage = 4 * kPlane;        // d0 d2 | d1 d3
-constexpr int kSmem = kAStages * kAStage + kBStages * kBStage + 1024 + 256;
+constexpr int kBStage = 4 * kPlane;        // one k-block: d0 d2 | d1 d3
+// KB = 128-column k-blocks per crossbar (C = 128 KB)
+template <int KB> constexpr int kAStage = 2 * KB * kPlane;  // [dh][kb]
+template <int KB> constexpr int kAStages = KB == 1 ? 2 : 1;
+template <int KB> constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages * kBStage + 1024 + 256;
 
 // ------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -143,8 +145,10 @@ struct BwdArgs {
 
 constexpr int kBHalf = 64 * 128;  // one [64 rows][128 cols] digit box
 
+template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const BwdArgs a) {
+  constexpr int kAStage = tc::kAStage<KB>, kAStages = tc::kAStages<KB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -194,10 +198,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int tc = 0; tc < a.GC; ++tc) {
           mbar_wait_sleep(&a_empty[as], aph ^ 1);
           mbar_expect_tx(&a_full[as], kAStage);
-          tma_load_2d(sA + as * kAStage, &mapA, &a_full[as], tc * a.C, mb * 128);
-          tma_load_2d(sA + as * kAStage + kPlane, &mapA, &a_full[as], tc * a.C, int(a.rowsB) + mb * 128);
+#pragma unroll
+          for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb)
+              tma_load_2d(sA + as * kAStage + (dh * KB + kb) * kPlane, &mapA, &a_full[as], tc * a.C + kb * 128,
+                          int(dh * a.rowsB) + mb * 128);
           if (++as == kAStages) { as = 0; aph ^= 1; }
-          for (int s = 0; s < a.S; ++s) {
+          for (int s = 0; s < a.S; ++s)
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
             mbar_wait_sleep(&b_empty[bs], bph ^ 1);
             mbar_expect_tx(&b_full[bs], kBStage);
             uint8_t* dst = sB + bs * kBStage;
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int acc = 0; acc < 2; ++acc) {
                   const int row = (((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) + 2 * acc + dh) * a.R + rh * 64;
-                  tma_load_2d(dst + ((dh * 2 + p) * 2 + acc) * kBHalf, &mapB, &b_full[bs], 0, row);
+                  tma_load_2d(dst + ((dh * 2 + p) * 2 + acc) * kBHalf, &mapB, &b_full[bs], kb * 128, row);
                 }
             if (++bs == kBStages) { bs = 0; bph ^= 1; }
           }
@@ -227,20 +237,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a0 = smem_u32(sA + as * kAStage);
           for (int s = 0; s < a.S; ++s) {
             mbar_wait_sleep(&t_empty[ab], abph ^ 1);
-            mbar_wait_sleep(&b_full[bs], bph);
-            tc_fence_after();
-            const uint32_t b0 = smem_u32(sB + bs * kBStage);
             const uint32_t td = tmem + ab * 256;
 #pragma unroll
-            for (int dh = 0; dh < 2; ++dh)
+            for (int kb = 0; kb < KB; ++kb) {
+              mbar_wait_sleep(&b_full[bs], bph);
+              tc_fence_after();
+              const uint32_t b0 = smem_u32(sB + bs * kBStage);
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {
-                const uint64_t ad = sdesc(a0 + dh * kPlane + 32 * ks, 16, 1024, 2);
-                const uint64_t bd = sdesc(b0 + dh * 4 * kBHalf + 32 * ks, 16, 1024, 2);
-                umma_i8(td, ad, bd, idesc, (dh | ks) != 0);
-              }
-            umma_commit(&b_empty[bs]);
-            if (++bs == kBStages) { bs = 0; bph ^= 1; }
+              for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                  const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kPlane + 32 * ks, 16, 1024, 2);
+                  const uint64_t bd = sdesc(b0 + dh * 4 * kBHalf + 32 * ks, 16, 1024, 2);
+                  umma_i8(td, ad, bd, idesc, (kb | dh | ks) != 0);
+                }
+              umma_commit(&b_empty[bs]);
+              if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            }
             umma_commit(&t_full[ab]);
             if (++ab == 2) { ab = 0; abph ^= 1; }
           }
@@ -307,13 +320,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   using namespace tc;
   const Geo& g = c->g;
-  if (g.R != 128 || g.C != 128 || g.TPe > 16 || c->adc.passthrough) return false;
+  if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc.passthrough) return false;
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   if (double(g.GC) * c->adc.maxc * sw * 2.0 >= 16777216.0) return false;
   const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
   if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
   if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 64)) return false;
+  const int KB = g.C / 128;
   BwdArgs a{};
   a.GR = g.GR;
   a.GC = g.GC;
@@ -339,11 +353,13 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_bwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem<1>);
+    cudaFuncSetAttribute(k_bwd_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem<2>);
     attr = true;
   }
   const int grid = std::min(a.num_units, sm_count());
-  k_bwd_tc<<<grid, kThreads, kSmem, st>>>(mA, mB, a);
+  if (KB == 1) k_bwd_tc<1><<<grid, kThreads, kSmem<1>, st>>>(mA, mB, a);
+  else k_bwd_tc<2><<<grid, kThreads, kSmem<2>, st>>>(mA, mB, a);
   return cudaPeekAtLastError() == cudaSuccess;
 }
 
