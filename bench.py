@@ -43,12 +43,45 @@ def parse():
     p.add_argument("--config", default="c2-4096")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-peak", action="store_true", help="skip the live int8 peak GEMM (ncu launch lists)")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
     return p.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def init_dist(world, local_rank, backend):
+    """One process per GPU (nccl) -- or per CPU rank (gloo, the CPU tests)."""
+    if world <= 1:
+        return
+    import torch
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        dist.init_process_group("gloo")
+
+
+def max_over_ranks(x, world, device="cpu"):
+    """Max of a per-rank scalar (device-timed ms) over all ranks."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
 
 
 # ----------------------------------------------------------------- clocks
@@ -124,7 +157,7 @@ def measure_int8_peak():
 
 
 # ----------------------------------------------------------- CPU baseline
-def cpu_sample(cfg, n_feat=256, steps=1):
+def cpu_sample(cfg, n_feat=256, steps=1, idx=0):
     """The oracle (restated reference CPU path, 1 thread: the reference's
     forward/backward/update are serial, layers.hpp:34) on a bounded sample of
     the same workload: a K=N=n_feat slice of the layer (same tile geometry,
@@ -134,9 +167,10 @@ def cpu_sample(cfg, n_feat=256, steps=1):
     from paper_2002_11151_b200.configs import Layer
 
     layer = cfg.layers[0]
+    n_feat = min(n_feat, layer.K, layer.N)
     sl = Layer("sample", layer.M, n_feat, n_feat)
     opt = cfg.options()
-    W, x, dy = cfg.weights(sl), cfg.inputs(sl), cfg.errors(sl)
+    W, x, dy = cfg.weights(sl, idx), cfg.inputs(sl, idx), cfg.errors(sl, idx)
     orc = oracle_py.OracleCore(W, opt, snapped=True)
     t0 = time.perf_counter()
     for it in range(steps):
@@ -151,27 +185,49 @@ def cpu_sample(cfg, n_feat=256, steps=1):
     return macs / dt, dt, desc
 
 
+def _ref_worker(a):
+    from paper_2002_11151_b200.configs import CONFIGS
+
+    name, idx = a
+    v, dt, desc = cpu_sample(CONFIGS[name], 256, 1, idx)
+    return v * dt, desc  # MACs done, description
+
+
 def run_reference(args, cfg):
+    """The reference algorithm's CPU implementation on all host cores.  The
+    reference's VMM loop is serial per core (threads only split regeneration,
+    layers.hpp:34), so the whole-host rate is one independent K=N=256 tile
+    slice of the workload per core, run concurrently: value = sum of MACs /
+    wall time of the step.  Under torchrun only rank 0 runs."""
+    import multiprocessing as mp
+
     rank, _, world = dist_env()
     if rank != 0:
         return
-    ncores = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_sample(cfg, 256, 1)
-    vals = [cpu_sample(cfg, 256, 1) for _ in range(args.steps)]
-    v = statistics.median([x[0] for x in vals])
-    dt = statistics.median([x[1] for x in vals])
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    ctx = mp.get_context("fork")
+    vals, desc = [], ""
+    with ctx.Pool(ncores) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, [(args.config, 100 * i + w) for w in range(ncores)])
+            dt = time.perf_counter() - t0
+            desc = res[0][1]
+            if i >= args.warmup:
+                vals.append((sum(r[0] for r in res) / dt, dt))
+    v = statistics.median([x[0] for x in vals]) if vals else 0.0
+    dt = statistics.median([x[1] for x in vals]) if vals else 0.0
+    sample = f"{ncores} concurrent processes, each: " + desc
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "MAC/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "layer": vars(cfg.layers[0]), "parallelism": "cpu"},
-        "cpu_baseline": {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port", "sample": vals[0][2],
-                         "host_cores_available": ncores,
-                         "note": "reference unbuildable here (Eigen3 absent); restated oracle, serial like the reference"},
+        "config": {"workload": cfg.name, "layer": vars(cfg.layers[0]), "parallelism": f"cpu{ncores}"},
+        "cpu_baseline": {"value": v, "unit": "MAC/s", "cores": ncores, "kind": "port", "sample": sample,
+                         "note": "reference unbuildable here (Eigen3 absent, DESIGN.md); restated oracle"},
         "e2e": {"value": v, "unit": "MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- ours
@@ -187,11 +243,8 @@ def main():
     import torch
 
     rank, local_rank, world = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
+    init_dist(world, local_rank, "nccl")
     from paper_2002_11151_b200 import xbarsim as xb
 
     layer = cfg.layers[0]
@@ -219,8 +272,7 @@ def main():
         step()
     core.synchronize()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    barrier(world)
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
@@ -238,12 +290,8 @@ def main():
     stages = core.stage_times()
     core.profile(False)
     launches = core.launch_count() - launches0
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    barrier(world)
+    ms = max_over_ranks(ms, world, "cuda")
 
     # e2e through the host-pointer C ABI with pinned host buffers
     e2e = None
@@ -254,28 +302,34 @@ def main():
         hx, hdy, hy, hdx = pinned(M, K), pinned(M, N), pinned(M, N), pinned(M, K)
         hx[:] = x
         hdy[:] = dy
-        for _ in range(2):
+        for _ in range(max(3, args.warmup)):
             core.forward(hx, True, out=hy)
             core.backward(hdy, 1.0, out=hdx)
             core.apply_updates(it[0])
             it[0] += 1
+        core.synchronize()
+        barrier(world)
+        # the host calls are synchronous; events on the core's stream bracket
+        # every H2D copy, kernel and D2H copy of the K steps
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        f0.record(stream)
         for _ in range(args.steps):
             core.forward(hx, True, out=hy)
             core.backward(hdy, 1.0, out=hdx)
             core.apply_updates(it[0])
             it[0] += 1
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        if world > 1:
-            t = torch.tensor([e2e_s], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"h2d_bytes_per_step": 8 * M * (K + N), "d2h_bytes_per_step": 8 * M * (N + K), "s": e2e_s}
+        f1.record(stream)
+        f1.synchronize()
+        wall_s = (time.perf_counter() - t0) / args.steps
+        e2e_s = max_over_ranks(f0.elapsed_time(f1) * 1e-3 / args.steps, world, "cuda")
+        e2e = {"h2d_bytes_per_step": 8 * M * (K + N), "d2h_bytes_per_step": 8 * M * (N + K), "s": e2e_s,
+               "wall_s": max_over_ranks(wall_s, world, "cuda")}
     clk = clocks.stop()
 
     macs = cfg.macs(layer)
     S = cfg.weight_bits // cfg.device_bits
-    peak_tops, peak_src = measure_int8_peak()
+    peak_tops, peak_src = (4500.0, "NVIDIA dense int8 spec (--no-peak)") if args.no_peak else measure_int8_peak()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -320,10 +374,13 @@ def main():
     }
     if e2e:
         line["e2e"] = {"value": world * macs["total"] / e2e["s"], "unit": "MAC/s",
-                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]}
+                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                       "ms_per_step": e2e["s"] * 1e3, "wall_ms_per_step": e2e["wall_s"] * 1e3,
+                       "path": "xbs_core_forward/backward/apply_updates (host pointers, pinned)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = cpu_sample(cfg, 256, 1)
-        line["cpu_baseline"] = {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port", "sample": desc}
+        v, dt, desc = cpu_sample(cfg, 512, 3)
+        line["cpu_baseline"] = {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port",
+                                "sample": desc + f"; 3 steps, {3 * dt:.1f} s of CPU work"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define XBS_ABI_VERSION 1
+#define XBS_ABI_VERSION 2
 
 /* Status codes: one per reference exception class (errors.hpp:10-47). */
 typedef enum xbs_status {
@@ -113,13 +113,16 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
                     xbs_core** out);
 void xbs_core_destroy(xbs_core* core);
 
-/* CrossbarCore::forward(x, training) — layers.cpp:215-284.  x: M x K,
+/* CrossbarCore::forward(x, training) — layers.cpp:215-284.  x: M x K
+ * (K must equal in_features, else XBS_INVALID_ARGUMENT as layers.cpp:216-217),
  * y: M x N, column-major host buffers. */
-int xbs_core_forward(xbs_core* core, const double* x, int64_t M, int64_t ldx, int32_t training, double* y,
-                     int64_t ldy);
+int xbs_core_forward(xbs_core* core, const double* x, int64_t M, int64_t K, int64_t ldx, int32_t training,
+                     double* y, int64_t ldy);
 /* CrossbarCore::backward(dy, grad_divisor) — layers.cpp:286-380.  dy: M x N,
- * dx: M x K, column-major host buffers. */
-int xbs_core_backward(xbs_core* core, const double* dy, int64_t M, int64_t lddy, double grad_divisor,
+ * dx: M x K, column-major host buffers.  Checks in the reference's order:
+ * no cached forward -> XBS_STATE_ERROR, then N != out_features or M != the
+ * forward batch -> XBS_INVALID_ARGUMENT (layers.cpp:287-290). */
+int xbs_core_backward(xbs_core* core, const double* dy, int64_t M, int64_t N, int64_t lddy, double grad_divisor,
                       double* dx, int64_t lddx);
 /* CrossbarCore::apply_updates(iteration) — layers.cpp:382-391. */
 int xbs_core_apply_updates(xbs_core* core, uint64_t iteration);

@@ -540,9 +540,11 @@ void xbs_core_destroy(xbs_core* c) {
   delete c;
 }
 
-int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t ldx, int32_t training, double* y, int64_t ldy) {
+int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t K, int64_t ldx, int32_t training, double* y,
+                     int64_t ldy) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    if (K != c->g.K) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: feature count mismatch");  // layers.cpp:216-217
     if (M < 0 || (M > 0 && (ldx < M || ldy < M || !x || !y))) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: bad buffers");
     ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
     if (M > 0)
@@ -558,11 +560,12 @@ int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t ldx, int32
   });
 }
 
-int xbs_core_backward(xbs_core* c, const double* dy, int64_t M, int64_t lddy, double gd, double* dx, int64_t lddx) {
+int xbs_core_backward(xbs_core* c, const double* dy, int64_t M, int64_t N, int64_t lddy, double gd, double* dx,
+                      int64_t lddx) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
     if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
-    if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
+    if (N != c->g.N || M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
     if (M > 0 && (lddy < M || lddx < M || !dy || !dx)) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: bad buffers");
     ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
     if (M > 0)

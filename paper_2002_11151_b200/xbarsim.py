@@ -231,8 +231,8 @@ SYMBOLS = {
     "xbs_options_init": (None, [ctypes.POINTER(CLayerOptions)]),
     "xbs_core_create": (ctypes.c_int, [ctypes.POINTER(CLayerOptions), _D, _I64, _I64, _I64, ctypes.POINTER(_P)]),
     "xbs_core_destroy": (None, [_P]),
-    "xbs_core_forward": (ctypes.c_int, [_P, _D, _I64, _I64, ctypes.c_int32, _D, _I64]),
-    "xbs_core_backward": (ctypes.c_int, [_P, _D, _I64, _I64, ctypes.c_double, _D, _I64]),
+    "xbs_core_forward": (ctypes.c_int, [_P, _D, _I64, _I64, _I64, ctypes.c_int32, _D, _I64]),
+    "xbs_core_backward": (ctypes.c_int, [_P, _D, _I64, _I64, _I64, ctypes.c_double, _D, _I64]),
     "xbs_core_apply_updates": (ctypes.c_int, [_P, ctypes.c_uint64]),
     "xbs_core_forward_device": (ctypes.c_int, [_P, _P, _I64, ctypes.c_int32, _P]),
     "xbs_core_backward_device": (ctypes.c_int, [_P, _P, _I64, ctypes.c_double, _P]),
@@ -316,23 +316,24 @@ class CrossbarCore:
 
     def forward(self, x: np.ndarray, training: bool, out: Optional[np.ndarray] = None) -> np.ndarray:
         x = _fortran(x)
-        if x.ndim != 2 or x.shape[1] != self._K:
+        if x.ndim != 2:
             raise ValueError("CrossbarCore::forward: feature count mismatch")
         M = x.shape[0]
         y = np.zeros((M, self._N), dtype=np.float64, order="F") if out is None else out
         assert y.shape == (M, self._N) and y.flags.f_contiguous
-        _check(load_library().xbs_core_forward(self._h, _ptr(x), M, max(1, M), int(bool(training)), _ptr(y),
+        _check(load_library().xbs_core_forward(self._h, _ptr(x), M, x.shape[1], max(1, M), int(bool(training)), _ptr(y),
                                                max(1, M)))
         return y
 
     def backward(self, dy: np.ndarray, grad_divisor: float, out: Optional[np.ndarray] = None) -> np.ndarray:
         dy = _fortran(dy)
-        if dy.ndim != 2 or dy.shape[1] != self._N:
+        if dy.ndim != 2:
             raise ValueError("CrossbarCore::backward: gradient shape mismatch")
         M = dy.shape[0]
         dx = np.zeros((M, self._K), dtype=np.float64, order="F") if out is None else out
         assert dx.shape == (M, self._K) and dx.flags.f_contiguous
-        _check(load_library().xbs_core_backward(self._h, _ptr(dy), M, max(1, M), float(grad_divisor), _ptr(dx),
+        _check(load_library().xbs_core_backward(self._h, _ptr(dy), M, dy.shape[1], max(1, M), float(grad_divisor),
+                                                _ptr(dx),
                                                 max(1, M)))
         return dx
 

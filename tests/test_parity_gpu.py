@@ -140,6 +140,10 @@ def test_backward_before_forward_and_zero_error():
     gpu = xb.CrossbarCore(normal((20, 10), 1, 0.05), opt)
     with pytest.raises(xb.StateError):
         gpu.backward(np.zeros((2, 10)), 1.0)
+    with pytest.raises(xb.StateError):  # state before shape (layers.cpp:287-290)
+        gpu.backward(np.zeros((2, 11)), 1.0)
+    with pytest.raises(ValueError):
+        gpu.forward(np.zeros((2, 21)), False)
     gpu.forward(np.ones((2, 20)) * 0.5, True)
     dx = gpu.backward(np.zeros((2, 10)), 1.0)
     assert np.all(dx == 0.0) and not np.any(np.signbit(dx))
