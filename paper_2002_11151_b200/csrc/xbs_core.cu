@@ -482,6 +482,32 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     }
 
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!a.passthrough) {
+      // code(n) of converters.cpp:79-87 on the snapped current I = n 2^sh is
+      // monotone in n, so T[k] = min{n : code(n) >= k} decides every code
+      // exactly; the tcgen05 epilogues use it for the boundary cases.
+      auto code = [&](uint64_t n) {
+        const double scaled = std::ldexp(double(n), a.sh) / a.i_fs * a.maxc_d;
+        return scaled >= a.maxc_d ? int64_t(a.maxc) : int64_t(std::llround(scaled));
+      };
+      std::vector<unsigned long long> T(size_t(a.maxc) + 1, 0ull);
+      const uint64_t top = uint64_t(1) << 44;  // > 65025^2 * 256 >= any column current
+      for (int k = 1; k <= a.maxc; ++k) {
+        uint64_t lo = k > 1 ? T[size_t(k) - 1] : 0, hi = top;
+        if (code(hi) < k) {
+          T[size_t(k)] = top;
+          continue;
+        }
+        while (lo < hi) {
+          const uint64_t mid = lo + (hi - lo) / 2;
+          if (code(mid) >= k) hi = mid;
+          else lo = mid + 1;
+        }
+        T[size_t(k)] = lo;
+      }
+      ck(cudaMalloc(&c->d_adc_tab, T.size() * 8), "cudaMalloc adc table");
+      ck(cudaMemcpy(c->d_adc_tab, T.data(), T.size() * 8, cudaMemcpyHostToDevice), "H2D adc table");
+    }
     ck(cudaMalloc(&c->d_master, size_t(g.S) * g.Kp * g.Np * 8), "cudaMalloc master");
     ck(cudaMalloc(&c->d_digits, g.digits_bytes()), "cudaMalloc digits");
     ck(cudaMemsetAsync(c->d_digits, 0, g.digits_bytes(), c->stream), "memset digits");
@@ -518,6 +544,7 @@ void xbs_core_destroy(xbs_core* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_digits);
   cudaFree(c->d_qmin);
+  cudaFree(c->d_adc_tab);
   cudaFree(c->d_master);
   cudaFree(c->d_dW);
   cudaFree(c->d_wimp);

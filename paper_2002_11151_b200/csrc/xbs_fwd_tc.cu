@@ -3,29 +3,37 @@
 // Unit = (two 128-row M-blocks of input bit-plane rows [b * TPi + k],
 //         64 device output columns of one crossbar tile column).
 // For every crossbar row tile tr, slice s and polarity p the MMA thread
-// issues, per M-block, a K = 2 x 128 chain of tcgen05.mma.kind::i8
+// issues, per M-block, a K = 2 x R chain of tcgen05.mma.kind::i8
 // (M=128, N=128, K=32) against the SAME B tile:
 //     D[:,  0: 64] = A_bits . d0 + A_255 . d1    (lo digit pair of q)
 //     D[:, 64:128] = A_bits . d2 + A_255 . d3    (hi digit pair of q)
 // i.e. the exact column current of every (row, bit plane, column) split as
 // hi * 65025 + lo in s32 TMEM accumulators.  The accumulation K-extent is
-// exactly one crossbar (128 rows); the epilogue then applies the ADC (fp32
-// fast path + exact fp64 fix-up, xbs_tc_common.cuh) and the signed shift-add
-// P += +-2^(s db) * code.  Sharing the 32 KB B tile between two M-blocks
-// halves the L2 -> SMEM traffic of the conductance digits.  After the last
-// tile the TPi bit-plane lanes of each batch row are combined in int64 as
-// sum_k 2^k P_k and scaled once by k_out (layers.cpp:272-283).
+// exactly one crossbar (R = 128 or 256 rows, one or two k-blocks); the
+// epilogue then applies the ADC (fp32 fast path + exact threshold fix-up,
+// xbs_tc_common.cuh) and the signed shift-add P += +-2^(s db) * code.  The
+// B tile (4 digit planes x 128 rows x 64 columns, 32 KB, SW64) is shared by
+// both M-blocks (N = 128 keeps an MMA's 8 KB of SMEM operand reads within
+// the 128 B/clk SMEM port).  After the last tile the TPi bit-plane lanes of
+// each batch row are combined in int64 as sum_k 2^k P_k and scaled once by
+// k_out (layers.cpp:272-283).
+//
+// Scheduling: persistent CTAs take units round-robin; when the last wave
+// would leave SMs idle (C2-4096: 512 units = 3.46 waves on 148 SMs), its
+// units are split into single-M-block half units (3.5 waves instead of 4).
+// Column blocks made only of tile padding are never scheduled (C3's N = 16
+// / 32 layers compute 64 of a padded 128-column tile).
 //
 // Roles (576 threads, 1 CTA / SM): warp 0 TMA producer, warp 1 TMEM
 // allocator + MMA issuer, warps 2..17 epilogue: warp w reads TMEM lanes
 // 32 (w % 4).., M-block ((w-2)/4) & 1, columns 32 ((w-2)/8)...
-// Pipelines: A (64 KB: 2 M-blocks x {bits, 255 bits}) x 2 stages,
-// B (32 KB: 4 digit planes x 128 rows x 64 columns, SW64) x 3 stages,
-// TMEM accumulators (2 M-blocks x 128 columns) x 2 buffers.
+// Pipelines: A (64 KB per k-block: 2 M-blocks x {bits, 255 bits}) x 2 stages
+// (1 for 256-row crossbars), B (32 KB) x 3 stages, TMEM accumulators
+// (2 M-blocks x 128 columns) x 2 buffers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <cstdlib>
+#include <cmath>
 
 #include "xbs_internal.cuh"
 #include "xbs_tc_common.cuh"
@@ -36,10 +44,12 @@ namespace tc {
 namespace fw {
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kABox = 128 * 128;  // 128 rows x 128 B (one k-block), SW128
-constexpr int kBBox = 128 * 64;   // 128 crossbar rows x 64 columns, SW64
-constexpr int kBStage = 4 * kBBox;  // one k-block of the 4 digit planes
+constexpr int kCW = 64;               // device columns per unit
+constexpr int kABox = 128 * 128;      // 128 rows x 128 B (one k-block), SW128
+constexpr int kBBox = 128 * kCW;      // 128 crossbar rows x 64 columns, SW64
+constexpr int kBStage = 4 * kBBox;    // one k-block of the 4 digit planes
 constexpr int kBStages = 3;
+constexpr int kTBufs = 2;             // TMEM buffers of 2 M-blocks x 128 columns
 // KB = 128-row k-blocks per crossbar (1: 128-row tiles, 2: 256-row tiles)
 template <int KB> constexpr int kAStage = 4 * KB * kABox;  // [mb][dh][kb]
 template <int KB> constexpr int kAStages = KB == 1 ? 2 : 1;
@@ -48,14 +58,24 @@ template <int KB> constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages * 
 
 struct FwdArgs {
   int GR, GC, S, db, TPi, tile_cols, C, R, N;
+  int live;  // 64-column units per tile column that hold logical columns
   int64_t M, rowsF;
   int num_mbp, num_units;
+  int n_full, sched;  // units [n_full, num_units) run as 2 half units each
   double k_out;
   AdcConst adc;
   double* y;
   unsigned long long* ctr;
-  int dbg;  // perf experiments: 2 = skip MMAs
 };
+
+struct Unit {
+  int mbp, nb, only;  // only: -1 both M-blocks, else the single M-block
+};
+__device__ __forceinline__ Unit unit_of(int u, const FwdArgs& a) {
+  if (u < a.n_full) return {u % a.num_mbp, u / a.num_mbp, -1};
+  const int v = u - a.n_full, base = a.n_full + (v >> 1);
+  return {base % a.num_mbp, base / a.num_mbp, v & 1};
+}
 
 template <int KB>
 __global__ void __launch_bounds__(fw::kThreads, 1)
@@ -71,9 +91,9 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
   uint64_t* a_empty = a_full + kAStages;
   uint64_t* b_full = a_empty + kAStages;
   uint64_t* b_empty = b_full + kBStages;
-  uint64_t* t_full = b_empty + kBStages;  // [buffer][M-block]
-  uint64_t* t_empty = t_full + 4;         // [buffer][M-block]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 4);
+  uint64_t* t_full = b_empty + kBStages;    // [buffer][M-block]
+  uint64_t* t_empty = t_full + 2 * kTBufs;  // [buffer][M-block]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2 * kTBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -85,7 +105,7 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2 * kTBufs; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], kEpiWarps / 2);
     }
@@ -100,25 +120,26 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nsplit = a.C / 64;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------- TMA producer
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        const int mbp = u % a.num_mbp, nb = u / a.num_mbp;
-        const int tc = nb / nsplit, h = nb % nsplit;
+      for (int u = blockIdx.x; u < a.sched; u += gridDim.x) {
+        const Unit un = unit_of(u, a);
+        const int tc = un.nb / a.live, h = un.nb % a.live;
         for (int tr = 0; tr < a.GR; ++tr) {
           mbar_wait(&a_empty[as], aph ^ 1);
-          mbar_expect_tx(&a_full[as], kAStage);
+          mbar_expect_tx(&a_full[as], un.only < 0 ? kAStage : kAStage / 2);
 #pragma unroll
-          for (int mb = 0; mb < 2; ++mb)
+          for (int mb = 0; mb < 2; ++mb) {
+            if (un.only >= 0 && mb != un.only) continue;
 #pragma unroll
             for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
               for (int kb = 0; kb < KB; ++kb)
                 tma_load_2d(sA + as * kAStage + ((mb * 2 + dh) * KB + kb) * kABox, &mapA, &a_full[as],
-                            tr * a.R + kb * 128, int(dh * a.rowsF) + (2 * mbp + mb) * 128);
+                            tr * a.R + kb * 128, int(dh * a.rowsF) + (2 * un.mbp + mb) * 128);
+          }
           if (++as == kAStages) { as = 0; aph ^= 1; }
           for (int s = 0; s < a.S; ++s)
             for (int p = 0; p < 2; ++p)
@@ -128,10 +149,10 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
                 mbar_expect_tx(&b_full[bs], kBStage);
                 const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R + kb * 128;
                 uint8_t* dst = sB + bs * kBStage;  // [dh][acc]: d0 d2 | d1 d3
-                tma_load_2d(dst + 0 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 0 * a.R);
-                tma_load_2d(dst + 1 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 2 * a.R);
-                tma_load_2d(dst + 2 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 1 * a.R);
-                tma_load_2d(dst + 3 * kBBox, &mapB, &b_full[bs], h * 64, row0 + 3 * a.R);
+                tma_load_2d(dst + 0 * kBBox, &mapB, &b_full[bs], h * kCW, row0 + 0 * a.R);
+                tma_load_2d(dst + 1 * kBBox, &mapB, &b_full[bs], h * kCW, row0 + 2 * a.R);
+                tma_load_2d(dst + 2 * kBBox, &mapB, &b_full[bs], h * kCW, row0 + 1 * a.R);
+                tma_load_2d(dst + 3 * kBBox, &mapB, &b_full[bs], h * kCW, row0 + 3 * a.R);
                 if (++bs == kBStages) { bs = 0; bph ^= 1; }
               }
         }
@@ -139,9 +160,10 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_i8(128, 128, /*b_mn_major=*/true);
+      constexpr uint32_t idesc = idesc_i8(128, 2 * kCW, /*b_mn_major=*/true);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
+      for (int u = blockIdx.x; u < a.sched; u += gridDim.x) {
+        const int only = unit_of(u, a).only;
         for (int tr = 0; tr < a.GR; ++tr) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
@@ -153,24 +175,26 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
               const uint32_t b0 = smem_u32(sB + bs * kBStage);
 #pragma unroll
               for (int mb = 0; mb < 2; ++mb) {
+                if (only >= 0 && mb != only) continue;  // a half unit is the CTA's last
                 if (kb == 0) mbar_wait(&t_empty[ab * 2 + mb], abph ^ 1);
                 tc_fence_after();
-                if (!(a.dbg & 2)) {
 #pragma unroll
-                  for (int dh = 0; dh < 2; ++dh)
+                for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
-                      const uint64_t ad = sdesc(a0 + ((mb * 2 + dh) * KB + kb) * kABox + 32 * ks, 16, 1024, 2);
-                      const uint64_t bd = sdesc(b0 + dh * 2 * kBBox + 2048 * ks, kBBox, 512, 4);
-                      umma_i8(tmem + ab * 256 + mb * 128, ad, bd, idesc, (kb | dh | ks) != 0);
-                    }
-                }
+                  for (int ks = 0; ks < 4; ++ks) {
+                    // A: K-major SW128 (LBO 16, SBO 1024); B: MN-major SW64,
+                    // the lo / hi 64-column boxes kBBox apart (LBO), 8-row
+                    // K groups 512 B apart (SBO), 32 K rows per MMA = 2 KB
+                    const uint64_t ad = sdesc(a0 + ((mb * 2 + dh) * KB + kb) * kABox + 32 * ks, 16, 1024, 2);
+                    const uint64_t bd = sdesc(b0 + dh * 2 * kBBox + 2048 * ks, kBBox, 512, 4);
+                    umma_i8(tmem + ab * 256 + mb * 128, ad, bd, idesc, (kb | dh | ks) != 0);
+                  }
                 if (kb == KB - 1) umma_commit(&t_full[ab * 2 + mb]);
               }
               umma_commit(&b_empty[bs]);
               if (++bs == kBStages) { bs = 0; bph ^= 1; }
             }
-            if (++ab == 2) { ab = 0; abph ^= 1; }
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           }
           umma_commit(&a_empty[as]);
           if (++as == kAStages) { as = 0; aph ^= 1; }
@@ -183,8 +207,10 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
     const int ml = 32 * lg + lane;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int mbp = u % a.num_mbp, nb = u / a.num_mbp;
+    for (int u = blockIdx.x; u < a.sched; u += gridDim.x) {
+      const Unit un = unit_of(u, a);
+      if (un.only >= 0 && un.only != mb) break;  // half unit of the other M-block (last unit)
+      const int mbp = un.mbp, nb = un.nb;
       float P[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) P[j] = 0.f;
@@ -195,28 +221,19 @@ __global__ void __launch_bounds__(fw::kThreads, 1)
             mbar_wait(&t_full[ab * 2 + mb], abph);
             tc_fence_after();
             const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + mb * 128 + 32 * ch;
-            if (a.dbg & 1) {  // perf experiment: no ADC work, just hand the buffer back
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&t_empty[ab * 2 + mb]);
-              if (++ab == 2) { ab = 0; abph ^= 1; }
-              continue;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              adc_chunk8s(ta + 8 * q, ta + 64 + 8 * q, k, w, P, 8 * q, exact,
-                          q == 3 ? &t_empty[ab * 2 + mb] : nullptr);
-            if (++ab == 2) { ab = 0; abph ^= 1; }
+            adc_chunk16s(ta, ta + kCW, k, w, P, 0, exact, nullptr);
+            adc_chunk16s(ta + 16, ta + kCW + 16, k, w, P, 16, exact, &t_empty[ab * 2 + mb]);
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
       const int kk = ml % a.TPi;
       const int64_t b = (int64_t(2 * mbp + mb) * 128 + ml) / a.TPi;
+      const int tc = nb / a.live, h = nb % a.live;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         long long v = (long long)__float2ll_rn(P[j]) << kk;
         for (int o = 1; o < a.TPi; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int col = nb * 64 + 32 * ch + j;
-        const int tc = col / a.C, c = col % a.C;
+        const int c = h * kCW + 32 * ch + j;
         const int jg = tc * a.tile_cols + c;
         if (kk == 0 && b < a.M && c < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v) * a.k_out;
       }
@@ -240,7 +257,8 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   const int64_t rowsF = rows_fwd(M, g.TPi);
   CUtensorMap mA, mB;
   if (!make_map_u8(&mA, c->d_Af, uint64_t(g.KI), uint64_t(2 * rowsF), 128, 128, 128)) return false;
-  if (!make_map_u8(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 64, 128, 64)) return false;
+  if (!make_map_u8(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), fw::kCW, 128, 64))
+    return false;
   FwdArgs a{};
   a.GR = g.GR;
   a.GC = g.GC;
@@ -251,15 +269,15 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.C = g.C;
   a.R = g.R;
   a.N = g.N;
+  a.live = (g.tile_cols + fw::kCW - 1) / fw::kCW;
   a.M = M;
   a.rowsF = rowsF;
   a.num_mbp = int(rowsF / 256);
-  a.num_units = a.num_mbp * (g.NI / 64);
+  a.num_units = a.num_mbp * g.GC * a.live;
   a.k_out = c->k_out_fwd;
   a.adc = make_adc_const(c);
   a.y = d_y;
   a.ctr = &c->d_sc->exact_path;
-  a.dbg = getenv("XBS_DBG_FWD") ? atoi(getenv("XBS_DBG_FWD")) : 0;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
@@ -267,6 +285,15 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
     attr = true;
   }
   const int grid = std::min(a.num_units, num_sms());
+  // last-wave balancing: leftover full units run as 2 single-M-block halves
+  // when those all fit in one extra wave
+  const int rounds = a.num_units / grid, rem = a.num_units - rounds * grid;
+  a.n_full = a.num_units;
+  a.sched = a.num_units;
+  if (rem > 0 && 2 * rem <= grid) {
+    a.n_full = rounds * grid;
+    a.sched = a.n_full + 2 * rem;
+  }
   if (g.R == 128) k_fwd_tc<1><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
   else k_fwd_tc<2><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
   return cudaPeekAtLastError() == cudaSuccess;

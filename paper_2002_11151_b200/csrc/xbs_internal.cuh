@@ -105,6 +105,7 @@ struct xbs_core {
   // device buffers
   uint8_t* d_digits = nullptr;
   uint32_t* d_qmin = nullptr;  // sigma == 0: snapped q of g_min per tile position
+  unsigned long long* d_adc_tab = nullptr;  // T[k] = min column current n (units 2^-e) with code >= k
   double* d_master = nullptr;
   double* d_dW = nullptr;
   double* d_wimp = nullptr;  // implied weights (fully-ideal fast path), K x N row-major

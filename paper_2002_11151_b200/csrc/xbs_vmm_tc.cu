@@ -88,7 +88,9 @@ static int sm_count() {
 bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
                  int swizzle_bytes) {
   return make_map(m, base, inner, outer, bi, bo,
-                  swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+                  swizzle_bytes == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
+                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                        : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 int num_sms() { return sm_count(); }
 
@@ -97,22 +99,14 @@ AdcConst make_adc_const(const xbs_core* c) {
   const double cn = std::ldexp(1.0, c->adc.sh) / c->adc.i_fs * c->adc.maxc_d;  // codes per current unit
   k.c_lo = float(cn);
   k.c_hi = float(65025.0 * cn);
-  k.k_lo = -8388608.0f * k.c_lo;
-  k.k2 = float(-8388608.0 * (double(k.c_lo) + double(k.c_hi)));
-  // Error bound of the fast x (in code units): rounding of k2 and of the
-  // inner FFMA (each <= 2^23 (c_hi + c_lo) 2^-24), of x itself (<= 2^-24 x,
-  // x < 2 maxc before the saturation check) plus the float constants'
-  // relative error on n (2 * 2^-24 x).  delta = 4x that bound, >= 2^-12.
+  // |x_fast - scaled| <= 3 2^-24 x (constants' rounding, FMUL, FFMA) with
+  // x <= maxc + 1 wherever the code is not saturated; delta = 4x that.
   const double maxc = double(c->adc.maxc);
-  const double err = 3.0 * 0x1p-24 * (maxc + 1.0);  // fast-x error on the unclamped range
-  const double delta = std::max(0x1p-12, 4.0 * err);
+  const double delta = 4.0 * 3.0 * 0x1p-24 * (maxc + 1.0);
   k.thr = float(0.5 - delta);
-  k.sat = float(maxc - 0.5 - delta);
   k.maxc = float(c->adc.maxc);
-  k.sh = c->adc.sh;
   k.maxc_i = c->adc.maxc;
-  k.i_fs = c->adc.i_fs;
-  k.maxc_d = c->adc.maxc_d;
+  k.tab = c->d_adc_tab;
   return k;
 }
 
@@ -269,7 +263,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int phi = ml & 1;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
-    const AdcConst2 c2 = make_const2(k);
     const double se = a.sc->se;
     const double step_e = se > 0 ? se / a.lev_e : 0.0;
     double k_out = step_e * a.F / a.vu;  // layers.cpp:375-377
