@@ -447,6 +447,7 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     rp.r_sense = o.r_sense;
     rp.aam = (o.engine == XBS_ENGINE_AAM && !zero_par) ? 1 : 0;
     rp.snap_e = snap_exponent(o.g_max);
+    rp.snap_scale = std::ldexp(1.0, rp.snap_e);
 
     // scale constants, same expressions as layers.cpp:272-281 / 369-377
     const double vu = o.dac_v_fs / (std::pow(2.0, o.dac_bits) - 1.0);
@@ -543,8 +544,8 @@ void xbs_core_destroy(xbs_core* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_digits);
-  cudaFree(c->d_qmin);
   cudaFree(c->d_adc_tab);
+  cudaFree(c->d_qmin);
   cudaFree(c->d_master);
   cudaFree(c->d_dW);
   cudaFree(c->d_wimp);

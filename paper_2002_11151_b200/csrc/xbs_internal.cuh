@@ -56,6 +56,7 @@ struct RegenP {
   double r_row, r_col, r_source, r_sense;
   int aam;     // 1: AAM conversion, 0: identity (ideal / zero-parasitic fcm)
   int snap_e;  // grid exponent e
+  double snap_scale;  // 2^e
 };
 
 // update.cpp:43-88 + implied weights (mapping.cpp:70-81)

@@ -47,41 +47,29 @@ __device__ __forceinline__ T warp_max(T v) {
 }
 
 // ------------------------------------------------- conductance conversion
-// mapping.cpp:39-58 + aam.cpp:14-31 + snap: one device (s, p, global padded
-// i, j) from its master value u.
-__device__ __forceinline__ uint32_t convert_device_rc(const RegenP& rp, const Geo& g, double u, int s, int p,
-                                                      int i, int j, int r, int c) {
-  double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
-  if (rp.sigma != 0.0) {
-    const int64_t idx = int64_t(i) * g.Np + j;
-    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, uint64_t(idx), 0));
-    m = m > 1e-12 ? m : 1e-12;
-    gv = fmin(gv * m, rp.g_max);
-  }
-  if (rp.aam) {
-    const double rpth = rp.r_source + double(c + 1) * rp.r_row + double(g.tile_rows - r) * rp.r_col + rp.r_sense;
-    if (gv == 0.0) gv = 0.0;
-    else if (rpth != 0.0) gv = 1.0 / (1.0 / gv + rpth);
-  }
-  return uint32_t(rint(ldexp(gv, rp.snap_e)));
+// aam.cpp:5-12: series path resistance of tile position (r, c), summed left
+// to right like the reference.
+__device__ __forceinline__ double aam_rpath(const RegenP& rp, const Geo& g, int r, int c) {
+  return rp.r_source + double(c + 1) * rp.r_row + double(g.tile_rows - r) * rp.r_col + rp.r_sense;
 }
 
-__device__ __forceinline__ uint32_t convert_device(const RegenP& rp, const Geo& g, double u, int s, int p,
-                                                   int i, int j) {
+// mapping.cpp:39-58 (polarity split, variation) + aam.cpp:14-31 + snap of one
+// device (slice s, polarity p, padded index idx = i * Np + j) from its master
+// value u.  __drcp_rn is the correctly rounded 1/x (= the reference's 1.0 / x)
+// and gv * 2^e is exact (= ldexp), so q is bit-identical to the oracle's.
+__device__ __forceinline__ uint32_t convert_q(const RegenP& rp, double u, int s, int p, uint64_t idx,
+                                              double rpath) {
   double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
   if (rp.sigma != 0.0) {
-    const int64_t idx = int64_t(i) * g.Np + j;
-    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, uint64_t(idx), 0));
+    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, idx, 0));
     m = m > 1e-12 ? m : 1e-12;
     gv = fmin(gv * m, rp.g_max);
   }
   if (rp.aam) {
-    const int r = i % g.tile_rows, c = j % g.tile_cols;
-    const double rpth = rp.r_source + double(c + 1) * rp.r_row + double(g.tile_rows - r) * rp.r_col + rp.r_sense;
     if (gv == 0.0) gv = 0.0;
-    else if (rpth != 0.0) gv = 1.0 / (1.0 / gv + rpth);
+    else if (rpath != 0.0) gv = __drcp_rn(__dadd_rn(__drcp_rn(gv), rpath));
   }
-  return uint32_t(rint(ldexp(gv, rp.snap_e)));  // nearbyint, ties-to-even
+  return __double2uint_rn(__dmul_rn(gv, rp.snap_scale));  // nearbyint(ldexp(gv, e))
 }
 
 __device__ __forceinline__ void store_digits(uint8_t* digits, const Geo& g, int s, int p, int i, int j,
@@ -154,9 +142,11 @@ __global__ void k_regen_all(Geo g, RegenP rp, const double* __restrict__ master,
   const int64_t n = int64_t(g.Kp) * g.Np;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int i = int(t / g.Np), j = int(t % g.Np);
+    const double rpath = rp.aam ? aam_rpath(rp, g, i % g.tile_rows, j % g.tile_cols) : 0.0;
     for (int s = 0; s < g.S; ++s) {
       const double u = master[(size_t(s) * g.Kp + i) * g.Np + j];
-      for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_device(rp, g, u, s, p, i, j));
+      for (int p = 0; p < 2; ++p)
+        store_digits(digits, g, s, p, i, j, convert_q(rp, u, s, p, uint64_t(i) * g.Np + j, rpath));
     }
   }
 }
@@ -168,47 +158,172 @@ void launch_regen_all(const xbs_core* c, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------- apply_updates
-// update.cpp:43-88 for every slice of one logical weight (i, j), then the
-// regeneration of both polarities of every slice (layers.cpp:388) and the
-// implied-weight Horner (mapping.cpp:70-81) for the |W| statistic.
-__global__ void k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW, double* __restrict__ master,
-                         uint8_t* __restrict__ digits, DevScalars* sc) {
-  const int64_t n = int64_t(g.K) * g.N;
-  double wmax = 0.0, dwmax = 0.0;
+// K3b: update.cpp:43-88 for every slice of a logical weight (i, j), the
+// regeneration of both devices of every slice (layers.cpp:388 ->
+// mapping.cpp:39-58 variation, aam.cpp:14-31, snap, radix-255 digits) and
+// the implied-weight Horner (mapping.cpp:70-81) for the |W| statistic.
+//
+// Layout for HBM: blockIdx.y walks rows i, each thread owns JPT consecutive
+// columns j (vector dW / master loads, all S slices loaded up front; each
+// digit plane row segment written as one packed JPT-byte store so every
+// 32-byte sector is written whole -- a partial sector costs a DRAM read).
+// Compile-time flags strip the variation / non-linearity / noise code when
+// those are off.  With sigma == 0 the inactive polarity of each device sits
+// exactly at g_min, whose snapped conductance depends on the tile position
+// only (qmin table), so one conversion per device and slice suffices.
+template <int JPT>
+struct VecT;
+template <>
+struct VecT<2> {
+  using D = double2;
+  using Q = uint2;
+  using B = uint16_t;
+};
+template <>
+struct VecT<4> {
+  using D = double4;
+  using Q = uint4;
+  using B = uint32_t;
+};
+
+template <int JPT>
+__device__ __forceinline__ void ld_vec(const double* p, double (&v)[JPT]) {
+  const typename VecT<JPT>::D t = *reinterpret_cast<const typename VecT<JPT>::D*>(p);
+  if constexpr (JPT == 2) {
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+  }
+}
+template <int JPT>
+__device__ __forceinline__ void st_vec(double* p, const double (&v)[JPT]) {
+  typename VecT<JPT>::D t;
+  if constexpr (JPT == 2) {
+    t.x = v[0];
+    t.y = v[1];
+  } else {
+    t.x = v[0];
+    t.y = v[1];
+    t.z = v[2];
+    t.w = v[3];
+  }
+  *reinterpret_cast<typename VecT<JPT>::D*>(p) = t;
+}
+
+template <int S_T, int JPT, bool VAR, bool NL, bool NOISE>
+__global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
+                                                double* __restrict__ master, uint8_t* __restrict__ digits,
+                                                DevScalars* sc, const uint32_t* __restrict__ qmin) {
+  constexpr int S = S_T;
   const double range = rp.range;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const int i = int(t / g.N), j = int(t % g.N);
-    const double dw = dW[t];
-    dwmax = fmax(dwmax, fabs(dw));
-    const double dg = dw * up.factor;  // scale_gradient (update.cpp:16-24)
-    double acc = 0.0;
-    for (int s = g.S - 1; s >= 0; --s) {
-      double* up_ = &master[(size_t(s) * g.Kp + i) * g.Np + j];
-      const double ui = *up_;
-      double du = dg;
-      if (!up.linear && dg != 0.0) {
-        const bool pos_active = ui > 0.0 || (ui == 0.0 && dg < 0.0);
-        const double dev_arg = pos_active ? -dg : dg;
-        const double gg = rp.g_min + fabs(ui);
-        if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
-        const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
-        const double nl = dev_arg * exp(-up.v * x);
-        du = pos_active ? -nl : nl;
+  double wmax = 0.0, dwmax = 0.0;
+  const int j0 = JPT * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (j0 < g.N) {
+    // column-only terms, hoisted out of the row loop
+    const int tc = j0 / g.tile_cols, c0 = j0 - tc * g.tile_cols;  // JPT | tile_cols (host-checked)
+    double rrow[JPT];
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) rrow[jj] = rp.r_source + double(c0 + jj + 1) * rp.r_row;
+    const size_t plane = g.plane_bytes();
+    const size_t sp_stride = size_t(g.GR) * g.GC * 4 * plane;
+    const size_t sstride = size_t(g.Kp) * g.Np;
+    for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
+      const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
+      const double rcol = double(g.tile_rows - r) * rp.r_col;
+      double dg[JPT], u[S][JPT], acc[JPT];
+      {
+        double dw[JPT];
+        ld_vec<JPT>(dW + size_t(i) * g.N + j0, dw);
+#pragma unroll
+        for (int jj = 0; jj < JPT; ++jj) {
+          dwmax = fmax(dwmax, fabs(dw[jj]));
+          dg[jj] = dw[jj] * up.factor;  // scale_gradient (update.cpp:16-24)
+          acc[jj] = 0.0;
+        }
       }
-      double noise = 0.0;
-      if (up.gamma != 0.0 && dg != 0.0) {
-        const double sigma = up.gamma * sqrt(range * fabs(dg));
-        if (sigma != 0.0)
-          noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s), uint64_t(t)));
+      double* mrow = master + size_t(i) * g.Np + j0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) ld_vec<JPT>(mrow + s * sstride, u[s]);
+      uint32_t qi[JPT];
+      if constexpr (!VAR) {
+        const typename VecT<JPT>::Q t =
+            *reinterpret_cast<const typename VecT<JPT>::Q*>(qmin + size_t(r) * g.tile_cols + c0);
+        qi[0] = t.x;
+        qi[1] = t.y;
+        if constexpr (JPT == 4) {
+          qi[2] = reinterpret_cast<const uint4&>(t).z;
+          qi[3] = reinterpret_cast<const uint4&>(t).w;
+        }
       }
-      double nu = ui - up.lr * (du + noise);
-      if (nu > range) nu = range;
-      if (nu < -range) nu = -range;
-      *up_ = nu;
-      for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_device(rp, g, nu, s, p, i, j));
-      acc = acc * double(1u << g.db) + nu;
+      uint8_t* dbase = digits + (size_t(tr) * g.GC + tc) * 4 * plane + size_t(r) * g.C + c0;
+#pragma unroll
+      for (int s = S - 1; s >= 0; --s) {  // Horner order: most significant slice first
+        uint32_t q[2][JPT];
+#pragma unroll
+        for (int jj = 0; jj < JPT; ++jj) {
+          const double ui = u[s][jj];
+          double du = dg[jj];
+          if constexpr (NL) {
+            if (dg[jj] != 0.0) {
+              const bool pos_active = ui > 0.0 || (ui == 0.0 && dg[jj] < 0.0);
+              const double dev_arg = pos_active ? -dg[jj] : dg[jj];
+              const double gg = rp.g_min + fabs(ui);
+              if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
+              const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
+              const double nl = dev_arg * exp(-up.v * x);
+              du = pos_active ? -nl : nl;
+            }
+          }
+          double noise = 0.0;
+          if constexpr (NOISE) {
+            if (dg[jj] != 0.0) {
+              const double sigma = up.gamma * sqrt(range * fabs(dg[jj]));
+              if (sigma != 0.0)
+                noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s),
+                                                     uint64_t(int64_t(i) * g.N + j0 + jj)));
+            }
+          }
+          double nu = ui - up.lr * (du + noise);
+          nu = nu > range ? range : nu;
+          nu = nu < -range ? -range : nu;
+          u[s][jj] = nu;
+          acc[jj] = acc[jj] * double(1u << g.db) + nu;
+          const double rpath = rp.aam ? (rrow[jj] + rcol) + rp.r_sense : 0.0;
+          const uint64_t idx = uint64_t(i) * g.Np + j0 + jj;
+          if constexpr (VAR) {
+            q[0][jj] = convert_q(rp, nu, s, 0, idx, rpath);
+            q[1][jj] = convert_q(rp, nu, s, 1, idx, rpath);
+          } else {
+            const int pa = nu > 0.0 ? 0 : 1;
+            const uint32_t qa = convert_q(rp, nu, s, pa, idx, rpath);
+            q[0][jj] = pa == 0 ? qa : qi[jj];
+            q[1][jj] = pa == 0 ? qi[jj] : qa;
+          }
+        }
+        st_vec<JPT>(mrow + s * sstride, u[s]);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          typename VecT<JPT>::B w[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int jj = 0; jj < JPT; ++jj) {
+            const uint32_t lo = q[p][jj] % 65025u, hi = q[p][jj] / 65025u;
+            w[0] |= typename VecT<JPT>::B((lo % 255u) << (8 * jj));
+            w[1] |= typename VecT<JPT>::B((lo / 255u) << (8 * jj));
+            w[2] |= typename VecT<JPT>::B((hi % 255u) << (8 * jj));
+            w[3] |= typename VecT<JPT>::B((hi / 255u) << (8 * jj));
+          }
+          uint8_t* d = dbase + (size_t(s) * 2 + p) * sp_stride;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) *reinterpret_cast<typename VecT<JPT>::B*>(d + k * plane) = w[k];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < JPT; ++jj) wmax = fmax(wmax, fabs(up.wfactor * acc[jj]));
     }
-    wmax = fmax(wmax, fabs(up.wfactor * acc));
   }
   wmax = warp_max(wmax);
   dwmax = warp_max(dwmax);
@@ -218,109 +333,53 @@ __global__ void k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ d
   }
 }
 
-// Same arithmetic as k_update, laid out for HBM: blockIdx.y = weight row i,
-// each thread owns 4 consecutive columns j (coalesced fp64 dW / master
-// read-modify-write) and emits each digit plane row segment as one packed
-// 32-bit store.  Per weight it moves 8 B dW + 16 B x S master + 8 B x S
-// conductance digits (both polarities) -- the K3b roofline bytes.
-__global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
-                                                 double* __restrict__ master, uint8_t* __restrict__ digits,
-                                                 DevScalars* sc, const uint32_t* __restrict__ qmin) {
-  const double range = rp.range;
+// Generic fallback (any S, ragged shapes): one weight per thread, runtime
+// flags, scalar stores.  Used when S is not 1/2/4/8 or JPT does not divide
+// N and tile_cols.
+__global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
+                                                    double* __restrict__ master, uint8_t* __restrict__ digits,
+                                                    DevScalars* sc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double wmax = 0.0, dwmax = 0.0;
-  const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-  for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
-    if (j0 >= g.N) break;
-    const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
-    int tcj[4], cj[4];
-    {
-      int tc = j0 / g.tile_cols, c = j0 - tc * g.tile_cols;
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        tcj[jj] = tc;
-        cj[jj] = c;
-        if (++c == g.tile_cols) { c = 0; ++tc; }
-      }
-    }
-    const bool vec = (g.tile_cols % 4 == 0) && (j0 + 3 < g.N);
-    const int nj = min(4, g.N - j0);
-    double dg[4], acc[4];
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const double dw = jj < nj ? dW[int64_t(i) * g.N + j0 + jj] : 0.0;
+  if (j < g.N) {
+    const int tc = j / g.tile_cols, c = j - tc * g.tile_cols;
+    const double range = rp.range;
+    for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
+      const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
+      const double dw = dW[size_t(i) * g.N + j];
       dwmax = fmax(dwmax, fabs(dw));
-      dg[jj] = dw * up.factor;  // scale_gradient (update.cpp:16-24)
-      acc[jj] = 0.0;
-    }
-    for (int s = g.S - 1; s >= 0; --s) {
-      double* urow = &master[(size_t(s) * g.Kp + i) * g.Np + j0];
-      uint32_t q[2][4];
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        if (jj >= nj) {
-          q[0][jj] = q[1][jj] = 0;
-          continue;
-        }
-        const double ui = urow[jj];
-        double du = dg[jj];
-        if (!up.linear && dg[jj] != 0.0) {
-          const bool pos_active = ui > 0.0 || (ui == 0.0 && dg[jj] < 0.0);
-          const double dev_arg = pos_active ? -dg[jj] : dg[jj];
+      const double dg = dw * up.factor;
+      const double rpath = rp.aam ? aam_rpath(rp, g, r, c) : 0.0;
+      const uint64_t idx = uint64_t(i) * g.Np + j;
+      double acc = 0.0;
+      for (int s = g.S - 1; s >= 0; --s) {
+        double* mp = master + (size_t(s) * g.Kp + i) * g.Np + j;
+        const double ui = *mp;
+        double du = dg;
+        if (!up.linear && dg != 0.0) {
+          const bool pos_active = ui > 0.0 || (ui == 0.0 && dg < 0.0);
+          const double dev_arg = pos_active ? -dg : dg;
           const double gg = rp.g_min + fabs(ui);
-          if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
+          if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);
           const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
           const double nl = dev_arg * exp(-up.v * x);
           du = pos_active ? -nl : nl;
         }
         double noise = 0.0;
-        if (up.gamma != 0.0 && dg[jj] != 0.0) {
-          const double sigma = up.gamma * sqrt(range * fabs(dg[jj]));
+        if (up.gamma != 0.0 && dg != 0.0) {
+          const double sigma = up.gamma * sqrt(range * fabs(dg));
           if (sigma != 0.0)
-            noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s),
-                                                 uint64_t(int64_t(i) * g.N + j0 + jj)));
+            noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s), uint64_t(int64_t(i) * g.N + j)));
         }
         double nu = ui - up.lr * (du + noise);
         if (nu > range) nu = range;
         if (nu < -range) nu = -range;
-        urow[jj] = nu;
-        acc[jj] = acc[jj] * double(1u << g.db) + nu;
-        if (qmin) {
-          // sigma == 0: the inactive polarity sits exactly at g_min (mapping.cpp:39-45),
-          // whose snapped non-ideal value depends only on the tile position.
-          const int pa = nu > 0.0 ? 0 : 1;
-          const uint32_t qa = convert_device_rc(rp, g, nu, s, pa, i, j0 + jj, r, cj[jj]);
-          const uint32_t qi = qmin[r * g.tile_cols + cj[jj]];
-          q[0][jj] = pa == 0 ? qa : qi;
-          q[1][jj] = pa == 0 ? qi : qa;
-        } else {
-#pragma unroll
-          for (int p = 0; p < 2; ++p) q[p][jj] = convert_device_rc(rp, g, nu, s, p, i, j0 + jj, r, cj[jj]);
-        }
+        *mp = nu;
+        acc = acc * double(1u << g.db) + nu;
+        for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_q(rp, nu, s, p, idx, rpath));
       }
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        if (vec) {
-          uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const uint32_t lo = q[p][jj] % 65025u, hi = q[p][jj] / 65025u;
-            w[0] |= (lo % 255u) << (8 * jj);
-            w[1] |= (lo / 255u) << (8 * jj);
-            w[2] |= (hi % 255u) << (8 * jj);
-            w[3] |= (hi / 255u) << (8 * jj);
-          }
-          const size_t off = size_t(r) * g.C + cj[0];
-#pragma unroll
-          for (int d = 0; d < 4; ++d)
-            *reinterpret_cast<uint32_t*>(digits + g.tile_digit_offset(s, p, tr, tcj[0], d) + off) = w[d];
-        } else {
-          for (int jj = 0; jj < nj; ++jj) store_digits(digits, g, s, p, i, j0 + jj, q[p][jj]);
-        }
-      }
+      wmax = fmax(wmax, fabs(up.wfactor * acc));
     }
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-      if (jj < nj) wmax = fmax(wmax, fabs(up.wfactor * acc[jj]));
   }
   wmax = warp_max(wmax);
   dwmax = warp_max(dwmax);
@@ -330,11 +389,36 @@ __global__ void __launch_bounds__(256) k_update4(Geo g, RegenP rp, UpdP up, cons
   }
 }
 
+template <int S, int JPT>
+static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st) {
+  const dim3 grid((c->g.N / JPT + 255) / 256, std::min(c->g.K, 65535));
+  const bool var = c->rp.sigma != 0.0, nl = !up.linear, noise = up.gamma != 0.0;
+  auto go = [&](auto kern) {
+    kern<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
+  };
+  if (!var && !nl && !noise) go(k_update<S, JPT, false, false, false>);
+  else if (var && !nl && !noise) go(k_update<S, JPT, true, false, false>);
+  else if (!var) go(k_update<S, JPT, false, true, true>);
+  else go(k_update<S, JPT, true, true, true>);
+}
+
+template <int JPT>
+static bool launch_update_j(const xbs_core* c, const UpdP& up, cudaStream_t st) {
+  if (c->g.N % JPT || c->g.tile_cols % JPT || c->g.C % JPT) return false;
+  switch (c->g.S) {
+    case 1: launch_update_s<1, JPT>(c, up, st); return true;
+    case 2: launch_update_s<2, JPT>(c, up, st); return true;
+    case 4: launch_update_s<4, JPT>(c, up, st); return true;
+    case 8: launch_update_s<8, JPT>(c, up, st); return true;
+    default: return false;
+  }
+}
+
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st) {
-  const int bx = (c->g.N + 4 * 256 - 1) / (4 * 256);
-  const int by = std::min(c->g.K, 65535);
-  k_update4<<<dim3(bx, by), 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
-  (void)k_update;
+  if (launch_update_j<4>(c, up, st)) return;
+  if (launch_update_j<2>(c, up, st)) return;
+  const dim3 grid((c->g.N + 255) / 256, std::min(c->g.K, 65535));
+  k_update_any<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
 }
 
 // q(g_min) per tile position (sigma == 0 only): tile_rows x tile_cols
@@ -342,13 +426,11 @@ __global__ void k_qmin(Geo g, RegenP rp, uint32_t* qmin) {
   const int n = g.tile_rows * g.tile_cols;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int r = t / g.tile_cols, c = t % g.tile_cols;
-    qmin[t] = convert_device_rc(rp, g, 0.0, 0, 0, r, c, r, c);
+    qmin[t] = convert_q(rp, 0.0, 0, 0, 0, rp.aam ? aam_rpath(rp, g, r, c) : 0.0);
   }
 }
 
-void launch_qmin(const xbs_core* c, cudaStream_t st) {
-  k_qmin<<<64, 256, 0, st>>>(c->g, c->rp, c->d_qmin);
-}
+void launch_qmin(const xbs_core* c, cudaStream_t st) { k_qmin<<<64, 256, 0, st>>>(c->g, c->rp, c->d_qmin); }
 
 // implied_weights() (mapping.cpp:70-81) -> K x N row-major
 __global__ void k_implied(Geo g, double wfactor, const double* __restrict__ master, double* __restrict__ out) {
