@@ -1,15 +1,17 @@
 // K3a: the digital weight gradient dW = x_values^T dy_q / grad_divisor
 // (layers.cpp:304) as an exact integer outer product on tcgen05 kind::i8:
 //     S[i, j] = sum_b xcode[b, i] * (plus[b, j] - minus[b, j])
-// with the u8 activation codes as A (MN-major) and the u8 plus / minus error
-// magnitudes side by side in N (MN-major), s32 accumulation in TMEM (exact
-// for batch <= 33025), then dW = ((S * sx) * step_e) / grad_divisor in fp64
-// (the snapped-mode contract), written row-major [i][j].
+// computed transposed, D[j, i]: the u8 plus and minus error magnitudes are
+// two A operands (M = 128 columns j, MN-major), the u8 activation codes the
+// B operand (N = 128 rows i, MN-major), two s32 TMEM accumulators (exact for
+// batch <= 33025).  dW = ((S * sx) * step_e) / grad_divisor in fp64 (the
+// snapped-mode contract), written row-major [i][j]: TMEM lane
+// = column j, so each warp store covers 32 consecutive j (256 B) of a row.
 //
-// Unit = 128 rows i x 128 columns j; K loop over 128-row batch blocks.
+// Unit = 128 columns j x 128 rows i; K loop over 128-row batch blocks.
 // Warp roles as in the VMM kernels (TMA producer, MMA issuer, 8 epilogue
-// warps); the TMEM accumulator is double buffered so the epilogue's stores
-// overlap the next unit's MMAs.
+// warps); the TMEM accumulator pair is double buffered so the epilogue's
+// stores overlap the next unit's MMAs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -23,7 +25,7 @@ namespace dw {
 constexpr int kThreads = 320;
 constexpr int kStages = 4;
 constexpr int kBox = 128 * 128;
-constexpr int kStage = 3 * kBox;  // A | plus | minus
+constexpr int kStage = 3 * kBox;  // plus | minus | x codes
 constexpr int kSmem = kStages * kStage + 1024 + 256;
 }  // namespace dw
 
@@ -73,16 +75,16 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
           mbar_wait(&empty[st], ph ^ 1);
           mbar_expect_tx(&full[st], kStage);
           uint8_t* dst = smem + st * kStage;
-          tma_load_2d(dst, &mapA, &full[st], ib * 128, kb * 128);
-          tma_load_2d(dst + kBox, &mapE, &full[st], jb * 128, kb * 128);
-          tma_load_2d(dst + 2 * kBox, &mapE, &full[st], jb * 128, int(a.Mcap8) + kb * 128);
+          tma_load_2d(dst, &mapE, &full[st], jb * 128, kb * 128);
+          tma_load_2d(dst + kBox, &mapE, &full[st], jb * 128, int(a.Mcap8) + kb * 128);
+          tma_load_2d(dst + 2 * kBox, &mapA, &full[st], ib * 128, kb * 128);
           if (++st == kStages) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer: A MN-major (i), B MN-major (plus | minus)
-      constexpr uint32_t idesc = idesc_i8(128, 256, true) | (1u << 15);
+    if (lane == 0) {  // MMA issuer: A = plus / minus (MN-major, j), B = x codes (MN-major, i)
+      constexpr uint32_t idesc = idesc_i8(128, 128, true) | (1u << 15);
       uint32_t st = 0, ph = 0, ab = 0, abph = 0;
       for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
         mbar_wait(&t_empty[ab], abph ^ 1);
@@ -94,9 +96,12 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
           const uint32_t s0 = smem_u32(smem + st * kStage);
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad = sdesc(s0 + 4096 * ks, kBox, 1024, 2);
-            const uint64_t bd = sdesc(s0 + kBox + 4096 * ks, kBox, 1024, 2);
-            umma_i8(td, ad, bd, idesc, (kb | ks) != 0);
+            const uint64_t bd = sdesc(s0 + 2 * kBox + 4096 * ks, kBox, 1024, 2);
+#pragma unroll
+            for (int pm = 0; pm < 2; ++pm) {
+              const uint64_t ad = sdesc(s0 + pm * kBox + 4096 * ks, kBox, 1024, 2);
+              umma_i8(td + pm * 128, ad, bd, idesc, (kb | ks) != 0);
+            }
           }
           umma_commit(&empty[st]);
           if (++st == kStages) { st = 0; ph ^= 1; }
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
     uint32_t ab = 0, abph = 0;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int ib = u % a.num_ib, jb = u / a.num_ib;
-      const int i = ib * 128 + 32 * lg + lane;
+      const int j = jb * 128 + 32 * lg + lane;
       mbar_wait(&t_full[ab], abph);
       tc_fence_after();
       const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + 64 * ch;
@@ -127,13 +132,12 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[ab]);
         }
-        const int j0 = jb * 128 + 64 * ch + 16 * q;
-        if (i < a.K) {
-          double* row = a.dW + int64_t(i) * a.N;
+        const int i0 = ib * 128 + 64 * ch + 16 * q;
+        if (j < a.N) {
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int S = int(pv[jj]) - int(mv[jj]);
-            if (j0 + jj < a.N) row[j0 + jj] = ((double(S) * a.sx) * step_e) / a.gd;
+          for (int ii = 0; ii < 16; ++ii) {
+            const int S = int(pv[ii]) - int(mv[ii]);
+            if (i0 + ii < a.K) a.dW[int64_t(i0 + ii) * a.N + j] = ((double(S) * a.sx) * step_e) / a.gd;
           }
         }
       }

@@ -81,13 +81,26 @@ def test_forward_backward_dw_bit_exact(case, kernel):
     assert np.array_equal(gpu.gradient(), orc.gradient())
 
 
+UPDATE_CASES = [
+    # (K, N, opt kwargs): each hits a different specialisation of K3b
+    (100, 70, dict(sigma=0.1, v=0.5, gamma=2.0)),          # 2 weights/thread, variation + nonlinear + noise
+    (100, 72, dict(sigma=0.0, v=0.5, gamma=2.0)),          # 4 weights/thread, qmin table + nonlinear + noise
+    (50, 33, dict(sigma=0.1, v=0.5, gamma=2.0)),           # odd N: generic one-weight-per-thread kernel
+    (96, 64, dict(sigma=0.0, wb=8, db=1, lr=0.5)),         # S = 8, linear, sigma = 0
+    (80, 128, dict(sigma=0.2, wb=8, db=4, lr=0.5)),        # S = 2, linear, variation
+]
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_update_and_regeneration(kernel):
-    opt = aam_options(tile=64, adc_bits=6, i_fs=6e-5, sigma=0.1, v=0.5, gamma=2.0, lr=0.3, useed=7, vseed=3)
-    W = normal((100, 70), 1, 0.05)
+@pytest.mark.parametrize("ucase", range(len(UPDATE_CASES)))
+def test_update_and_regeneration(kernel, ucase):
+    K, N, kw = UPDATE_CASES[ucase]
+    kw = dict(dict(lr=0.3), **kw)
+    opt = aam_options(tile=64, adc_bits=6, i_fs=6e-5, useed=7, vseed=3, **kw)
+    W = normal((K, N), 1, 0.05)
     gpu, orc = _pair(W, opt, kernel)
-    x = rand((6, 100), 2, 0.0, 1.0)
-    dy = rand((6, 70), 3)
+    x = rand((6, K), 2, 0.0, 1.0)
+    dy = rand((6, N), 3)
     for it in range(3):
         gpu.forward(x, True)
         orc.forward(x, True)
