@@ -257,37 +257,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
+    // Per chain a warp converts kRows = 16 rows x 2 polarities as four
+    // 8-column chunks, TMEM loads software-pipelined as in K1.
     constexpr int kRows = 64 / (kEpiWarps / 4);  // output rows per epilogue warp
+    static_assert(kRows == 16, "four 8-column chunks per chain");
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
     const int phi = ml & 1;
+    const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kRows * ch;
     uint32_t ab = 0, abph = 0, exact = 0;
+    bool pref = false;
+    uint32_t lA[8], hA[8], lB[8], hB[8];
     const AdcConst k = a.adc;
     const double se = a.sc->se;
     const double step_e = se > 0 ? se / a.lev_e : 0.0;
     double k_out = step_e * a.F / a.vu;  // layers.cpp:375-377
     if (a.adc_scaled) k_out *= a.ifs_fac;
+    const int nchain = a.GC * a.S;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int mb = u % a.num_mb, rb = u / a.num_mb;
       const int tr = rb / rhalves, rh = rb % rhalves;
       float P[kRows];
 #pragma unroll
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
-      for (int tc = 0; tc < a.GC; ++tc)
-        for (int s = 0; s < a.S; ++s) {
-          const float w = float(1 << (s * a.db));
-          const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
-          const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
+      for (int c = 0; c < nchain; ++c) {
+        const int s = c % a.S;  // chains run tc-major, then slice
+        const float w = float(1 << (s * a.db));
+        const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
+        const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
+        const uint32_t ta = tl + ab * 256;
+        if (!pref) {
           mbar_wait_sleep(&t_full[ab], abph);
           tc_fence_after();
-          const uint32_t ta = tmem + (uint32_t(32 * lg) << 16) + ab * 256 + kRows * ch;
-          constexpr int QP = kRows / 8;  // chunks per polarity
-#pragma unroll
-          for (int q = 0; q < 2 * QP; ++q)
-            adc_chunk8s(ta + (q / QP) * 128 + 8 * (q % QP), ta + (q / QP) * 128 + 64 + 8 * (q % QP), k,
-                        q < QP ? wpos : wneg, P, 8 * (q % QP), exact, q == 2 * QP - 1 ? &t_empty[ab] : nullptr);
-          if (++ab == 2) { ab = 0; abph ^= 1; }
+          tmem_ld8(ta, lA);
+          tmem_ld8(ta + 64, hA);
         }
+        tmem_wait_ld();
+        tmem_ld8(ta + 8, lB);
+        tmem_ld8(ta + 64 + 8, hB);
+        adc_conv8<0>(lA, hA, k, wpos, P, 0, exact);
+        tmem_wait_ld();
+        tmem_ld8(ta + 128, lA);
+        tmem_ld8(ta + 128 + 64, hA);
+        adc_conv8<0>(lB, hB, k, wpos, P, 8, exact);
+        tmem_wait_ld();
+        tmem_ld8(ta + 128 + 8, lB);
+        tmem_ld8(ta + 128 + 64 + 8, hB);
+        adc_conv8<0>(lA, hA, k, wneg, P, 0, exact);
+        tmem_wait_ld();
+        tmem_release(&t_empty[ab]);
+        if (++ab == 2) { ab = 0; abph ^= 1; }
+        pref = mbar_try(&t_full[ab], abph);
+        if (pref) {
+          tc_fence_after();
+          tmem_ld8(tl + ab * 256, lA);
+          tmem_ld8(tl + ab * 256 + 64, hA);
+        }
+        adc_conv8<0>(lB, hB, k, wneg, P, 8, exact);
+      }
       // combine the 2*TPe (plane, phase) lanes of each batch row
       const int grp = 2 * a.TPe;
       const int kk = (ml % grp) >> 1;
