@@ -212,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       for (int c = 0; c < nchain; ++c) {
         const int sp = c % (2 * a.S);  // chains run tr-major, then slice, then polarity
         const float w = (sp & 1) == 0 ? float(1 << ((sp >> 1) * a.db)) : -float(1 << ((sp >> 1) * a.db));
-        mbar_wait(&t_full[ab], abph);
+        mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         if (a.dbg & 1) {
           tc_fence_before();

@@ -72,6 +72,25 @@ __device__ __forceinline__ uint32_t convert_q(const RegenP& rp, double u, int s,
   return __double2uint_rn(__dmul_rn(gv, rp.snap_scale));  // nearbyint(ldexp(gv, e))
 }
 
+// Compile-time specialised conversion for the update kernel.  VAR: sigma
+// != 0; AAM: AAM engine with a non-zero path resistance.  g_min > 0
+// (CrossbarConfig::validate) and the variation multiplier >= 1e-12, so gv
+// is never 0 here; max(+-u, 0) + g_min is written as a select (an exact -0
+// or +0 adds to g_min identically).
+template <bool VAR, bool AAM>
+__device__ __forceinline__ uint32_t convert_qt(const RegenP& rp, double u, int s, int p, uint64_t idx,
+                                               double rpath) {
+  const double up = p == 0 ? u : -u;
+  double gv = (up > 0.0 ? up : 0.0) + rp.g_min;
+  if constexpr (VAR) {
+    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, idx, 0));
+    m = m > 1e-12 ? m : 1e-12;
+    gv = fmin(gv * m, rp.g_max);
+  }
+  if constexpr (AAM) gv = __drcp_rn(__dadd_rn(__drcp_rn(gv), rpath));
+  return __double2uint_rn(__dmul_rn(gv, rp.snap_scale));
+}
+
 __device__ __forceinline__ void store_digits(uint8_t* digits, const Geo& g, int s, int p, int i, int j,
                                              uint32_t q) {
   const int tr = i / g.tile_rows, r = i % g.tile_rows, tc = j / g.tile_cols, c = j % g.tile_cols;
@@ -214,7 +233,7 @@ __device__ __forceinline__ void st_vec(double* p, const double (&v)[JPT]) {
   *reinterpret_cast<typename VecT<JPT>::D*>(p) = t;
 }
 
-template <int S_T, int JPT, bool VAR, bool NL, bool NOISE>
+template <int S_T, int JPT, bool VAR, bool NL, bool NOISE, bool AAM>
 __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
                                                 double* __restrict__ master, uint8_t* __restrict__ digits,
                                                 DevScalars* sc, const uint32_t* __restrict__ qmin) {
@@ -292,14 +311,14 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
           nu = nu < -range ? -range : nu;
           u[s][jj] = nu;
           acc[jj] = acc[jj] * double(1u << g.db) + nu;
-          const double rpath = rp.aam ? (rrow[jj] + rcol) + rp.r_sense : 0.0;
+          const double rpath = AAM ? (rrow[jj] + rcol) + rp.r_sense : 0.0;
           const uint64_t idx = uint64_t(i) * g.Np + j0 + jj;
           if constexpr (VAR) {
-            q[0][jj] = convert_q(rp, nu, s, 0, idx, rpath);
-            q[1][jj] = convert_q(rp, nu, s, 1, idx, rpath);
+            q[0][jj] = convert_qt<true, AAM>(rp, nu, s, 0, idx, rpath);
+            q[1][jj] = convert_qt<true, AAM>(rp, nu, s, 1, idx, rpath);
           } else {
             const int pa = nu > 0.0 ? 0 : 1;
-            const uint32_t qa = convert_q(rp, nu, s, pa, idx, rpath);
+            const uint32_t qa = convert_qt<false, AAM>(rp, nu, s, pa, idx, rpath);
             q[0][jj] = pa == 0 ? qa : qi[jj];
             q[1][jj] = pa == 0 ? qi[jj] : qa;
           }
@@ -393,13 +412,24 @@ template <int S, int JPT>
 static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st) {
   const dim3 grid((c->g.N / JPT + 255) / 256, std::min(c->g.K, 65535));
   const bool var = c->rp.sigma != 0.0, nl = !up.linear, noise = up.gamma != 0.0;
+  // AAM with a zero path resistance everywhere is the identity conversion
+  const bool aam = c->rp.aam && (c->rp.r_source + c->rp.r_row + c->rp.r_col + c->rp.r_sense) > 0.0;
   auto go = [&](auto kern) {
     kern<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
   };
-  if (!var && !nl && !noise) go(k_update<S, JPT, false, false, false>);
-  else if (var && !nl && !noise) go(k_update<S, JPT, true, false, false>);
-  else if (!var) go(k_update<S, JPT, false, true, true>);
-  else go(k_update<S, JPT, true, true, true>);
+#define XBS_UPD(V, N, A) go(k_update<S, JPT, V, N, N, A>)
+  if (aam) {
+    if (!var && !nl && !noise) XBS_UPD(false, false, true);
+    else if (var && !nl && !noise) XBS_UPD(true, false, true);
+    else if (!var) XBS_UPD(false, true, true);
+    else XBS_UPD(true, true, true);
+  } else {
+    if (!var && !nl && !noise) XBS_UPD(false, false, false);
+    else if (var && !nl && !noise) XBS_UPD(true, false, false);
+    else if (!var) XBS_UPD(false, true, false);
+    else XBS_UPD(true, true, false);
+  }
+#undef XBS_UPD
 }
 
 template <int JPT>

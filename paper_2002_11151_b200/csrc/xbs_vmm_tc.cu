@@ -286,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float w = float(1 << (s * a.db));
         const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
         const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
-        mbar_wait(&t_full[ab], abph);
+        mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         const uint32_t ta = tl + ab * 256;
         uint32_t lo[16], hi[16];
