@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-peak", action="store_true", help="skip the live int8 peak GEMM (ncu launch lists)")
+    p.add_argument("--all-layers", action="store_true",
+                   help="every layer of the config (C1/C3/C4 networks), one core per layer on one stream")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
     return p.parse_args()
 
@@ -247,49 +249,63 @@ def main():
     init_dist(world, local_rank, "nccl")
     from paper_2002_11151_b200 import xbarsim as xb
 
-    layer = cfg.layers[0]
-    M, K, N = layer.M, layer.K, layer.N
+    layers = list(cfg.layers) if args.all_layers else [cfg.layers[0]]
     opt = cfg.options()
-    W, x, dy = cfg.weights(layer), cfg.inputs(layer), cfg.errors(layer)
-    core = xb.CrossbarCore(W, opt)
-    stream = torch.cuda.ExternalStream(core.stream())
-    # device-resident operands, column-major (Eigen layout): (K, M) C-order == M x K col-major
-    d_x = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
-    d_dy = torch.from_numpy(np.ascontiguousarray(dy.T)).cuda()
-    d_y = torch.empty((N, M), dtype=torch.float64, device="cuda")
-    d_dx = torch.empty((K, M), dtype=torch.float64, device="cuda")
+    cores, host, dev = [], [], []
+    for li, layer in enumerate(layers):
+        W, x, dy = cfg.weights(layer, li), cfg.inputs(layer, li), cfg.errors(layer, li)
+        cores.append(xb.CrossbarCore(W, opt))
+        host.append((x, dy))
+        # device-resident operands, column-major (Eigen layout): (K, M) C-order == M x K col-major
+        dev.append((torch.from_numpy(np.ascontiguousarray(x.T)).cuda(),
+                    torch.from_numpy(np.ascontiguousarray(dy.T)).cuda(),
+                    torch.empty((layer.N, layer.M), dtype=torch.float64, device="cuda"),
+                    torch.empty((layer.K, layer.M), dtype=torch.float64, device="cuda")))
+    for c in cores[1:]:
+        c.set_stream(cores[0].stream())  # one stream for the whole network
+    stream = torch.cuda.ExternalStream(cores[0].stream())
     torch.cuda.synchronize()
 
     it = [0]
 
     def step():
-        core.forward_device(d_x.data_ptr(), M, True, d_y.data_ptr())
-        core.backward_device(d_dy.data_ptr(), M, 1.0, d_dx.data_ptr())
-        core.apply_updates_device(it[0])
+        for c, layer, (d_x, d_dy, d_y, d_dx) in zip(cores, layers, dev):
+            c.forward_device(d_x.data_ptr(), layer.M, True, d_y.data_ptr())
+        for c, layer, (d_x, d_dy, d_y, d_dx) in reversed(list(zip(cores, layers, dev))):
+            c.backward_device(d_dy.data_ptr(), layer.M, 1.0, d_dx.data_ptr())
+        for c in cores:
+            c.apply_updates_device(it[0])
         it[0] += 1
 
     for _ in range(args.warmup):
         step()
-    core.synchronize()
+    for c in cores:
+        c.synchronize()
     torch.cuda.synchronize()
     barrier(world)
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    launches0 = core.launch_count()
-    core.profile(True)
+    launches0 = sum(c.launch_count() for c in cores)
+    for c in cores:
+        c.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     e1.synchronize()
-    core.synchronize()
+    for c in cores:
+        c.synchronize()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    stages = core.stage_times()
-    core.profile(False)
-    launches = core.launch_count() - launches0
+    stages = {}
+    for c in cores:
+        for k, (t, n) in c.stage_times().items():
+            t0, n0 = stages.get(k, (0.0, 0))
+            stages[k] = (t0 + t, n0 + n)
+        c.profile(False)
+    launches = sum(c.launch_count() for c in cores) - launches0
     barrier(world)
     ms = max_over_ranks(ms, world, "cuda")
 
@@ -299,46 +315,65 @@ def main():
         def pinned(rows, cols):  # F-ordered (rows x cols) numpy view of pinned memory
             return torch.empty((cols, rows), dtype=torch.float64, pin_memory=True).numpy().T
 
-        hx, hdy, hy, hdx = pinned(M, K), pinned(M, N), pinned(M, N), pinned(M, K)
-        hx[:] = x
-        hdy[:] = dy
-        for _ in range(max(3, args.warmup)):
-            core.forward(hx, True, out=hy)
-            core.backward(hdy, 1.0, out=hdx)
-            core.apply_updates(it[0])
+        hbuf = []
+        for layer, (x, dy) in zip(layers, host):
+            hx, hdy, hy, hdx = pinned(layer.M, layer.K), pinned(layer.M, layer.N), pinned(layer.M, layer.N), pinned(
+                layer.M, layer.K)
+            hx[:] = x
+            hdy[:] = dy
+            hbuf.append((hx, hdy, hy, hdx))
+
+        def host_step():
+            for c, (hx, hdy, hy, hdx) in zip(cores, hbuf):
+                c.forward(hx, True, out=hy)
+            for c, (hx, hdy, hy, hdx) in reversed(list(zip(cores, hbuf))):
+                c.backward(hdy, 1.0, out=hdx)
+            for c in cores:
+                c.apply_updates(it[0])
             it[0] += 1
-        core.synchronize()
+
+        for _ in range(max(3, args.warmup)):
+            host_step()
+        for c in cores:
+            c.synchronize()
         barrier(world)
-        # the host calls are synchronous; events on the core's stream bracket
-        # every H2D copy, kernel and D2H copy of the K steps
+        # the host calls are synchronous; events on the (shared) stream
+        # bracket every H2D copy, kernel and D2H copy of the K steps
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         f0.record(stream)
         for _ in range(args.steps):
-            core.forward(hx, True, out=hy)
-            core.backward(hdy, 1.0, out=hdx)
-            core.apply_updates(it[0])
-            it[0] += 1
+            host_step()
         f1.record(stream)
         f1.synchronize()
         wall_s = (time.perf_counter() - t0) / args.steps
         e2e_s = max_over_ranks(f0.elapsed_time(f1) * 1e-3 / args.steps, world, "cuda")
-        e2e = {"h2d_bytes_per_step": 8 * M * (K + N), "d2h_bytes_per_step": 8 * M * (N + K), "s": e2e_s,
+        bi = sum(8 * L.M * (L.K + L.N) for L in layers)
+        e2e = {"h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi, "s": e2e_s,
                "wall_s": max_over_ranks(wall_s, world, "cuda")}
     clk = clocks.stop()
 
-    macs = cfg.macs(layer)
+    macs = {}
+    for L in layers:
+        for k, v in cfg.macs(L).items():
+            macs[k] = macs.get(k, 0) + v
     S = cfg.weight_bits // cfg.device_bits
     peak_tops, peak_src = (4500.0, "NVIDIA dense int8 spec (--no-peak)") if args.no_peak else measure_int8_peak()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in stages.items()}
-    work = {  # algorithmic work per launch of each stage
+    per = {k: (v[0] / v[1] * len(layers) if v[1] else 0.0) for k, v in stages.items()}  # ms per step
+    work = {  # algorithmic work per step of each stage
         "fwd_vmm": ("tensor", 2 * L_LIMBS * macs["fwd"] / 1e12, "TFLOP/s"),
         "bwd_vmm": ("tensor", 2 * L_LIMBS * macs["bwd"] / 1e12, "TFLOP/s"),
-        "dw": ("tensor", 2 * macs["upd"] / 1e12, "TFLOP/s"),
-        "update": ("hbm", K * N * (24 * S + 8) / 1e9, "GB/s"),
+        # dW: an M-deep outer product whose cost is writing K x N fp64 and
+        # reading the u8 codes -- HBM-bound
+        "dw": ("hbm", sum(8 * L.K * L.N + L.M * (L.K + 2 * L.N) for L in layers) / 1e9, "GB/s"),
+        "update": ("hbm", sum(L.K * L.N * (24 * S + 8) for L in layers) / 1e9, "GB/s"),
+        # input / error quantisation + bit-plane emission: read fp64, write
+        # codes and the two u8 plane copies (x: T_in planes; dy: 2 T_err)
+        "prep_x": ("hbm", sum(L.M * L.K * (8 + 2 + 1 + 2 * 8) for L in layers) / 1e9, "GB/s"),
+        "prep_dy": ("hbm", sum(L.M * L.N * (8 + 2 + 2 + 4 * 8) for L in layers) / 1e9, "GB/s"),
     }
     roof_all = {}
     for st, (bound, amount, unit) in work.items():
@@ -347,7 +382,7 @@ def main():
             pk = peak_tops if bound == "tensor" else hbm
             roof_all[st] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk,
                             "ms": per[st]}
-    dominant = max(("fwd_vmm", "bwd_vmm", "update", "dw"), key=lambda s: per.get(s, 0.0))
+    dominant = max(("fwd_vmm", "bwd_vmm", "update", "dw", "prep_x", "prep_dy"), key=lambda s: per.get(s, 0.0))
     traffic = None
     tpath = args.traffic or os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tpath):
@@ -361,10 +396,13 @@ def main():
         "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic",
-        "config": {"workload": cfg.name, "M": M, "K": K, "N": N, "tile": cfg.tile, "slices": S,
-                   "adc_bits": cfg.adc_bits, "parallelism": f"replicas{world}",
-                   "l2": "inputs larger than L2 (conductance digits %.0f MB/step > 126 MB)" % (
-                       2 * S * K * N * 4 / 1e6)},
+        "config": dict(
+            {"workload": cfg.name, "tile": cfg.tile, "slices": S, "adc_bits": cfg.adc_bits,
+             "parallelism": f"replicas{world}",
+             "l2": "conductance digits %.0f MB read per pass (L2 126 MB)" % (
+                 sum(2 * S * L.K * L.N * 4 for L in layers) / 1e6)},
+            **({"layers": [[L.M, L.K, L.N] for L in layers]} if len(layers) > 1 else
+               {"M": layers[0].M, "K": layers[0].K, "N": layers[0].N})),
         "roofline": roof,
         "roofline_stages": roof_all,
         "int8_peak_tops": peak_tops,

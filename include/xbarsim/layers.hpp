@@ -153,6 +153,8 @@ class CrossbarCore {
     grad_valid_ = false;
   }
   void synchronize() { detail::check(xbs_core_synchronize(h_.get())); }
+  /// Enqueue on the caller's cudaStream_t (nullptr: a private stream).
+  void set_stream(void* stream) { detail::check(xbs_core_set_stream(h_.get(), stream)); }
   xbs_core* handle() const { return h_.get(); }
 
  private:

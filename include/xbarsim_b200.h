@@ -153,6 +153,10 @@ int xbs_core_adc_counters(xbs_core* core, int64_t* exact_path, int64_t* conversi
 int xbs_core_select_kernel(xbs_core* core, int32_t kernel);
 /* CUDA stream (cudaStream_t) the core enqueues on, as an opaque pointer. */
 void* xbs_core_stream(xbs_core* core);
+/* Enqueue on the caller's stream from now on (e.g. all layers of a network
+ * on one stream); the core never destroys a caller's stream.  NULL returns
+ * to a private stream.  Waits for work queued on the previous stream. */
+int xbs_core_set_stream(xbs_core* core, void* stream);
 
 /* Per-stage device timing (CUDA events recorded on the core's stream around
  * each stage while enabled).  Stages: 0 prep_x (K0a), 1 forward VMM (K1),

@@ -557,6 +557,7 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_ecodes);
   cudaFree(c->d_xc8);
   cudaFree(c->d_e8);
+  cudaFree(c->d_S64);
   cudaFree(c->d_io_in);
   cudaFree(c->d_io_out);
   for (auto& p : c->pending) {
@@ -564,7 +565,7 @@ void xbs_core_destroy(xbs_core* c) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 
@@ -757,6 +758,21 @@ int xbs_core_select_kernel(xbs_core* c, int32_t kernel) {
 }
 
 void* xbs_core_stream(xbs_core* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int xbs_core_set_stream(xbs_core* c, void* stream) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    sync(c);  // work already queued on the old stream completes first
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      c->own_stream = true;
+    }
+  });
+}
 
 int xbs_core_profile(xbs_core* c, int32_t enable) {
   return guard([&] {

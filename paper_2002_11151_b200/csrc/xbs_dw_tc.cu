@@ -8,7 +8,12 @@
 // snapped-mode contract), written row-major [i][j]: TMEM lane
 // = column j, so each warp store covers 32 consecutive j (256 B) of a row.
 //
-// Unit = 128 columns j x 128 rows i; K loop over 128-row batch blocks.
+// Unit = 128 columns j x 128 rows i x one slice of the batch (K loop over
+// its 128-row blocks).  Deep, narrow im2col layers (C3/C4: up to 401408
+// batch rows, K x N of one or two tiles) are split along the batch so every
+// SM has work and every partial stays exact in s32 (<= 32768 rows x 255 x
+// 255); the partials are added in int64 (atomics on S64) and k_dw_finalize
+// applies the fp64 contract.  Shallow layers write dW directly.
 // Warp roles as in the VMM kernels (TMA producer, MMA issuer, 8 epilogue
 // warps); the TMEM accumulator pair is double buffered so the epilogue's
 // stores overlap the next unit's MMAs.
@@ -31,6 +36,9 @@ constexpr int kSmem = kStages * kStage + 1024 + 256;
 
 struct DwArgs {
   int K, N, num_ib, num_units, kblocks;
+  int ntiles, kb_chunk;  // units = ntiles x batch chunks of kb_chunk 128-row blocks
+  int NA;
+  unsigned long long* S64;  // split mode: int64 partial sums [KA][NA]; nullptr: direct dW
   int64_t Mcap8;
   double sx, lev_e, gd;
   const DevScalars* sc;
@@ -70,8 +78,10 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
     if (lane == 0) {  // TMA producer
       uint32_t st = 0, ph = 0;
       for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        const int ib = u % a.num_ib, jb = u / a.num_ib;
-        for (int kb = 0; kb < a.kblocks; ++kb) {
+        const int t = u % a.ntiles, chunk = u / a.ntiles;
+        const int ib = t % a.num_ib, jb = t / a.num_ib;
+        const int kb1 = min(a.kblocks, (chunk + 1) * a.kb_chunk);
+        for (int kb = chunk * a.kb_chunk; kb < kb1; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
           mbar_expect_tx(&full[st], kStage);
           uint8_t* dst = smem + st * kStage;
@@ -90,7 +100,8 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
         mbar_wait(&t_empty[ab], abph ^ 1);
         tc_fence_after();
         const uint32_t td = tmem + ab * 256;
-        for (int kb = 0; kb < a.kblocks; ++kb) {
+        const int chunk = u / a.ntiles, kb0 = chunk * a.kb_chunk, kb1 = min(a.kblocks, kb0 + a.kb_chunk);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint32_t s0 = smem_u32(smem + st * kStage);
@@ -100,7 +111,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
 #pragma unroll
             for (int pm = 0; pm < 2; ++pm) {
               const uint64_t ad = sdesc(s0 + pm * kBox + 4096 * ks, kBox, 1024, 2);
-              umma_i8(td + pm * 128, ad, bd, idesc, (kb | ks) != 0);
+              umma_i8(td + pm * 128, ad, bd, idesc, (kb != kb0 || ks != 0));
             }
           }
           umma_commit(&empty[st]);
@@ -116,7 +127,8 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
     const double step_e = se > 0 ? se / a.lev_e : 0.0;
     uint32_t ab = 0, abph = 0;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      const int ib = u % a.num_ib, jb = u / a.num_ib;
+      const int t = u % a.ntiles;
+      const int ib = t % a.num_ib, jb = t / a.num_ib;
       const int j = jb * 128 + 32 * lg + lane;
       mbar_wait(&t_full[ab], abph);
       tc_fence_after();
@@ -137,7 +149,13 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
 #pragma unroll
           for (int ii = 0; ii < 16; ++ii) {
             const int S = int(pv[ii]) - int(mv[ii]);
-            if (i0 + ii < a.K) a.dW[int64_t(i0 + ii) * a.N + j] = ((double(S) * a.sx) * step_e) / a.gd;
+            if (i0 + ii < a.K) {
+              if (a.S64) {
+                if (S != 0) atomicAdd(&a.S64[int64_t(i0 + ii) * a.NA + j], (unsigned long long)(long long)S);
+              } else {
+                a.dW[int64_t(i0 + ii) * a.N + j] = ((double(S) * a.sx) * step_e) / a.gd;
+              }
+            }
           }
         }
       }
@@ -149,11 +167,27 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// Split mode: dW = ((S * sx) * step_e) / grad_divisor from the int64 sums,
+// then S64 is cleared for the next call.
+__global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, double gd, const DevScalars* sc,
+                              unsigned long long* __restrict__ S64, double* __restrict__ dW) {
+  const double se = sc->se;
+  const double step_e = se > 0 ? se / lev_e : 0.0;
+  const int64_t n = int64_t(K) * N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / N), j = int(t % N);
+    unsigned long long* p = &S64[int64_t(i) * NA + j];
+    const long long S = (long long)*p;
+    *p = 0ull;
+    dW[t] = ((double(S) * sx) * step_e) / gd;
+  }
+}
+
 }  // namespace tc
 
 bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) {
   using namespace tc;
-  if (!c->d_xc8 || !c->d_e8 || M > 32768 || M == 0) return false;
+  if (!c->d_xc8 || !c->d_e8 || M == 0) return false;
   const int64_t Mp = ((M + 127) / 128) * 128;
   CUtensorMap mA, mE;
   if (!make_map_u8(&mA, c->d_xc8, uint64_t(c->KA), uint64_t(Mp), 128, 128)) return false;
@@ -162,8 +196,27 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
   a.K = c->g.K;
   a.N = c->g.N;
   a.num_ib = c->KA / 128;
-  a.num_units = a.num_ib * (c->NA / 128);
+  a.ntiles = a.num_ib * (c->NA / 128);
   a.kblocks = int(Mp / 128);
+  a.NA = c->NA;
+  // batch chunks: exact s32 partials (<= 256 blocks = 32768 rows) and at
+  // least ~2 units per SM when the K x N tiles alone cannot fill the GPU
+  const int want = std::max((a.kblocks + 255) / 256, (2 * num_sms() + a.ntiles - 1) / a.ntiles);
+  const int nchunks = std::max(1, std::min(a.kblocks, want));
+  a.kb_chunk = (a.kblocks + nchunks - 1) / nchunks;
+  const int nch = (a.kblocks + a.kb_chunk - 1) / a.kb_chunk;
+  a.num_units = a.ntiles * nch;
+  a.S64 = nullptr;
+  if (nch > 1) {
+    const size_t bytes = size_t(c->KA) * c->NA * 8;
+    if (c->S64_bytes < bytes) {
+      cudaFree(c->d_S64);
+      if (cudaMalloc(&c->d_S64, bytes) != cudaSuccess) return false;
+      cudaMemsetAsync(c->d_S64, 0, bytes, st);
+      c->S64_bytes = bytes;
+    }
+    a.S64 = c->d_S64;
+  }
   a.Mcap8 = c->M_cap8;
   a.sx = c->sx;
   a.lev_e = c->lev_e;
@@ -177,6 +230,13 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
   }
   const int grid = std::min(a.num_units, num_sms());
   k_dw_tc<<<grid, dw::kThreads, dw::kSmem, st>>>(mA, mE, a);
+  if (a.S64) {
+    const int64_t n = int64_t(c->g.K) * c->g.N;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+    c->launches += 1;  // the finalize pass (the caller counts k_dw_tc)
+    k_dw_finalize<<<blocks, 256, 0, st>>>(c->g.K, c->g.N, c->NA, c->sx, c->lev_e, grad_divisor, c->d_sc, c->d_S64,
+                                          c->d_dW);
+  }
   return cudaPeekAtLastError() == cudaSuccess;
 }
 

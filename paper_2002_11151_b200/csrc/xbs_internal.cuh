@@ -96,6 +96,7 @@ struct xbs_core {
   xbs::RegenP rp{};
   xbs::AdcP adc{};
   cudaStream_t stream = nullptr;
+  bool own_stream = true;  // false after xbs_core_set_stream(caller's stream)
   int kernel = 0;  // 0 tcgen05, 1 SIMT
   bool fully_ideal = false;
   bool adc_scaled = false;  // k_out includes i_fs/(2^bits-1)
@@ -124,6 +125,8 @@ struct xbs_core {
   uint8_t* d_xc8 = nullptr;
   uint8_t* d_e8 = nullptr;
   int KA = 0, NA = 0;
+  unsigned long long* d_S64 = nullptr;  // split-batch dW: int64 partial sums [KA][NA]
+  size_t S64_bytes = 0;
   int64_t M_cap8 = 0;
   double* d_io_in = nullptr;   // host-API staging (M x max(K,N))
   double* d_io_out = nullptr;

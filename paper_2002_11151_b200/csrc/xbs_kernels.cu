@@ -497,50 +497,60 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 }
 
 // ------------------------------------------------------------------ prep_x
-// quantize_unsigned_codes (tensor.cpp:8-25) + DAC bit planes (layers.cpp:236-241)
-// x: M x K column-major (ld = M).  One thread per (b, 16-column chunk of the
-// device-padded K axis); writes codes and both A planes (bits, 255*bits).
-__global__ void k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF, double step, double levels,
-                         uint16_t* __restrict__ codes, uint8_t* __restrict__ A, uint8_t* __restrict__ c8,
-                         int ld8) {
-  const int chunks = g.KI / 16;
-  const int64_t n = M * chunks;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = t % M;
-    const int ch = int(t / M);
-    uint32_t cv[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int col = ch * 16 + q;
-      const int tr = col / g.R, r = col % g.R;
-      const int i = tr * g.tile_rows + r;
-      uint32_t code = 0;
-      if (r < g.tile_rows && i < g.K) {
-        double v = double(llround(x[int64_t(i) * M + b] / step));
-        if (v < 0) v = 0;
-        if (v > levels) v = levels;
-        code = uint32_t(v);
-        codes[b * g.K + i] = uint16_t(code);
-        if (c8) c8[b * ld8 + i] = uint8_t(code);
-      }
-      cv[q] = code;
+// quantize_unsigned_codes (tensor.cpp:8-25) + DAC bit planes (layers.cpp:236-241).
+// x is M x K column-major (ld = M) and the planes are row-major [b*TPi+k][KI],
+// so the kernel is a tiled transpose: a 64 (batch) x 64 (device column) tile
+// of codes is staged in shared memory from coalesced column reads, then the
+// code rows, the u8 dW code plane and both bit-plane copies (bits, 255*bits)
+// are written as contiguous row segments.
+constexpr int kPrepTB = 64, kPrepTI = 64;
+
+__global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF,
+                                                double step, double levels, uint16_t* __restrict__ codes,
+                                                uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8) {
+  __shared__ uint16_t cs[kPrepTB][kPrepTI + 2];
+  const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
+  const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. KI)
+  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+    const int bl = e % kPrepTB, il = e / kPrepTB;  // consecutive threads: consecutive batch rows
+    const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
+    const int64_t b = b0 + bl;
+    uint32_t code = 0;
+    if (b < M && r < g.tile_rows && i < g.K) {
+      double v = double(llround(x[int64_t(i) * M + b] / step));
+      if (v < 0) v = 0;
+      if (v > levels) v = levels;
+      code = uint32_t(v);
     }
-    for (int k = 0; k < g.TPi; ++k) {
-      uint32_t w0[4], w1[4];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        uint32_t a = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) a |= ((cv[q4 * 4 + q] >> k) & 1u) << (8 * q);
-        w0[q4] = a;
-        w1[q4] = a * 255u;
-      }
-      const int64_t row = b * g.TPi + k;
-      uint4* p0 = reinterpret_cast<uint4*>(A + row * g.KI + ch * 16);
-      uint4* p1 = reinterpret_cast<uint4*>(A + (rowsF + row) * g.KI + ch * 16);
-      *p0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-      *p1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    cs[bl][il] = uint16_t(code);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+    const int il = e % kPrepTI, bl = e / kPrepTI;  // consecutive threads: consecutive columns
+    const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
+    const int64_t b = b0 + bl;
+    if (b < M && r < g.tile_rows && i < g.K) {
+      codes[b * g.K + i] = cs[bl][il];
+      if (c8) c8[b * ld8 + i] = uint8_t(cs[bl][il]);
     }
+  }
+  constexpr int Q = kPrepTI / 16;
+  for (int e = threadIdx.x; e < kPrepTB * g.TPi * Q; e += blockDim.x) {
+    const int q = e % Q, k = (e / Q) % g.TPi, bl = e / (Q * g.TPi);
+    const int64_t b = b0 + bl;
+    if (b >= M) continue;
+    uint32_t w0[4];
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) v |= ((uint32_t(cs[bl][q * 16 + q4 * 4 + qq]) >> k) & 1u) << (8 * qq);
+      w0[q4] = v;
+    }
+    const int64_t row = b * g.TPi + k;
+    uint8_t* p0 = A + row * g.KI + c0 + q * 16;
+    *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    *reinterpret_cast<uint4*>(p0 + rowsF * g.KI) = make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
   }
 }
 
@@ -552,72 +562,80 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
     cudaMemsetAsync(c->d_Af + pad0 * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
     cudaMemsetAsync(c->d_Af + (rowsF + pad0) * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
   }
-  const int64_t n = M * (c->g.KI / 16);
-  if (n == 0) return;
-  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  if (M == 0) return;
+  const dim3 grid(unsigned((M + kPrepTB - 1) / kPrepTB), unsigned(c->g.KI / kPrepTI));
   const double levels = double((1 << c->opt.act_bits) - 1);
   if (c->d_xc8) {  // u8 code plane for the tcgen05 dW: rows [M, Mpad) must read 0
     const int64_t Mp = ((M + 127) / 128) * 128;
     if (Mp > M) cudaMemsetAsync(c->d_xc8 + M * c->KA, 0, size_t(Mp - M) * c->KA, st);
   }
-  k_prep_x<<<blocks, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
-                                    c->d_Af, c->d_xc8, c->KA);
+  k_prep_x<<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+                                  c->d_Af, c->d_xc8, c->KA);
 }
 
 // ----------------------------------------------------------------- prep_dy
 // se = max|dy| (layers.cpp:298), quantize_signed_codes (tensor.cpp:33-51),
 // plus/minus planes (layers.cpp:316-331).  Row (b*TPe + k)*2 + phi, phi=0
-// plus, phi=1 minus.
-__global__ void k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB, double levels,
-                          const DevScalars* __restrict__ sc, int16_t* __restrict__ ecodes, uint8_t* __restrict__ A,
-                          uint8_t* __restrict__ e8, int64_t plane8, int ld8) {
+// plus, phi=1 minus.  Tiled transpose as in k_prep_x.
+__global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB,
+                                                 double levels, const DevScalars* __restrict__ sc,
+                                                 int16_t* __restrict__ ecodes, uint8_t* __restrict__ A,
+                                                 uint8_t* __restrict__ e8, int64_t plane8, int ld8) {
+  __shared__ int16_t cs[kPrepTB][kPrepTI + 2];
   const double se = sc->se;
   const double step = se / levels;
-  const int chunks = g.NI / 16;
-  const int64_t n = M * chunks;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = t % M;
-    const int ch = int(t / M);
-    uint32_t pv[16], mv[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int col = ch * 16 + q;
-      const int tc = col / g.C, c = col % g.C;
-      const int j = tc * g.tile_cols + c;
-      int sm = 0;
-      if (c < g.tile_cols && j < g.N) {
-        if (se > 0) {
-          const double v = dy[int64_t(j) * M + b];
-          double qq = double(llround(fabs(v) / step));
-          if (qq > levels) qq = levels;
-          const int mag = int(qq);
-          sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
-        }
-        ecodes[b * g.N + j] = int16_t(sm);
-        if (e8) {
-          e8[b * ld8 + j] = uint8_t(sm > 0 ? sm : 0);
-          e8[plane8 + b * ld8 + j] = uint8_t(sm < 0 ? -sm : 0);
-        }
-      }
-      pv[q] = sm > 0 ? uint32_t(sm) : 0u;
-      mv[q] = sm < 0 ? uint32_t(-sm) : 0u;
+  const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
+  const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. NI)
+  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+    const int bl = e % kPrepTB, il = e / kPrepTB;
+    const int col = c0 + il, tc = col / g.C, cc = col % g.C, j = tc * g.tile_cols + cc;
+    const int64_t b = b0 + bl;
+    int sm = 0;
+    if (b < M && cc < g.tile_cols && j < g.N && se > 0) {
+      const double v = dy[int64_t(j) * M + b];
+      double qq = double(llround(fabs(v) / step));
+      if (qq > levels) qq = levels;
+      const int mag = int(qq);
+      sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
     }
-    for (int k = 0; k < g.TPe; ++k)
-      for (int phi = 0; phi < 2; ++phi) {
-        const uint32_t* src = phi ? mv : pv;
-        uint32_t w0[4], w1[4];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint32_t a = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) a |= ((src[q4 * 4 + q] >> k) & 1u) << (8 * q);
-          w0[q4] = a;
-          w1[q4] = a * 255u;
-        }
-        const int64_t row = (b * g.TPe + k) * 2 + phi;
-        *reinterpret_cast<uint4*>(A + row * g.NI + ch * 16) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-        *reinterpret_cast<uint4*>(A + (rowsB + row) * g.NI + ch * 16) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    cs[bl][il] = int16_t(sm);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+    const int il = e % kPrepTI, bl = e / kPrepTI;
+    const int col = c0 + il, tc = col / g.C, cc = col % g.C, j = tc * g.tile_cols + cc;
+    const int64_t b = b0 + bl;
+    if (b < M && cc < g.tile_cols && j < g.N) {
+      const int sm = cs[bl][il];
+      ecodes[b * g.N + j] = int16_t(sm);
+      if (e8) {
+        e8[b * ld8 + j] = uint8_t(sm > 0 ? sm : 0);
+        e8[plane8 + b * ld8 + j] = uint8_t(sm < 0 ? -sm : 0);
       }
+    }
+  }
+  constexpr int Q = kPrepTI / 16;
+  for (int e = threadIdx.x; e < kPrepTB * g.TPe * 2 * Q; e += blockDim.x) {
+    const int q = e % Q, kp = (e / Q) % (2 * g.TPe), bl = e / (Q * 2 * g.TPe);
+    const int k = kp >> 1, phi = kp & 1;
+    const int64_t b = b0 + bl;
+    if (b >= M) continue;
+    uint32_t w0[4];
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const int sm = cs[bl][q * 16 + q4 * 4 + qq];
+        const uint32_t mag = phi ? uint32_t(sm < 0 ? -sm : 0) : uint32_t(sm > 0 ? sm : 0);
+        v |= ((mag >> k) & 1u) << (8 * qq);
+      }
+      w0[q4] = v;
+    }
+    const int64_t row = (b * g.TPe + k) * 2 + phi;
+    uint8_t* p0 = A + row * g.NI + c0 + q * 16;
+    *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    *reinterpret_cast<uint4*>(p0 + rowsB * g.NI) = make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
   }
 }
 
@@ -635,9 +653,8 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
     cudaMemsetAsync(c->d_Ab + pad0 * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
     cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
   }
-  const int64_t n = M * (c->g.NI / 16);
-  if (n == 0) return;
-  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  if (M == 0) return;
+  const dim3 grid(unsigned((M + kPrepTB - 1) / kPrepTB), unsigned(c->g.NI / kPrepTI));
   const int64_t plane8 = c->M_cap8 * c->NA;
   if (c->d_e8) {
     const int64_t Mp = ((M + 127) / 128) * 128;
@@ -646,7 +663,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
       cudaMemsetAsync(c->d_e8 + plane8 + M * c->NA, 0, size_t(Mp - M) * c->NA, st);
     }
   }
-  k_prep_dy<<<blocks, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
+  k_prep_dy<<<grid, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
                                      c->d_ecodes, c->d_Ab, c->d_e8, plane8, c->NA);
 }
 

@@ -248,6 +248,7 @@ SYMBOLS = {
     "xbs_core_adc_counters": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "xbs_core_select_kernel": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stream": (_P, [_P]),
+    "xbs_core_set_stream": (ctypes.c_int, [_P, _P]),
     "xbs_core_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(_I64), ctypes.c_int32]),
     "xbs_core_launch_count": (_I64, [_P]),
@@ -419,6 +420,10 @@ class CrossbarCore:
 
     def stream(self) -> int:
         return load_library().xbs_core_stream(self._h) or 0
+
+    def set_stream(self, stream: int) -> None:
+        """Enqueue on a caller-owned cudaStream_t (0: back to a private stream)."""
+        _check(load_library().xbs_core_set_stream(self._h, stream or None))
 
     def profile(self, enable: bool) -> None:
         _check(load_library().xbs_core_profile(self._h, int(bool(enable))))
