@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-peak", action="store_true", help="skip the live int8 peak GEMM (ncu launch lists)")
+    p.add_argument("--layer", type=int, default=0, help="layer index of a multi-layer config (default 0)")
     p.add_argument("--all-layers", action="store_true",
                    help="every layer of the config (C1/C3/C4 networks), one core per layer on one stream")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
@@ -249,7 +250,7 @@ def main():
     init_dist(world, local_rank, "nccl")
     from paper_2002_11151_b200 import xbarsim as xb
 
-    layers = list(cfg.layers) if args.all_layers else [cfg.layers[0]]
+    layers = list(cfg.layers) if args.all_layers else [cfg.layers[args.layer]]
     opt = cfg.options()
     cores, host, dev = [], [], []
     for li, layer in enumerate(layers):

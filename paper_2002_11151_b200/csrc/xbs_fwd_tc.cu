@@ -56,7 +56,9 @@ constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages<KB> * kBStage + 1024
 
 struct FwdArgs {
   int GR, GC, S, db, TPi, tile_cols, C, R, N;
-  int live;  // 64-column units per tile column that hold logical columns
+  int live, live_last;  // 64-column units holding logical columns per tile column / in the last one
+  int n_nb;              // scheduled column units
+  int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = column units fastest
   int64_t M, rowsF;
   int num_mbp, num_units;
   double k_out;
@@ -65,6 +67,18 @@ struct FwdArgs {
   unsigned long long* ctr;
   int dbg;  // perf experiments (XBS_DBG_FWD): 1 skip ADC work, 4 skip TMA
 };
+
+// Column unit index -> (tile column, 64-column unit); units made only of
+// padding are not scheduled.
+__device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int& h) {
+  tc = nb / a.live;
+  if (tc >= a.GC - 1) {
+    tc = a.GC - 1;
+    h = nb - (a.GC - 1) * a.live;
+  } else {
+    h = nb - tc * a.live;
+  }
+}
 
 template <int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
@@ -116,8 +130,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int mbp = u % a.num_mbp, nb = u / a.num_mbp;
-        const int tc = nb / a.live, h = nb % a.live;
+        const int mbp = a.mfast ? u % a.num_mbp : u / a.n_nb, nb = a.mfast ? u / a.num_mbp : u % a.n_nb;
+        int tc, h;
+        col_unit(nb, a, tc, h);
         const int mrow = (2 * mbp + int(rank)) * 128;
         for (int tr = 0; tr < a.GR; ++tr) {
           mbar_wait(&a_empty[as], aph ^ 1);
@@ -205,7 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     for (int u = cid; u < a.num_units; u += ncl) {
-      const int mbp = u % a.num_mbp, nb = u / a.num_mbp;
+      const int mbp = a.mfast ? u % a.num_mbp : u / a.n_nb, nb = a.mfast ? u / a.num_mbp : u % a.n_nb;
       float P[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) P[j] = 0.f;
@@ -233,16 +248,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         adc_conv8<8>(lo, hi, k, w, P, 8, exact);
       }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
+      // (exact in int32: host-checked bound); lane q ends with the totals of
+      // columns q * (16 / TPi) + i
       const int kk = ml % a.TPi;
       const int64_t b = (int64_t(2 * mbp + int(rank)) * 128 + ml) / a.TPi;
-      const int tc = nb / a.live, h = nb % a.live;
+      int tc, h;
+      col_unit(nb, a, tc, h);
+      int v[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        long long v = (long long)__float2ll_rn(P[j]) << kk;
-        for (int o = 1; o < a.TPi; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int cc = h * kCW + 16 * q + j;
+      for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[j]) * (1 << kk);
+      group_reduce16(v, kk, a.TPi);
+      const int per = 16 / a.TPi;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= per) break;
+        const int cc = h * kCW + 16 * q + kk * per + i;
         const int jg = tc * a.tile_cols + cc;
-        if (kk == 0 && b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v) * a.k_out;
+        if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v[i]) * a.k_out;
       }
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
@@ -261,6 +283,8 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   // fp32 P accumulators must stay exact: GR * maxc * sum_s 2^(s db) < 2^24
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   if (double(g.GR) * c->adc.maxc * sw >= 16777216.0) return false;
+  // int32 bit-plane combine: |sum_k 2^k P_k| < 2^31
+  if (double(g.GR) * c->adc.maxc * sw * (std::pow(2.0, g.Ti) - 1) >= 2147483648.0) return false;
   const int64_t rowsF = rows_fwd(M, g.TPi);
   CUtensorMap mA, mB;
   if (!make_map_u8(&mA, c->d_Af, uint64_t(g.KI), uint64_t(2 * rowsF), 128, 128, 128)) return false;
@@ -280,7 +304,17 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.M = M;
   a.rowsF = rowsF;
   a.num_mbp = int(rowsF / 256);
-  a.num_units = a.num_mbp * g.GC * a.live;
+  a.live_last = (g.N - (g.GC - 1) * g.tile_cols + fw::kCW - 1) / fw::kCW;
+  a.n_nb = (g.GC - 1) * a.live + a.live_last;
+  a.num_units = a.num_mbp * a.n_nb;
+  {  // sweep the larger operand once: A (input planes) vs the conductance digits
+    const double bytesA = 2.0 * double(rowsF) * g.KI, bytesB = double(g.digits_bytes()) * a.n_nb / (g.GC * (g.C / fw::kCW));
+    // an operand that fits in L2 (126 MB; use half) is re-read for free
+    const double l2 = 64.0 * 1024 * 1024;
+    const double costM = (bytesA <= l2 ? bytesA : bytesA * a.n_nb) + bytesB;  // M-blocks fastest
+    const double costO = bytesA + (bytesB <= l2 ? bytesB : bytesB * a.num_mbp);        // other index fastest
+    a.mfast = costM <= costO ? 1 : 0;
+  }
   a.k_out = c->k_out_fwd;
   a.adc = make_adc_const(c);
   a.y = d_y;

@@ -351,6 +351,41 @@ __device__ __forceinline__ void adc_chunk16s(uint32_t ta_lo, uint32_t ta_hi, con
   adc_conv8<8>(lo, hi, k, w, P, b + 8, exact_ctr);
 }
 
+// Transpose-reduce of 16 int32 values over groups of G consecutive lanes
+// (the bit-plane / phase lanes of one batch row): at each butterfly step a
+// lane sends half of its values to its partner and keeps the other half, so
+// after log2(G) steps lane q (= lane % G) holds the totals of rows
+// q * (16 / G) + i (G <= 16; for G = 32, lanes q and q ^ 1 share row q >> 1).
+// 15 shuffles for 16 rows instead of 16 x log2(G) for a full butterfly.
+template <int O, int N>
+__device__ __forceinline__ void tr_step(int (&v)[16], int q) {
+  if constexpr (O >= 1) {
+    if constexpr (N > 1) {
+      const bool up = (q & O) != 0;
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const int a = v[i], b = v[i + N / 2];
+        const int keep = up ? b : a;
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, up ? a : b, O);
+      }
+      tr_step<O / 2, N / 2>(v, q);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+      tr_step<O / 2, 1>(v, q);
+    }
+  }
+}
+__device__ __forceinline__ void group_reduce16(int (&v)[16], int q, int G) {
+  switch (G) {
+    case 2: tr_step<1, 16>(v, q); break;
+    case 4: tr_step<2, 16>(v, q); break;
+    case 8: tr_step<4, 16>(v, q); break;
+    case 16: tr_step<8, 16>(v, q); break;
+    case 32: tr_step<16, 16>(v, q); break;
+    default: break;  // G == 1
+  }
+}
+
 // host helpers (xbs_vmm_tc.cu)
 bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
                  int swizzle_bytes = 128);

@@ -115,6 +115,9 @@ constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages<KB> * kBStage + 1024
 
 struct BwdArgs {
   int GR, GC, S, db, TPe, tile_rows, R, C, K;
+  int live, live_last;  // 64-row blocks holding logical rows per row tile / in the last row tile
+  int n_rb;              // scheduled row blocks
+  int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = row blocks fastest
   int64_t M, rowsB;
   int num_mbp, num_units;
   double F, vu, ifs_fac, lev_e;
@@ -124,6 +127,18 @@ struct BwdArgs {
   double* dx;
   unsigned long long* ctr;
 };
+
+// Row block index -> (row tile, 64-row half); blocks made only of padding
+// (beyond K in the last row tile) are not scheduled.
+__device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int& rh) {
+  tr = rb / a.live;
+  if (tr >= a.GR - 1) {
+    tr = a.GR - 1;
+    rh = rb - (a.GR - 1) * a.live;
+  } else {
+    rh = rb - tr * a.live;
+  }
+}
 
 template <int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -170,14 +185,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int rhalves = a.R / 64;
 
   if (warp == 0) {
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int mbp = u % a.num_mbp, rb = u / a.num_mbp;
-        const int tr = rb / rhalves, rh = rb % rhalves;
+        const int mbp = a.mfast ? u % a.num_mbp : u / a.n_rb, rb = a.mfast ? u / a.num_mbp : u % a.n_rb;
+        int tr, rh;
+        row_block(rb, a, tr, rh);
         const int mrow = (2 * mbp + int(rank)) * 128;
         for (int tc = 0; tc < a.GC; ++tc) {
           mbar_wait(&a_empty[as], aph ^ 1);
@@ -276,8 +291,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (a.adc_scaled) k_out *= a.ifs_fac;
     const int nchain = a.GC * a.S;
     for (int u = cid; u < a.num_units; u += ncl) {
-      const int mbp = u % a.num_mbp, rb = u / a.num_mbp;
-      const int tr = rb / rhalves, rh = rb % rhalves;
+      const int mbp = a.mfast ? u % a.num_mbp : u / a.n_rb, rb = a.mfast ? u / a.num_mbp : u % a.n_rb;
+      int tr, rh;
+      row_block(rb, a, tr, rh);
       float P[kRows];
 #pragma unroll
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
@@ -307,17 +323,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         adc_conv8<0>(lo, hi, k, wneg, P, 0, exact);
         adc_conv8<8>(lo, hi, k, wneg, P, 8, exact);
       }
-      // combine the 2*TPe (plane, phase) lanes of each batch row
+      // combine the 2*TPe (plane, phase) lanes of each batch row (exact in
+      // int32: host-checked bound); lane q ends with the totals of rows
+      // q * (16 / grp) + i (grp = 32: lanes q, q ^ 1 share row q >> 1)
       const int grp = 2 * a.TPe;
-      const int kk = (ml % grp) >> 1;
+      const int q = ml % grp, kk = q >> 1;
       const int64_t b = int64_t(2 * mbp + int(rank)) * (128 / grp) + ml / grp;
+      int v[16];
 #pragma unroll
-      for (int j = 0; j < kRows; ++j) {
-        long long v = (long long)__float2ll_rn(P[j]) << kk;
-        for (int o = 1; o < grp; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int rloc = rh * 64 + kRows * ch + j;
+      for (int j = 0; j < kRows; ++j) v[j] = __float2int_rn(P[j]) * (1 << kk);
+      group_reduce16(v, q, grp);
+      const int per = grp <= 16 ? 16 / grp : 1;
+      const int j0 = grp <= 16 ? q * per : (q >> 1);
+      const bool writer = grp <= 16 || (q & 1) == 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= per) break;
+        const int rloc = rh * 64 + kRows * ch + j0 + i;
         const int ig = tr * a.tile_rows + rloc;
-        if ((ml % grp) == 0 && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v) * k_out;
+        if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v[i]) * k_out;
       }
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
@@ -335,6 +359,8 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc.passthrough) return false;
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   if (double(g.GC) * c->adc.maxc * sw * 2.0 >= 16777216.0) return false;
+  // int32 (plane, phase) combine: |sum| < 2^31
+  if (double(g.GC) * c->adc.maxc * sw * 2.0 * (std::pow(2.0, g.Te) - 1) >= 2147483648.0) return false;
   const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
   if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
@@ -353,7 +379,18 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   a.M = M;
   a.rowsB = rowsB;
   a.num_mbp = int(rowsB / 256);
-  a.num_units = a.num_mbp * (g.KI / 64);
+  a.live = (g.tile_rows + 63) / 64;
+  a.live_last = (g.K - (g.GR - 1) * g.tile_rows + 63) / 64;
+  a.n_rb = (g.GR - 1) * a.live + a.live_last;
+  a.num_units = a.num_mbp * a.n_rb;
+  {  // sweep the larger operand once: A' (error planes) vs the conductance digits
+    const double bytesA = 2.0 * double(rowsB) * g.NI, bytesB = double(g.digits_bytes()) / g.GR * (double(a.n_rb) / a.live);
+    // an operand that fits in L2 (126 MB; use half) is re-read for free
+    const double l2 = 64.0 * 1024 * 1024;
+    const double costM = (bytesA <= l2 ? bytesA : bytesA * a.n_rb) + bytesB;  // M-blocks fastest
+    const double costO = bytesA + (bytesB <= l2 ? bytesB : bytesB * a.num_mbp);        // other index fastest
+    a.mfast = costM <= costO ? 1 : 0;
+  }
   a.F = c->F;
   a.vu = c->vu;
   a.ifs_fac = c->ifs_fac;
