@@ -448,6 +448,8 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     rp.aam = (o.engine == XBS_ENGINE_AAM && !zero_par) ? 1 : 0;
     rp.snap_e = snap_exponent(o.g_max);
     rp.snap_scale = std::ldexp(1.0, rp.snap_e);
+    rp.kpnp = uint64_t(g.Kp) * g.Np;
+    rp.varm = nullptr;
 
     // scale constants, same expressions as layers.cpp:272-281 / 369-377
     const double vu = o.dac_v_fs / (std::pow(2.0, o.dac_bits) - 1.0);
@@ -530,6 +532,11 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
       ck(cudaMalloc(&c->d_qmin, size_t(o.tile_rows) * o.tile_cols * sizeof(uint32_t)), "cudaMalloc qmin");
       xbs::launch_qmin(c.get(), c->stream);
     }
+    if (o.variation_sigma != 0.0 && !c->fully_ideal) {
+      ck(cudaMalloc(&c->d_varm, size_t(g.S) * 2 * size_t(g.Kp) * g.Np * sizeof(double)), "cudaMalloc variation");
+      c->rp.varm = c->d_varm;
+      xbs::launch_varm(c.get(), c->stream);
+    }
     const auto t0 = std::chrono::steady_clock::now();
     if (!c->fully_ideal) xbs::launch_regen_all(c.get(), c->stream);
     regenerate_bookkeeping(c.get());
@@ -546,6 +553,7 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_digits);
   cudaFree(c->d_adc_tab);
   cudaFree(c->d_qmin);
+  cudaFree(c->d_varm);
   cudaFree(c->d_master);
   cudaFree(c->d_dW);
   cudaFree(c->d_wimp);

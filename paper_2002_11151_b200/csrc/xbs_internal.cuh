@@ -57,6 +57,11 @@ struct RegenP {
   int aam;     // 1: AAM conversion, 0: identity (ideal / zero-parasitic fcm)
   int snap_e;  // grid exponent e
   double snap_scale;  // 2^e
+  // sigma != 0: the variation multipliers m(s, p, device) are fixed for the
+  // life of the core (mapping.cpp:28-35 keys them by seed and position only),
+  // so they are computed once at create and read back: [s][p][Kp][Np] fp64
+  const double* varm;
+  uint64_t kpnp;  // Kp * Np
 };
 
 // update.cpp:43-88 + implied weights (mapping.cpp:70-81)
@@ -107,6 +112,7 @@ struct xbs_core {
   // device buffers
   uint8_t* d_digits = nullptr;
   uint32_t* d_qmin = nullptr;  // sigma == 0: snapped q of g_min per tile position
+  double* d_varm = nullptr;    // sigma != 0: variation multipliers [s][p][Kp][Np]
   unsigned long long* d_adc_tab = nullptr;  // T[k] = min column current n (units 2^-e) with code >= k
   double* d_master = nullptr;
   double* d_dW = nullptr;
@@ -164,6 +170,7 @@ void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* 
 void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st);
 void launch_qmin(const xbs_core* c, cudaStream_t st);
+void launch_varm(const xbs_core* c, cudaStream_t st);
 void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);
 void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double* d_out, cudaStream_t st);
 // tcgen05 kernels (xbs_vmm_tc.cu); return false if the shape is not covered

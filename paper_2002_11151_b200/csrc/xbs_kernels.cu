@@ -60,16 +60,29 @@ __device__ __forceinline__ double aam_rpath(const RegenP& rp, const Geo& g, int 
 __device__ __forceinline__ uint32_t convert_q(const RegenP& rp, double u, int s, int p, uint64_t idx,
                                               double rpath) {
   double gv = (p == 0 ? fmax(u, 0.0) : fmax(-u, 0.0)) + rp.g_min;
-  if (rp.sigma != 0.0) {
-    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, idx, 0));
-    m = m > 1e-12 ? m : 1e-12;
-    gv = fmin(gv * m, rp.g_max);
-  }
+  if (rp.sigma != 0.0) gv = fmin(gv * rp.varm[(uint64_t(s) * 2 + p) * rp.kpnp + idx], rp.g_max);
   if (rp.aam) {
     if (gv == 0.0) gv = 0.0;
     else if (rpath != 0.0) gv = __drcp_rn(__dadd_rn(__drcp_rn(gv), rpath));
   }
   return __double2uint_rn(__dmul_rn(gv, rp.snap_scale));  // nearbyint(ldexp(gv, e))
+}
+
+// mapping.cpp:28-35: m = max(1 + sigma * N(0, 1), 1e-12), keyed by
+// (seed, 2 s + p, padded device index), computed once per core.
+__global__ void k_varm(Geo g, RegenP rp, double* __restrict__ varm) {
+  const uint64_t n = uint64_t(g.S) * 2 * rp.kpnp;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t sp = t / rp.kpnp, idx = t - sp * rp.kpnp;
+    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, sp, idx, 0));
+    varm[t] = m > 1e-12 ? m : 1e-12;
+  }
+}
+
+void launch_varm(const xbs_core* c, cudaStream_t st) {
+  const uint64_t n = uint64_t(c->g.S) * 2 * c->rp.kpnp;
+  const int blocks = int(std::min<uint64_t>((n + 255) / 256, 148 * 32));
+  k_varm<<<blocks, 256, 0, st>>>(c->g, c->rp, c->d_varm);
 }
 
 // Compile-time specialised conversion for the update kernel.  VAR: sigma
@@ -82,11 +95,7 @@ __device__ __forceinline__ uint32_t convert_qt(const RegenP& rp, double u, int s
                                                double rpath) {
   const double up = p == 0 ? u : -u;
   double gv = (up > 0.0 ? up : 0.0) + rp.g_min;
-  if constexpr (VAR) {
-    double m = 1.0 + rp.sigma * rng_gaussian(rng_key(rp.vseed, uint64_t(s) * 2 + p, idx, 0));
-    m = m > 1e-12 ? m : 1e-12;
-    gv = fmin(gv * m, rp.g_max);
-  }
+  if constexpr (VAR) gv = fmin(gv * __ldg(&rp.varm[(uint64_t(s) * 2 + p) * rp.kpnp + idx]), rp.g_max);
   if constexpr (AAM) gv = __drcp_rn(__dadd_rn(__drcp_rn(gv), rpath));
   return __double2uint_rn(__dmul_rn(gv, rp.snap_scale));
 }
@@ -253,7 +262,8 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
     for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
       const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
       const double rcol = double(g.tile_rows - r) * rp.r_col;
-      double dg[JPT], u[S][JPT], acc[JPT];
+      constexpr int PRE = S < 4 ? S : 4;  // slices loaded per group (register budget)
+      double dg[JPT], u[PRE][JPT], acc[JPT];
       {
         double dw[JPT];
         ld_vec<JPT>(dW + size_t(i) * g.N + j0, dw);
@@ -265,8 +275,6 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
         }
       }
       double* mrow = master + size_t(i) * g.Np + j0;
-#pragma unroll
-      for (int s = 0; s < S; ++s) ld_vec<JPT>(mrow + s * sstride, u[s]);
       uint32_t qi[JPT];
       if constexpr (!VAR) {
         const typename VecT<JPT>::Q t =
@@ -281,10 +289,15 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
       uint8_t* dbase = digits + (size_t(tr) * g.GC + tc) * 4 * plane + size_t(r) * g.C + c0;
 #pragma unroll
       for (int s = S - 1; s >= 0; --s) {  // Horner order: most significant slice first
+        const int qs = (S - 1 - s) % PRE;  // position within the current group
+        if (qs == 0) {                     // all slices of the next group in flight at once
+#pragma unroll
+          for (int q = 0; q < PRE; ++q) ld_vec<JPT>(mrow + (s - q) * sstride, u[q]);
+        }
         uint32_t q[2][JPT];
 #pragma unroll
         for (int jj = 0; jj < JPT; ++jj) {
-          const double ui = u[s][jj];
+          const double ui = u[qs][jj];
           double du = dg[jj];
           if constexpr (NL) {
             if (dg[jj] != 0.0) {
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
           double nu = ui - up.lr * (du + noise);
           nu = nu > range ? range : nu;
           nu = nu < -range ? -range : nu;
-          u[s][jj] = nu;
+          u[qs][jj] = nu;
           acc[jj] = acc[jj] * double(1u << g.db) + nu;
           const double rpath = AAM ? (rrow[jj] + rcol) + rp.r_sense : 0.0;
           const uint64_t idx = uint64_t(i) * g.Np + j0 + jj;
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
             q[1][jj] = pa == 0 ? qi[jj] : qa;
           }
         }
-        st_vec<JPT>(mrow + s * sstride, u[s]);
+        st_vec<JPT>(mrow + s * sstride, u[qs]);
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           typename VecT<JPT>::B w[4] = {0, 0, 0, 0};
