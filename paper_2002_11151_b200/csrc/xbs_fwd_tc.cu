@@ -65,7 +65,6 @@ struct FwdArgs {
   AdcConst adc;
   double* y;
   unsigned long long* ctr;
-  int dbg;  // perf experiments (XBS_DBG_FWD): 1 skip ADC work, 4 skip TMA
 };
 
 // Column unit index -> (tile column, 64-column unit); units made only of
@@ -229,13 +228,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         const float w = (sp & 1) == 0 ? float(1 << ((sp >> 1) * a.db)) : -float(1 << ((sp >> 1) * a.db));
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
-        if (a.dbg & 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster_relaxed(te[ab]);
-          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-          continue;
-        }
         uint32_t lo[16], hi[16];
         tmem_ld16(tl + ab * 128, lo);
         tmem_ld16(tl + ab * 128 + kCW, hi);
@@ -319,7 +311,6 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.adc = make_adc_const(c);
   a.y = d_y;
   a.ctr = &c->d_sc->exact_path;
-  a.dbg = getenv("XBS_DBG_FWD") ? atoi(getenv("XBS_DBG_FWD")) : 0;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);

@@ -67,30 +67,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
-// Wait for the single-thread roles (TMA producer, MMA issuer): the thread is
-// suspended in hardware for up to ~0.5 us per try instead of spinning, so
-// its warp does not steal issue slots from the epilogue warps.
-#ifndef XBS_ROLE_WAIT_NS
-#define XBS_ROLE_WAIT_NS 0
-#endif
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  if constexpr (XBS_ROLE_WAIT_NS == 0) {
-    mbar_wait(bar, parity);
-  } else {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    do {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity), "r"(XBS_ROLE_WAIT_NS)
-          : "memory");
-    } while (!done);
-  }
-}
-
 // One lane of a converged warp (the others skip the guarded issue).
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -226,24 +202,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-// 16 lanes x 256 bits: thread t of the warp gets lane base + t/4... (shape 16x256b)
-__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -316,39 +274,6 @@ __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32
       }
     }
   }
-}
-
-__device__ __forceinline__ void tmem_release(uint64_t* release) {
-  tc_fence_before();
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(release);
-}
-
-// One 8-column chunk of a chain: TMEM -> registers, ADC, P[b+j] += w*code.
-// `release` (if set) is arrived once this warp's TMEM reads are complete.
-template <int kN>
-__device__ __forceinline__ void adc_chunk8s(uint32_t ta_lo, uint32_t ta_hi, const AdcConst& k, float w,
-                                            float (&P)[kN], int b, uint32_t& exact_ctr, uint64_t* release) {
-  uint32_t lo[8], hi[8];
-  tmem_ld8(ta_lo, lo);
-  tmem_ld8(ta_hi, hi);
-  tmem_wait_ld();
-  if (release) tmem_release(release);
-  adc_conv8<0>(lo, hi, k, w, P, b, exact_ctr);
-}
-
-// 16 columns with one TMEM round trip; the buffer is released before the
-// math so the MMA issuer can refill it while the ADC runs.
-template <int kN>
-__device__ __forceinline__ void adc_chunk16s(uint32_t ta_lo, uint32_t ta_hi, const AdcConst& k, float w,
-                                             float (&P)[kN], int b, uint32_t& exact_ctr, uint64_t* release) {
-  uint32_t lo[16], hi[16];
-  tmem_ld16(ta_lo, lo);
-  tmem_ld16(ta_hi, hi);
-  tmem_wait_ld();
-  if (release) tmem_release(release);
-  adc_conv8<0>(lo, hi, k, w, P, b, exact_ctr);
-  adc_conv8<8>(lo, hi, k, w, P, b + 8, exact_ctr);
 }
 
 // Transpose-reduce of 16 int32 values over groups of G consecutive lanes
