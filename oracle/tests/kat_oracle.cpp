@@ -1037,4 +1037,345 @@ TEST_CASE("snap grid: exponent, bound and exactness of currents") {
   CHECK(acc == std::ldexp(std::nearbyint(std::ldexp(1e-5, e)) * 256.0, -e));
 }
 
+// ---------------------------------------------------------------------------
+// Circuit engines: restated from the reference's tests/unit/test_circuit.cpp
+// (nodal oracle 64-141, fcm 143-237, aam/fcm 250-328, distortion 330-380).
+namespace circ {
+
+CrossbarConfig paper_cfg(int rows, int cols) {
+  CrossbarConfig c;
+  c.rows = rows;
+  c.cols = cols;
+  c.r_row = 1.0;
+  c.r_col = 4.6;
+  c.r_source = 0.0;
+  c.r_sense = 0.0;
+  c.g_min = 1e-6;
+  c.g_max = 1e-5;
+  c.v_fs = 1.0;
+  return c;
+}
+CrossbarConfig no_parasitics(int rows, int cols) {
+  CrossbarConfig c = paper_cfg(rows, cols);
+  c.r_row = c.r_col = c.r_source = c.r_sense = 0.0;
+  return c;
+}
+Matrix random_tile(const CrossbarConfig& c, std::mt19937_64& rng) {
+  std::uniform_real_distribution<double> d(c.g_min, c.g_max);
+  Matrix g(c.rows, c.cols);
+  for (long j = 0; j < c.cols; ++j)
+    for (long i = 0; i < c.rows; ++i) g(i, j) = d(rng);
+  return g;
+}
+std::vector<double> random_input(const CrossbarConfig& c, std::mt19937_64& rng) {
+  std::uniform_real_distribution<double> d(0.0, c.v_fs);
+  std::vector<double> v(size_t(c.rows));
+  for (double& x : v) x = d(rng);
+  return v;
+}
+// max |net node current| over every top and bottom node, in units of g_max * v_fs
+double max_kcl_residual(const CrossbarConfig& c, const Matrix& g, const std::vector<double>& v,
+                        const Matrix& vt, const Matrix& vb) {
+  double worst = 0.0;
+  const long R = c.rows, C = c.cols;
+  for (long i = 0; i < R; ++i)
+    for (long j = 0; j < C; ++j) {
+      double net = g(i, j) * (vt(i, j) - vb(i, j));  // leaving the top node through the device
+      if (c.r_row > 0.0) {
+        if (j == 0) net -= (v[size_t(i)] - vt(i, j)) / (c.r_source + c.r_row);
+        else net -= (vt(i, j - 1) - vt(i, j)) / c.r_row;
+        if (j + 1 < C) net -= (vt(i, j + 1) - vt(i, j)) / c.r_row;
+        worst = std::max(worst, std::fabs(net));
+      }
+      double netb = -g(i, j) * (vt(i, j) - vb(i, j));  // entering the bottom node
+      if (c.r_col > 0.0) {
+        if (i > 0) netb -= (vb(i - 1, j) - vb(i, j)) / c.r_col;
+        if (i + 1 < R) netb -= (vb(i + 1, j) - vb(i, j)) / c.r_col;
+        else netb -= (0.0 - vb(i, j)) / (c.r_col + c.r_sense);
+        worst = std::max(worst, std::fabs(netb));
+      }
+    }
+  return worst / (c.g_max * c.v_fs);
+}
+constexpr double kGolden2x2Col0 = 1.99973003770266967e-05;  // test_circuit.cpp:55-56
+constexpr double kGolden2x2Col1 = 1.99971004290162132e-05;
+std::vector<double> currents_at(const Matrix& g, double v) {
+  std::vector<double> out(size_t(g.cols), 0.0);
+  for (long j = 0; j < g.cols; ++j)
+    for (long i = 0; i < g.rows; ++i) out[size_t(j)] += g(i, j) * v;
+  return out;
+}
+double max_rel(const Matrix& a, const Matrix& ref) {
+  double m = 0.0;
+  for (size_t k = 0; k < a.v.size(); ++k) m = std::max(m, std::fabs(a.v[k] - ref.v[k]) / ref.v[k]);
+  return m;
+}
+
+}  // namespace circ
+
+TEST_CASE("nodal: 1x1 zero-parasitic tile is Ohm's law") {
+  auto c = circ::no_parasitics(1, 1);
+  auto sol = solve_nodal_oracle(c, Matrix(1, 1, 1e-5), {1.0});
+  CHECK(sol.i_col[0] == Approx(1e-5).epsilon(1e-12));
+  CHECK(sol.v_top(0, 0) == 1.0);
+  CHECK(sol.v_bot(0, 0) == 0.0);
+}
+
+TEST_CASE("nodal: zero excitation gives identically zero solution") {
+  std::mt19937_64 rng(7);
+  auto c = circ::paper_cfg(5, 4);
+  auto sol = solve_nodal_oracle(c, circ::random_tile(c, rng), std::vector<double>(5, 0.0));
+  for (double x : sol.i_col) CHECK(std::fabs(x) <= 1e-18);
+  for (double x : sol.v_top.v) CHECK(std::fabs(x) <= 1e-15);
+  for (double x : sol.v_bot.v) CHECK(std::fabs(x) <= 1e-15);
+}
+
+TEST_CASE("nodal: 2x2 golden vector") {
+  auto c = circ::paper_cfg(2, 2);
+  auto sol = solve_nodal_oracle(c, Matrix(2, 2, 1e-5), {1.0, 1.0});
+  CHECK(sol.i_col[0] == Approx(circ::kGolden2x2Col0).epsilon(1e-10));
+  CHECK(sol.i_col[1] == Approx(circ::kGolden2x2Col1).epsilon(1e-10));
+}
+
+TEST_CASE("nodal: all-parasitics-zero solution is exact") {
+  std::mt19937_64 rng(3);
+  auto c = circ::no_parasitics(6, 3);
+  auto g = circ::random_tile(c, rng);
+  auto v = circ::random_input(c, rng);
+  auto sol = solve_nodal_oracle(c, g, v);
+  for (long i = 0; i < 6; ++i)
+    for (long j = 0; j < 3; ++j) {
+      CHECK(sol.v_top(i, j) == v[size_t(i)]);
+      CHECK(sol.v_bot(i, j) == 0.0);
+    }
+}
+
+TEST_CASE("nodal: KCL residual below 1e-9 on random tiles up to 16x16") {
+  std::mt19937_64 rng(11);
+  for (int trial = 0; trial < 30; ++trial) {
+    const int rows = 1 + int(rng() % 16), cols = 1 + int(rng() % 16);
+    auto c = circ::paper_cfg(rows, cols);
+    auto g = circ::random_tile(c, rng);
+    auto v = circ::random_input(c, rng);
+    auto sol = solve_nodal_oracle(c, g, v);
+    CHECK(circ::max_kcl_residual(c, g, v, sol.v_top, sol.v_bot) < 1e-9);
+  }
+}
+
+TEST_CASE("nodal: iterative path (above the dense limit) satisfies KCL") {
+  std::mt19937_64 rng(13);
+  auto c = circ::paper_cfg(40, 40);
+  auto g = circ::random_tile(c, rng);
+  auto v = circ::random_input(c, rng);
+  auto sol = solve_nodal_oracle(c, g, v);
+  CHECK(circ::max_kcl_residual(c, g, v, sol.v_top, sol.v_bot) < 1e-8);
+}
+
+TEST_CASE("nodal: argument and degeneracy errors") {
+  auto c = circ::paper_cfg(2, 2);
+  Matrix g(2, 2, 1e-5);
+  CHECK_THROWS_AS(solve_nodal_oracle(c, g, {1.0, 1.0, 1.0}), std::invalid_argument);
+  CHECK_THROWS_AS(solve_nodal_oracle(c, g, {2.0, 2.0}), std::invalid_argument);
+  CHECK_THROWS_AS(solve_nodal_oracle(circ::no_parasitics(2, 2), Matrix(2, 2, 0.0), {1.0, 1.0}),
+                  DegenerateCircuitError);
+}
+
+TEST_CASE("fcm: zero parasitics is the identity, exactly") {
+  std::mt19937_64 rng(17);
+  for (int t = 0; t < 5; ++t) {
+    auto c = circ::no_parasitics(4, 6);
+    auto g = circ::random_tile(c, rng);
+    CHECK(fcm_convert(c, g).v == g.v);
+  }
+}
+
+TEST_CASE("fcm: reproduces the golden oracle currents within 0.1%") {
+  auto c = circ::paper_cfg(2, 2);
+  auto i = circ::currents_at(fcm_convert(c, Matrix(2, 2, 1e-5)), 1.0);
+  CHECK(std::fabs(i[0] - circ::kGolden2x2Col0) / circ::kGolden2x2Col0 < 1e-3);
+  CHECK(std::fabs(i[1] - circ::kGolden2x2Col1) / circ::kGolden2x2Col1 < 1e-3);
+}
+
+TEST_CASE("fcm: matches nodal-oracle currents at the calibration input on random tiles") {
+  std::mt19937_64 rng(19);
+  for (int size : {8, 16, 64}) {
+    auto c = circ::paper_cfg(size, size);
+    for (int t = 0; t < 3; ++t) {
+      auto g = circ::random_tile(c, rng);
+      auto i_fcm = circ::currents_at(fcm_convert(c, g), c.v_fs);
+      auto i_or = solve_nodal_oracle(c, g, std::vector<double>(size_t(size), c.v_fs)).i_col;
+      double err = 0.0;
+      for (int j = 0; j < size; ++j) err = std::max(err, std::fabs(i_fcm[size_t(j)] - i_or[size_t(j)]) / std::fabs(i_or[size_t(j)]));
+      CHECK(err < 1e-3);
+    }
+  }
+}
+
+TEST_CASE("fcm: distortion grows with column index for a uniform tile") {
+  auto c = circ::paper_cfg(64, 64);
+  auto gn = fcm_convert(c, Matrix(64, 64, c.g_min));
+  for (long i = 0; i < 64; ++i)
+    for (long j = 0; j + 1 < 64; ++j) {
+      const double dj = 1.0 - gn(i, j) / c.g_min, dj1 = 1.0 - gn(i, j + 1) / c.g_min;
+      CHECK(dj > 0.0);
+      CHECK(dj1 > dj);
+    }
+}
+
+TEST_CASE("fcm: zero-calibration rows take the fallback full-scale distortion") {
+  auto c = circ::paper_cfg(4, 4);
+  std::mt19937_64 rng(23);
+  auto g = circ::random_tile(c, rng);
+  FcmOptions o;
+  o.v_cal.assign(4, c.v_fs);
+  o.v_cal[2] = 0.0;
+  auto gn = fcm_convert(c, g, o);
+  auto full = fcm_convert(c, g);
+  for (long j = 0; j < 4; ++j) CHECK(gn(2, j) == Approx(full(2, j)).epsilon(1e-9));
+  CHECK(gn(0, 0) > 0.0);
+}
+
+TEST_CASE("fcm: errors on bad arguments and non-convergence") {
+  auto c = circ::paper_cfg(2, 2);
+  Matrix g(2, 2, 1e-5);
+  FcmOptions bad_tol;
+  bad_tol.tol = 0.0;
+  CHECK_THROWS_AS(fcm_convert(c, g, bad_tol), std::invalid_argument);
+  FcmOptions wrong_len;
+  wrong_len.v_cal.assign(3, 1.0);
+  CHECK_THROWS_AS(fcm_convert(c, g, wrong_len), std::invalid_argument);
+  auto heavy = circ::paper_cfg(16, 16);
+  heavy.g_min = 1e-3;
+  heavy.g_max = 1e-2;
+  heavy.r_row = 50.0;
+  heavy.r_col = 50.0;
+  std::mt19937_64 rng(29);
+  auto coupled = circ::random_tile(heavy, rng);
+  FcmOptions starved;
+  starved.tol = 1e-12;
+  starved.max_iter = 1;
+  bool thrown = false;
+  try {
+    fcm_convert(heavy, coupled, starved);
+  } catch (const ConvergenceError& e) {
+    thrown = true;
+    CHECK(e.residual > 0.0);
+    CHECK(e.iterations == 1);
+  }
+  CHECK(thrown);
+}
+
+TEST_CASE("aam: agrees with fcm for high-resistance uniform tiles, diverges at low range") {
+  auto c = circ::paper_cfg(64, 64);
+  Matrix g(64, 64, c.g_min);
+  CHECK(circ::max_rel(aam_convert(c, g), fcm_convert(c, g)) <= 0.02);
+  auto low = c;
+  low.g_min = 1e-4;
+  low.g_max = 1e-3;
+  Matrix gl(64, 64, low.g_min);
+  CHECK(circ::max_rel(aam_convert(low, gl), fcm_convert(low, gl)) > 0.10);
+}
+
+TEST_CASE("engines: parasitic monotonicity and shrinkage") {
+  std::mt19937_64 rng(41);
+  std::uniform_real_distribution<double> rd(0.0, 8.0);
+  for (int trial = 0; trial < 10; ++trial) {
+    auto c = circ::paper_cfg(8, 8);
+    c.r_row = rd(rng);
+    c.r_col = rd(rng);
+    c.r_source = rd(rng);
+    c.r_sense = rd(rng);
+    auto g = circ::random_tile(c, rng);
+    for (bool use_aam : {false, true}) {
+      auto conv = [&](const CrossbarConfig& cc) { return use_aam ? aam_convert(cc, g) : fcm_convert(cc, g); };
+      auto base = conv(c);
+      for (size_t k = 0; k < g.v.size(); ++k) {
+        CHECK(base.v[k] <= g.v[k] + 1e-18);
+        CHECK(base.v[k] > 0.0);
+      }
+      for (int which = 0; which < 4; ++which) {
+        auto b = c;
+        const double delta = 1.0 + rd(rng);
+        if (which == 0) b.r_row += delta;
+        if (which == 1) b.r_col += delta;
+        if (which == 2) b.r_source += delta;
+        if (which == 3) b.r_sense += delta;
+        auto worse = conv(b);
+        for (size_t k = 0; k < g.v.size(); ++k) CHECK(worse.v[k] <= base.v[k] + 1e-15);
+      }
+    }
+  }
+}
+
+TEST_CASE("engines: aam/fcm disagreement shrinks as devices get more resistive") {
+  std::mt19937_64 rng(43);
+  auto c = circ::paper_cfg(16, 16);
+  c.g_min = 1e-3;
+  c.g_max = 1e-2;
+  auto g = circ::random_tile(c, rng);
+  double prev = 1e9;
+  for (int decade = 0; decade < 6; ++decade) {
+    const double scale = std::pow(10.0, -decade);
+    auto cc = c;
+    cc.g_min *= scale;
+    cc.g_max *= scale;
+    Matrix t = g;
+    for (double& x : t.v) x *= scale;
+    const double err = circ::max_rel(aam_convert(cc, t), fcm_convert(cc, t));
+    CHECK(err < prev);
+    prev = err;
+  }
+}
+
+TEST_CASE("distortion: refresh then apply round-trips exactly") {
+  std::mt19937_64 rng(47);
+  auto c = circ::paper_cfg(8, 8);
+  auto g = circ::random_tile(c, rng);
+  DistortionCache cache;
+  cache.refresh_interval = 3;
+  refresh_distortion(cache, c, g, int(EngineKind::fcm), FcmOptions{});
+  CHECK(cache.age == 0);
+  for (double d : cache.d.v) CHECK(d >= 0.0 && d < 1.0);
+  CHECK(apply_distortion(cache, g).v == fcm_convert(c, g).v);
+  CHECK(cache.age == 1);
+}
+
+TEST_CASE("distortion: zero-parasitic tile has an all-zero profile") {
+  std::mt19937_64 rng(53);
+  auto c = circ::no_parasitics(4, 4);
+  auto g = circ::random_tile(c, rng);
+  DistortionCache cache;
+  refresh_distortion(cache, c, g, int(EngineKind::aam), FcmOptions{});
+  for (double d : cache.d.v) CHECK(d == 0.0);
+  CHECK(apply_distortion(cache, g).v == g.v);
+}
+
+TEST_CASE("distortion: staleness error once age reaches the interval") {
+  std::mt19937_64 rng(59);
+  auto c = circ::paper_cfg(4, 4);
+  auto g = circ::random_tile(c, rng);
+  DistortionCache cache;
+  cache.refresh_interval = 2;
+  refresh_distortion(cache, c, g, int(EngineKind::fcm), FcmOptions{});
+  (void)apply_distortion(cache, g);
+  (void)apply_distortion(cache, g);
+  CHECK_THROWS_AS(apply_distortion(cache, g), StaleCacheError);
+  refresh_distortion(cache, c, g, int(EngineKind::fcm), FcmOptions{});
+  CHECK(cache.age == 0);
+  (void)apply_distortion(cache, g);
+}
+
+TEST_CASE("distortion: applying a stored profile to an updated tile scales it") {
+  std::mt19937_64 rng(61);
+  auto c = circ::paper_cfg(6, 6);
+  auto g = circ::random_tile(c, rng);
+  DistortionCache cache;
+  cache.refresh_interval = 10;
+  refresh_distortion(cache, c, g, int(EngineKind::fcm), FcmOptions{});
+  Matrix moved = g;
+  for (double& x : moved.v) x *= 0.97;
+  auto approx = apply_distortion(cache, moved);
+  for (size_t k = 0; k < g.v.size(); ++k) CHECK(approx.v[k] == Approx(moved.v[k] * (1.0 - cache.d.v[k])).epsilon(1e-15));
+}
+
 MT_MAIN

@@ -463,23 +463,391 @@ bool CrossbarCore::fully_ideal() const {
          opt_.adc.bits == 0;
 }
 
-// layers.cpp:90-127 (ideal, aam; fcm/oracle only in their zero-parasitic
-// identity case fcm.cpp:181-184 / layers.cpp:105-107 -- the iterative solves
-// are out of scope), then the snapped-mode grid.
-Matrix CrossbarCore::convert_tile(const Matrix& tile) {
+// ------------------------------------------------------------------- fcm.cpp
+namespace {
+
+// fcm.cpp:18-46: Thomas algorithm for the top nodes of row i, bottom nodes
+// fixed; the driver reaches T(i, 0) through r_source plus one row segment.
+void solve_row_tridiag(const CrossbarConfig& cfg, const Matrix& g, long i, double v_drive, const Matrix& v_bot,
+                       Matrix& v_top, std::vector<double>& cw, std::vector<double>& dw) {
+  const long C = cfg.cols;
+  const double g_seg = 1.0 / cfg.r_row;
+  const double g_drv = 1.0 / (cfg.r_source + cfg.r_row);
+  double prev_c = 0.0, prev_d = 0.0;
+  for (long j = 0; j < C; ++j) {
+    const double gl = (j == 0) ? g_drv : g_seg;
+    const double gr = (j < C - 1) ? g_seg : 0.0;
+    const double diag = gl + gr + g(i, j);
+    double rhs = g(i, j) * v_bot(i, j);
+    if (j == 0) rhs += gl * v_drive;
+    const double denom = diag - gl * prev_c;
+    prev_c = gr / denom;
+    prev_d = (rhs + gl * prev_d) / denom;
+    cw[size_t(j)] = prev_c;
+    dw[size_t(j)] = prev_d;
+  }
+  double x = dw[size_t(C - 1)];
+  v_top(i, C - 1) = x;
+  for (long j = C - 2; j >= 0; --j) {
+    x = dw[size_t(j)] + cw[size_t(j)] * x;
+    v_top(i, j) = x;
+  }
+}
+
+// fcm.cpp:48-76: bottom nodes of column j, top nodes fixed; the foot drains
+// to ground through one column segment plus r_sense.
+void solve_col_tridiag(const CrossbarConfig& cfg, const Matrix& g, long j, const Matrix& v_top, Matrix& v_bot,
+                       std::vector<double>& cw, std::vector<double>& dw) {
+  const long R = cfg.rows;
+  const double g_seg = 1.0 / cfg.r_col;
+  const double g_foot = 1.0 / (cfg.r_col + cfg.r_sense);
+  double prev_c = 0.0, prev_d = 0.0;
+  for (long i = 0; i < R; ++i) {
+    const double gu = (i > 0) ? g_seg : 0.0;
+    const double gd = (i < R - 1) ? g_seg : g_foot;
+    const double diag = gu + gd + g(i, j);
+    const double rhs = g(i, j) * v_top(i, j);
+    const double denom = diag - gu * prev_c;
+    prev_c = gd / denom;
+    prev_d = (rhs + gu * prev_d) / denom;
+    cw[size_t(i)] = prev_c;
+    dw[size_t(i)] = prev_d;
+  }
+  double x = dw[size_t(R - 1)];
+  v_bot(R - 1, j) = x;
+  for (long i = R - 2; i >= 0; --i) {
+    x = dw[size_t(i)] + cw[size_t(i)] * x;
+    v_bot(i, j) = x;
+  }
+}
+
+// fcm.cpp:78-108: rows / columns collapsed to one node (zero wire resistance)
+void solve_row_collapsed(const CrossbarConfig& cfg, const Matrix& g, long i, double v_drive, const Matrix& v_bot,
+                         Matrix& v_top) {
+  if (cfg.r_source == 0.0) {
+    for (long j = 0; j < cfg.cols; ++j) v_top(i, j) = v_drive;
+    return;
+  }
+  double num = v_drive / cfg.r_source;
+  double den = 1.0 / cfg.r_source;
+  for (long j = 0; j < cfg.cols; ++j) {
+    num += g(i, j) * v_bot(i, j);
+    den += g(i, j);
+  }
+  for (long j = 0; j < cfg.cols; ++j) v_top(i, j) = num / den;
+}
+
+void solve_col_collapsed(const CrossbarConfig& cfg, const Matrix& g, long j, const Matrix& v_top, Matrix& v_bot) {
+  if (cfg.r_sense == 0.0) {
+    for (long i = 0; i < cfg.rows; ++i) v_bot(i, j) = 0.0;
+    return;
+  }
+  double num = 0.0;
+  double den = 1.0 / cfg.r_sense;
+  for (long i = 0; i < cfg.rows; ++i) {
+    num += g(i, j) * v_top(i, j);
+    den += g(i, j);
+  }
+  for (long i = 0; i < cfg.rows; ++i) v_bot(i, j) = num / den;
+}
+
+}  // namespace
+
+// fcm.cpp:112-153
+LadderResult solve_ladder(const CrossbarConfig& cfg, const Matrix& g, const std::vector<double>& v_in, double tol,
+                          int max_iter) {
+  const long R = cfg.rows, C = cfg.cols;
+  LadderResult res;
+  res.v_top = Matrix(R, C);
+  for (long j = 0; j < C; ++j)
+    for (long i = 0; i < R; ++i) res.v_top(i, j) = v_in[size_t(i)];
+  res.v_bot = Matrix(R, C, 0.0);
+  std::vector<double> cw(size_t(std::max(R, C))), dw(size_t(std::max(R, C)));
+  for (int sweep = 1; sweep <= max_iter; ++sweep) {
+    const Matrix top_prev = res.v_top, bot_prev = res.v_bot;
+    for (long i = 0; i < R; ++i) {
+      if (cfg.r_row == 0.0) solve_row_collapsed(cfg, g, i, v_in[size_t(i)], res.v_bot, res.v_top);
+      else solve_row_tridiag(cfg, g, i, v_in[size_t(i)], res.v_bot, res.v_top, cw, dw);
+    }
+    for (long j = 0; j < C; ++j) {
+      if (cfg.r_col == 0.0) solve_col_collapsed(cfg, g, j, res.v_top, res.v_bot);
+      else solve_col_tridiag(cfg, g, j, res.v_top, res.v_bot, cw, dw);
+    }
+    double delta = 0.0;
+    for (size_t k = 0; k < res.v_top.v.size(); ++k) delta = std::max(delta, std::fabs(res.v_top.v[k] - top_prev.v[k]));
+    for (size_t k = 0; k < res.v_bot.v.size(); ++k) delta = std::max(delta, std::fabs(res.v_bot.v[k] - bot_prev.v[k]));
+    res.sweeps = sweep;
+    res.residual = delta / cfg.v_fs;
+    if (res.residual <= tol) {
+      res.converged = true;
+      return res;
+    }
+  }
+  return res;
+}
+
+// fcm.cpp:169-224
+Matrix fcm_convert(const CrossbarConfig& cfg, const Matrix& g, const FcmOptions& opt) {
+  if (!(opt.tol > 0.0) || !std::isfinite(opt.tol))
+    throw std::invalid_argument("fcm_convert: tol must be positive and finite");
+  if (opt.max_iter < 1) throw std::invalid_argument("fcm_convert: max_iter must be >= 1");
+  std::vector<double> v_cal = opt.v_cal;
+  if (v_cal.empty()) v_cal.assign(size_t(cfg.rows), cfg.v_fs);
+  if (long(v_cal.size()) != cfg.rows) throw std::invalid_argument("fcm_convert: v_cal length does not match tile rows");
+  for (double v : v_cal)
+    if (!std::isfinite(v) || v < 0.0 || v > cfg.v_fs)
+      throw std::invalid_argument("fcm_convert: v_cal entries must lie in [0, v_fs]");
+  if (cfg.r_row == 0.0 && cfg.r_col == 0.0 && cfg.r_source == 0.0 && cfg.r_sense == 0.0) return g;
+  auto run = [&](const std::vector<double>& v) {
+    LadderResult r = solve_ladder(cfg, g, v, opt.tol, opt.max_iter);
+    if (!r.converged)
+      throw ConvergenceError("fcm_convert: no fixed point after " + std::to_string(opt.max_iter) +
+                                 " sweeps (residual " + std::to_string(r.residual) + ")",
+                             r.residual, r.sweeps);
+    return r;
+  };
+  LadderResult sol = run(v_cal);
+  Matrix gn(cfg.rows, cfg.cols);
+  bool any_zero = false;
+  for (long i = 0; i < cfg.rows; ++i) {
+    if (v_cal[size_t(i)] == 0.0) {
+      any_zero = true;
+      continue;
+    }
+    for (long j = 0; j < cfg.cols; ++j) {
+      const double gij = g(i, j);
+      const double v_dev = sol.v_top(i, j) - sol.v_bot(i, j);
+      const double eff = gij * v_dev / v_cal[size_t(i)];
+      gn(i, j) = std::min(std::max(eff, 0.0), gij);
+    }
+  }
+  if (any_zero) {
+    std::vector<double> v_fb = v_cal;
+    for (double& v : v_fb)
+      if (v == 0.0) v = cfg.v_fs;
+    LadderResult fb = run(v_fb);
+    for (long i = 0; i < cfg.rows; ++i) {
+      if (v_cal[size_t(i)] != 0.0) continue;
+      for (long j = 0; j < cfg.cols; ++j) {
+        const double gij = g(i, j);
+        const double eff = gij * (fb.v_top(i, j) - fb.v_bot(i, j)) / cfg.v_fs;
+        gn(i, j) = std::min(std::max(eff, 0.0), gij);
+      }
+    }
+  }
+  return gn;
+}
+
+// ------------------------------------------------------------------ nodal.cpp
+namespace {
+
+std::vector<double> column_currents(const Matrix& g, const Matrix& v_top, const Matrix& v_bot) {
+  std::vector<double> i_col(size_t(g.cols));
+  for (long j = 0; j < g.cols; ++j) {
+    double acc = 0.0;
+    for (long i = 0; i < g.rows; ++i) acc += g(i, j) * (v_top(i, j) - v_bot(i, j));
+    i_col[size_t(j)] = acc;
+  }
+  return i_col;
+}
+
+struct NodeRef {
+  long index = -1;  // >= 0: unknown
+  double value = 0.0;
+  bool fixed() const { return index < 0; }
+};
+
+// nodal.cpp:41-143 with zero-resistance chains collapsed onto supernodes (or
+// onto the driver / ground); the SPD system is factorised by a plain
+// row-oriented Cholesky (Eigen's LLT order is not reproducible here anyway).
+NodalSolution solve_dense(const CrossbarConfig& cfg, const Matrix& g, const std::vector<double>& v_in) {
+  const long R = cfg.rows, C = cfg.cols;
+  const bool rows_chain = cfg.r_row > 0.0, rows_super = !rows_chain && cfg.r_source > 0.0;
+  const bool cols_chain = cfg.r_col > 0.0, cols_super = !cols_chain && cfg.r_sense > 0.0;
+  long n = 0;
+  std::vector<long> top_idx, bot_idx, row_super(size_t(R), -1), col_super(size_t(C), -1);
+  if (rows_chain) {
+    top_idx.resize(size_t(R * C));
+    for (long i = 0; i < R; ++i)
+      for (long j = 0; j < C; ++j) top_idx[size_t(i * C + j)] = n++;
+  } else if (rows_super) {
+    for (long i = 0; i < R; ++i) row_super[size_t(i)] = n++;
+  }
+  if (cols_chain) {
+    bot_idx.resize(size_t(R * C));
+    for (long i = 0; i < R; ++i)
+      for (long j = 0; j < C; ++j) bot_idx[size_t(i * C + j)] = n++;
+  } else if (cols_super) {
+    for (long j = 0; j < C; ++j) col_super[size_t(j)] = n++;
+  }
+  auto top = [&](long i, long j) -> NodeRef {
+    if (rows_chain) return {top_idx[size_t(i * C + j)], 0.0};
+    if (rows_super) return {row_super[size_t(i)], 0.0};
+    return {-1, v_in[size_t(i)]};
+  };
+  auto bot = [&](long i, long j) -> NodeRef {
+    if (cols_chain) return {bot_idx[size_t(i * C + j)], 0.0};
+    if (cols_super) return {col_super[size_t(j)], 0.0};
+    return {-1, 0.0};
+  };
+  std::vector<double> A(size_t(n * n), 0.0), b(size_t(n), 0.0);
+  auto stamp = [&](NodeRef a, NodeRef c, double gamma) {
+    if (gamma == 0.0) return;
+    if (!a.fixed() && !c.fixed()) {
+      if (a.index == c.index) return;
+      A[size_t(a.index * n + a.index)] += gamma;
+      A[size_t(c.index * n + c.index)] += gamma;
+      A[size_t(a.index * n + c.index)] -= gamma;
+      A[size_t(c.index * n + a.index)] -= gamma;
+    } else if (!a.fixed()) {
+      A[size_t(a.index * n + a.index)] += gamma;
+      b[size_t(a.index)] += gamma * c.value;
+    } else if (!c.fixed()) {
+      A[size_t(c.index * n + c.index)] += gamma;
+      b[size_t(c.index)] += gamma * a.value;
+    }
+  };
+  for (long i = 0; i < R; ++i)
+    for (long j = 0; j < C; ++j) stamp(top(i, j), bot(i, j), g(i, j));
+  if (rows_chain) {
+    for (long i = 0; i < R; ++i) {
+      stamp({-1, v_in[size_t(i)]}, top(i, 0), 1.0 / (cfg.r_source + cfg.r_row));
+      for (long j = 0; j + 1 < C; ++j) stamp(top(i, j), top(i, j + 1), 1.0 / cfg.r_row);
+    }
+  } else if (rows_super) {
+    for (long i = 0; i < R; ++i) stamp({-1, v_in[size_t(i)]}, {row_super[size_t(i)], 0.0}, 1.0 / cfg.r_source);
+  }
+  if (cols_chain) {
+    for (long j = 0; j < C; ++j) {
+      for (long i = 0; i + 1 < R; ++i) stamp(bot(i, j), bot(i + 1, j), 1.0 / cfg.r_col);
+      stamp(bot(R - 1, j), {-1, 0.0}, 1.0 / (cfg.r_col + cfg.r_sense));
+    }
+  } else if (cols_super) {
+    for (long j = 0; j < C; ++j) stamp({col_super[size_t(j)], 0.0}, {-1, 0.0}, 1.0 / cfg.r_sense);
+  }
+  std::vector<double> x(size_t(n), 0.0);
+  if (n > 0) {
+    // Cholesky A = L L^T (L stored in the lower triangle of A)
+    for (long k = 0; k < n; ++k) {
+      double d = A[size_t(k * n + k)];
+      for (long m = 0; m < k; ++m) d -= A[size_t(k * n + m)] * A[size_t(k * n + m)];
+      if (!(d > 0.0)) throw DegenerateCircuitError("solve_nodal_oracle: singular nodal system");
+      const double lkk = std::sqrt(d);
+      A[size_t(k * n + k)] = lkk;
+      for (long r = k + 1; r < n; ++r) {
+        double v = A[size_t(r * n + k)];
+        for (long m = 0; m < k; ++m) v -= A[size_t(r * n + m)] * A[size_t(k * n + m)];
+        A[size_t(r * n + k)] = v / lkk;
+      }
+    }
+    std::vector<double> y(static_cast<size_t>(n));
+    for (long r = 0; r < n; ++r) {
+      double v = b[size_t(r)];
+      for (long m = 0; m < r; ++m) v -= A[size_t(r * n + m)] * y[size_t(m)];
+      y[size_t(r)] = v / A[size_t(r * n + r)];
+    }
+    for (long r = n - 1; r >= 0; --r) {
+      double v = y[size_t(r)];
+      for (long m = r + 1; m < n; ++m) v -= A[size_t(m * n + r)] * x[size_t(m)];
+      x[size_t(r)] = v / A[size_t(r * n + r)];
+    }
+    for (double v : x)
+      if (!std::isfinite(v)) throw DegenerateCircuitError("solve_nodal_oracle: non-finite nodal solution");
+  }
+  NodalSolution sol;
+  sol.v_top = Matrix(R, C);
+  sol.v_bot = Matrix(R, C);
+  for (long i = 0; i < R; ++i)
+    for (long j = 0; j < C; ++j) {
+      const NodeRef t = top(i, j), c = bot(i, j);
+      sol.v_top(i, j) = t.fixed() ? t.value : x[size_t(t.index)];
+      sol.v_bot(i, j) = c.fixed() ? c.value : x[size_t(c.index)];
+    }
+  sol.i_col = column_currents(g, sol.v_top, sol.v_bot);
+  return sol;
+}
+
+}  // namespace
+
+// nodal.cpp:147-176
+NodalSolution solve_nodal_oracle(const CrossbarConfig& cfg, const Matrix& g, const std::vector<double>& v_in) {
+  if (long(v_in.size()) != cfg.rows) throw std::invalid_argument("solve_nodal_oracle: v_in length does not match rows");
+  for (double v : v_in)
+    if (!std::isfinite(v) || v < 0.0 || v > cfg.v_fs)
+      throw std::invalid_argument("solve_nodal_oracle: v_in entries must lie in [0, v_fs]");
+  const bool no_par = cfg.r_row == 0.0 && cfg.r_col == 0.0 && cfg.r_source == 0.0 && cfg.r_sense == 0.0;
+  bool all_zero = true;
+  for (double x : g.v) all_zero = all_zero && x == 0.0;
+  if (no_par && all_zero) throw DegenerateCircuitError("solve_nodal_oracle: all conductances zero with zero parasitics");
+  if (cfg.rows <= 32 && cfg.cols <= 32) return solve_dense(cfg, g, v_in);
+  LadderResult r = solve_ladder(cfg, g, v_in, 1e-10, 50000);
+  if (!r.converged) throw ConvergenceError("solve_nodal_oracle: relaxation did not converge", r.residual, r.sweeps);
+  NodalSolution sol;
+  sol.v_top = r.v_top;
+  sol.v_bot = r.v_bot;
+  sol.i_col = column_currents(g, sol.v_top, sol.v_bot);
+  return sol;
+}
+
+// ------------------------------------------------------------ distortion.cpp
+void refresh_distortion(DistortionCache& cache, const CrossbarConfig& cfg, const Matrix& ideal, int engine_kind,
+                        const FcmOptions& fcm_opt) {
+  if (cache.refresh_interval < 1) throw std::invalid_argument("refresh_distortion: refresh_interval must be >= 1");
+  if (engine_kind != int(EngineKind::fcm) && engine_kind != int(EngineKind::aam))
+    throw std::invalid_argument("refresh_distortion: engine must be fcm or aam");
+  Matrix non = engine_kind == int(EngineKind::fcm) ? fcm_convert(cfg, ideal, fcm_opt) : aam_convert(cfg, ideal);
+  cache.d = Matrix(ideal.rows, ideal.cols);
+  for (long j = 0; j < ideal.cols; ++j)
+    for (long i = 0; i < ideal.rows; ++i) {
+      const double gi = ideal(i, j);
+      cache.d(i, j) = (gi == 0.0) ? 0.0 : (gi - non(i, j)) / gi;
+    }
+  cache.g_at_refresh = ideal;
+  cache.g_non_at_refresh = non;
+  cache.age = 0;
+}
+
+Matrix apply_distortion(DistortionCache& cache, const Matrix& ideal) {
+  if (cache.d.v.empty()) throw StateError("apply_distortion: cache never refreshed");
+  if (cache.d.rows != ideal.rows || cache.d.cols != ideal.cols)
+    throw std::invalid_argument("apply_distortion: cache dims do not match tile");
+  if (cache.age >= cache.refresh_interval)
+    throw StaleCacheError("apply_distortion: cache age " + std::to_string(cache.age) + " reached refresh interval " +
+                          std::to_string(cache.refresh_interval));
+  ++cache.age;
+  if (ideal.v == cache.g_at_refresh.v) return cache.g_non_at_refresh;  // unchanged tile: stored conversion
+  Matrix gn(ideal.rows, ideal.cols);
+  for (size_t k = 0; k < gn.v.size(); ++k) gn.v[k] = ideal.v[k] * (1.0 - cache.d.v[k]);
+  return gn;
+}
+
+// layers.cpp:90-127 (ideal, aam, fcm, interp_fcm; the oracle engine only in
+// its zero-parasitic identity case layers.cpp:105-107 -- the nodal solve is
+// §8f row 4), then the snapped-mode grid.
+Matrix CrossbarCore::convert_tile(const Matrix& tile, int slice, int pol, int tile_index) {
   const CrossbarConfig& cfg = weights_.tile_config();
+  FcmOptions fo;
+  fo.tol = opt_.fcm_tol;
+  fo.max_iter = opt_.fcm_max_iter;
+  const bool zero_par = cfg.r_row == 0.0 && cfg.r_col == 0.0 && cfg.r_source == 0.0 && cfg.r_sense == 0.0;
   Matrix g;
   switch (opt_.engine) {
     case EngineKind::ideal: g = tile; break;
     case EngineKind::aam: g = aam_convert(cfg, tile); break;
-    case EngineKind::fcm:
+    case EngineKind::fcm: g = fcm_convert(cfg, tile, fo); break;
+    case EngineKind::interp_fcm: {
+      DistortionCache& cache = caches_[size_t(slice)][size_t(pol)][size_t(tile_index)];
+      if (update_count_ % uint64_t(opt_.interp_interval) == 0)
+        refresh_distortion(cache, cfg, tile, int(opt_.interp_base), fo);
+      g = apply_distortion(cache, tile);
+      break;
+    }
     case EngineKind::oracle:
-    case EngineKind::interp_fcm:
-      if (cfg.r_row == 0.0 && cfg.r_col == 0.0 && cfg.r_source == 0.0 && cfg.r_sense == 0.0) {
+      if (zero_par) {
         g = tile;
         break;
       }
-      throw ConfigError("oracle: fcm/oracle/interp_fcm engines with parasitics are out of scope");
+      throw ConfigError("oracle: the nodal-oracle engine with parasitics is out of scope (SURVEY.md 8f-4)");
   }
   if (opt_.snapped)
     for (double& x : g.v) x = snap_conductance(x, snap_e_);
@@ -494,8 +862,18 @@ void CrossbarCore::regenerate() {
   }
   const int slices = weights_.num_slices();
   const int tiles = weights_.grid_rows() * weights_.grid_cols();
-  if (nonideal_.empty())
+  const bool interp = opt_.engine == EngineKind::interp_fcm;
+  const bool refresh_now = !interp || update_count_ % uint64_t(opt_.interp_interval) == 0;
+  if (nonideal_.empty()) {
     nonideal_.assign(size_t(slices), std::vector<std::vector<Matrix>>(2, std::vector<Matrix>(size_t(tiles))));
+    if (interp) {
+      caches_.assign(size_t(slices),
+                     std::vector<std::vector<DistortionCache>>(2, std::vector<DistortionCache>(size_t(tiles))));
+      for (auto& ps : caches_)
+        for (auto& pp : ps)
+          for (auto& c : pp) c.refresh_interval = opt_.interp_interval;
+    }
+  }
   std::vector<int> which = regen_tiles;
   if (which.empty())
     for (int t = 0; t < tiles; ++t) which.push_back(t);
@@ -504,9 +882,9 @@ void CrossbarCore::regenerate() {
       for (int t : which) {
         const int tr = t / weights_.grid_cols(), tc = t % weights_.grid_cols();
         nonideal_[size_t(s)][size_t(p)][size_t(t)] =
-            convert_tile(weights_.ideal_tile(s, p == 0 ? Polarity::pos : Polarity::neg, tr, tc));
+            convert_tile(weights_.ideal_tile(s, p == 0 ? Polarity::pos : Polarity::neg, tr, tc), s, p, t);
       }
-  if (opt_.engine != EngineKind::ideal) ++refreshes_;
+  if (refresh_now && opt_.engine != EngineKind::ideal) ++refreshes_;
 }
 
 const Matrix& CrossbarCore::nonideal(int slice, Polarity p, int tile) const {

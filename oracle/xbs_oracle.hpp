@@ -200,6 +200,52 @@ double variation_multiplier(uint64_t seed, int slice, Polarity p, int64_t linear
 // aam.cpp:5-35; `g` is a tile of cfg.rows x cfg.cols.
 Matrix aam_convert(const CrossbarConfig& cfg, const Matrix& g);
 
+// ----------------------------------------------------- fcm.hpp / ladder.hpp
+// fcm.cpp:14-224: block Gauss-Seidel over the row and column ladders, each
+// line solved exactly by the Thomas algorithm, to a fixed point.
+struct ConvergenceError : std::runtime_error {
+  double residual;
+  int iterations;
+  ConvergenceError(const std::string& m, double r, int it) : std::runtime_error(m), residual(r), iterations(it) {}
+};
+struct StaleCacheError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct FcmOptions {  // fcm.hpp:9-16
+  std::vector<double> v_cal;  // empty: all rows at v_fs
+  double tol = 1e-6;
+  int max_iter = 1000;
+};
+struct LadderResult {  // ladder.hpp:11-17
+  Matrix v_top, v_bot;
+  int sweeps = 0;
+  double residual = 0.0;
+  bool converged = false;
+};
+LadderResult solve_ladder(const CrossbarConfig& cfg, const Matrix& g, const std::vector<double>& v_in, double tol,
+                          int max_iter);
+Matrix fcm_convert(const CrossbarConfig& cfg, const Matrix& g, const FcmOptions& opt = {});
+
+// ----------------------------------------------------------------- nodal.hpp
+// nodal.cpp:14-176: the exact parasitic network (KCL at every top and bottom
+// node) -- dense Cholesky up to 32x32 tiles, the ladder relaxation to 1e-10
+// above.  CPU-only validation of FCM / AAM.
+struct DegenerateCircuitError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NodalSolution {
+  Matrix v_top, v_bot;
+  std::vector<double> i_col;
+};
+NodalSolution solve_nodal_oracle(const CrossbarConfig& cfg, const Matrix& g, const std::vector<double>& v_in);
+
+// ------------------------------------------------------------ distortion.hpp
+// distortion.cpp:10-48: interp_fcm's cached per-device distortion profile.
+struct DistortionCache {
+  Matrix d, g_at_refresh, g_non_at_refresh;
+  int age = 0;
+  int refresh_interval = 10;
+};
+void refresh_distortion(DistortionCache& cache, const CrossbarConfig& cfg, const Matrix& ideal, int engine_kind,
+                        const FcmOptions& fcm_opt);
+Matrix apply_distortion(DistortionCache& cache, const Matrix& ideal);
+
 // ---------------------------------------------------------------- update.hpp
 struct UpdateSpec {  // update.hpp:13-23
   double v = 0.0, gamma = 0.0, lr = 0.01;
@@ -284,7 +330,7 @@ class CrossbarCore {  // layers.hpp:49-111
   void maybe_freeze_adc();
   Matrix sense(const Matrix& currents, const AdcSpec& spec, AdcCalibrator& cal, bool observe);
   Matrix currents(const Matrix& V, long col0, const Matrix& G, bool transpose) const;
-  Matrix convert_tile(const Matrix& tile);
+  Matrix convert_tile(const Matrix& tile, int slice, int pol, int tile_index);
   double k_out_fwd() const;
   double k_out_bwd(double step_e) const;
 
@@ -292,6 +338,7 @@ class CrossbarCore {  // layers.hpp:49-111
   TiledLayerWeights weights_;
   Matrix wimp_;
   std::vector<std::vector<std::vector<Matrix>>> nonideal_;
+  std::vector<std::vector<std::vector<DistortionCache>>> caches_;  // interp_fcm
   AdcSpec adc_fwd_, adc_bwd_;
   AdcCalibrator cal_fwd_, cal_bwd_;
   bool adc_auto_ = false, adc_frozen_ = false;
