@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-peak", action="store_true", help="skip the live int8 peak GEMM (ncu launch lists)")
     p.add_argument("--layer", type=int, default=0, help="layer index of a multi-layer config (default 0)")
+    p.add_argument("--engine", default=None, choices=["aam", "fcm", "interp_fcm", "ideal"],
+                   help="override the config's conversion engine")
     p.add_argument("--all-layers", action="store_true",
                    help="every layer of the config (C1/C3/C4 networks), one core per layer on one stream")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
@@ -252,6 +254,8 @@ def main():
 
     layers = list(cfg.layers) if args.all_layers else [cfg.layers[args.layer]]
     opt = cfg.options()
+    if args.engine:
+        opt.engine = getattr(xb.EngineKind, args.engine)
     cores, host, dev = [], [], []
     for li, layer in enumerate(layers):
         W, x, dy = cfg.weights(layer, li), cfg.inputs(layer, li), cfg.errors(layer, li)

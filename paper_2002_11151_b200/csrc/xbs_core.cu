@@ -25,6 +25,12 @@ struct XbsError : std::runtime_error {
   XbsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 [[noreturn]] void fail(int code, const std::string& m) { throw XbsError(code, m); }
+void ck(cudaError_t e, const char* what);
+}  // namespace
+namespace xbs {
+void ck_cuda(cudaError_t e, const char* what) { ck(e, what); }
+}  // namespace xbs
+namespace {
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(XBS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -123,8 +129,14 @@ void validate_options(const xbs_layer_options& o, const std::vector<double>& dac
 // B200 path does not evaluate are refused loudly, never approximated.
 void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, const std::vector<double>& adc_tr) {
   const bool zero_par = o.r_row == 0.0 && o.r_col == 0.0 && o.r_source == 0.0 && o.r_sense == 0.0;
-  if ((o.engine == XBS_ENGINE_FCM || o.engine == XBS_ENGINE_ORACLE || o.engine == XBS_ENGINE_INTERP_FCM) && !zero_par)
-    fail(XBS_UNSUPPORTED, "engine fcm/oracle/interp_fcm with parasitics is not on this path (SURVEY §8f-1)");
+  if (o.engine == XBS_ENGINE_ORACLE && !zero_par)
+    fail(XBS_UNSUPPORTED, "engine oracle (dense nodal solve) with parasitics is not on this path (SURVEY §8f-4)");
+  if ((o.engine == XBS_ENGINE_FCM || (o.engine == XBS_ENGINE_INTERP_FCM && o.interp_base == XBS_ENGINE_FCM)) &&
+      !zero_par) {  // fcm.cpp:170-173, checked when the first tile is converted
+    if (!(o.fcm_tol > 0.0) || !std::isfinite(o.fcm_tol))
+      fail(XBS_INVALID_ARGUMENT, "fcm_convert: tol must be positive and finite");
+    if (o.fcm_max_iter < 1) fail(XBS_INVALID_ARGUMENT, "fcm_convert: max_iter must be >= 1");
+  }
   if (o.engine < 0 || o.engine > 4) fail(XBS_INVALID_ARGUMENT, "unknown engine");
   if (o.adc_bits > 0 && adc_tr.empty() && !(o.adc_i_fs > 0))
     fail(XBS_UNSUPPORTED, "ADC auto-calibration (adc.i_fs <= 0) is not on this path: pin adc.i_fs (SURVEY §8f-3)");
@@ -194,7 +206,36 @@ void sync(xbs_core* c) {
 
 void regenerate_bookkeeping(xbs_core* c) {
   if (c->opt.engine == XBS_ENGINE_IDEAL) xbs::launch_implied(c, c->d_wimp, c->stream);
-  if (c->opt.engine != XBS_ENGINE_IDEAL) ++c->refreshes;  // layers.cpp:176
+  const bool refresh_now = c->opt.engine != XBS_ENGINE_INTERP_FCM ||
+                           c->update_count % uint64_t(c->opt.interp_interval) == 0;  // layers.cpp:145-147
+  if (c->opt.engine != XBS_ENGINE_IDEAL && refresh_now) ++c->refreshes;           // layers.cpp:176
+}
+
+// Per-tile regeneration for the circuit engines (layers.cpp:129-179 with
+// convert_tile 90-127): fcm every time, interp_fcm refreshing its distortion
+// profile every interp_interval updates and applying it in between.
+void regenerate_tiles(xbs_core* c) {
+  ck(cudaMemsetAsync(&c->d_sc->fcm_fail, 0, sizeof(unsigned) * 2 + sizeof(unsigned long long), c->stream),
+     "memset");
+  if (c->opt.engine == XBS_ENGINE_INTERP_FCM && c->update_count % uint64_t(c->opt.interp_interval) != 0)
+    xbs::launch_interp_apply(c, c->stream);
+  else
+    xbs::launch_fcm_regen(c, c->opt.engine == XBS_ENGINE_INTERP_FCM, c->stream);
+  c->launches += 1;
+}
+
+void regenerate_all(xbs_core* c) {
+  if (c->fully_ideal) return;
+  if (c->tile_engine) regenerate_tiles(c);
+  else xbs::launch_regen_all(c, c->stream);
+}
+
+// fcm.cpp:186-190: a tile without a fixed point raises ConvergenceError
+void check_fcm(xbs_core* c) {
+  if (!c->tile_engine || c->h_sc->fcm_fail == 0) return;
+  const double r = __builtin_bit_cast(double, c->h_sc->fcm_residual);
+  fail(XBS_CONVERGENCE_ERROR, "fcm_convert: no fixed point after " + std::to_string(c->opt.fcm_max_iter) +
+                                  " sweeps (residual " + std::to_string(r) + ")");
 }
 
 // host col-major (ld) <-> device row-major (rows x cols)
@@ -316,7 +357,9 @@ void apply_updates_device(xbs_core* c, uint64_t iteration) {
   ck(cudaMemsetAsync(&c->d_sc->dwmax, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
   ck(cudaMemsetAsync(&c->d_sc->err_flag, 0, sizeof(int), c->stream), "memset");
   StageScope st(c, XBS_STAGE_UPDATE);
-  xbs::launch_update(c, up, c->stream);
+  xbs::launch_update(c, up, c->stream, c->tile_engine);  // tile engines: master only, then per-tile regeneration
+  ++c->update_count;                                     // layers.cpp:389
+  if (c->tile_engine) regenerate_tiles(c);
   regenerate_bookkeeping(c);
   c->launches += c->opt.engine == XBS_ENGINE_IDEAL ? 2 : 1;
   c->have_grad = false;
@@ -326,6 +369,7 @@ void apply_updates_device(xbs_core* c, uint64_t iteration) {
 void finish_update_stats(xbs_core* c) {
   ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
   if (c->h_sc->err_flag) fail(XBS_INVALID_ARGUMENT, "nonlinear_update: g outside device range");
+  check_fcm(c);
   c->dwmax_seen = std::max(c->dwmax_seen, __builtin_bit_cast(double, c->h_sc->dwmax));
   c->wmax_seen = std::max(c->wmax_seen, __builtin_bit_cast(double, c->h_sc->wmax));
 }
@@ -446,6 +490,8 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     rp.r_source = o.r_source;
     rp.r_sense = o.r_sense;
     rp.aam = (o.engine == XBS_ENGINE_AAM && !zero_par) ? 1 : 0;
+    c->tile_engine = (o.engine == XBS_ENGINE_FCM || o.engine == XBS_ENGINE_INTERP_FCM) && !zero_par;
+    c->fcm = xbs::FcmP{o.r_row, o.r_col, o.r_source, o.r_sense, o.v_fs, o.fcm_tol, o.fcm_max_iter, 1};
     rp.snap_e = snap_exponent(o.g_max);
     rp.snap_scale = std::ldexp(1.0, rp.snap_e);
     rp.kpnp = uint64_t(g.Kp) * g.Np;
@@ -537,10 +583,18 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
       c->rp.varm = c->d_varm;
       xbs::launch_varm(c.get(), c->stream);
     }
+    if (c->tile_engine && o.engine == XBS_ENGINE_INTERP_FCM) {
+      const size_t n = size_t(g.S) * 2 * size_t(g.Kp) * g.Np * sizeof(double);
+      ck(cudaMalloc(&c->d_cache_d, n), "cudaMalloc distortion cache");
+      ck(cudaMalloc(&c->d_cache_g, n), "cudaMalloc distortion cache");
+      ck(cudaMalloc(&c->d_cache_gn, n), "cudaMalloc distortion cache");
+    }
     const auto t0 = std::chrono::steady_clock::now();
-    if (!c->fully_ideal) xbs::launch_regen_all(c.get(), c->stream);
+    regenerate_all(c.get());
     regenerate_bookkeeping(c.get());
     sync(c.get());
+    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    check_fcm(c.get());
     c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     cudaFree(d_W);
     *out = c.release();
@@ -554,6 +608,10 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_adc_tab);
   cudaFree(c->d_qmin);
   cudaFree(c->d_varm);
+  cudaFree(c->d_fcm_scratch);
+  cudaFree(c->d_cache_d);
+  cudaFree(c->d_cache_g);
+  cudaFree(c->d_cache_gn);
   cudaFree(c->d_master);
   cudaFree(c->d_dW);
   cudaFree(c->d_wimp);
@@ -730,9 +788,11 @@ int xbs_core_set_master(xbs_core* c, int32_t s, const double* u, int64_t ld) {
     if (!c || s < 0 || s >= c->g.S || !u || ld < c->g.Kp) fail(XBS_INVALID_ARGUMENT, "set_master: bad arguments");
     sync(c);
     h2d_colmajor_to_rowmajor(c, u, c->g.Kp, c->g.Np, ld, c->d_master + size_t(s) * c->g.Kp * c->g.Np);
-    if (!c->fully_ideal) xbs::launch_regen_all(c, c->stream);
+    regenerate_all(c);
     if (c->opt.engine == XBS_ENGINE_IDEAL) xbs::launch_implied(c, c->d_wimp, c->stream);
     sync(c);
+    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    check_fcm(c);
   });
 }
 

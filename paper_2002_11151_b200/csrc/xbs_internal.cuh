@@ -90,6 +90,17 @@ struct DevScalars {
   int err_flag;              // 1: nonlinear_update range violation
   int pad;
   unsigned long long exact_path, conversions;
+  unsigned int fcm_fail;                 // FCM tiles without a fixed point in the last regeneration
+  unsigned int pad2;
+  unsigned long long fcm_residual;       // bits of the largest such residual (relative to v_fs)
+};
+
+// FCM conversion parameters (fcm.hpp:9-16, tile geometry and parasitics of
+// the mapped tile config, mapping.cpp:60-67)
+struct FcmP {
+  double r_row, r_col, r_source, r_sense, v_fs, tol;
+  int max_iter;
+  int use_fcm;  // 0: interp_fcm with the AAM base
 };
 
 }  // namespace xbs
@@ -100,6 +111,9 @@ struct xbs_core {
   xbs::Geo g;
   xbs::RegenP rp{};
   xbs::AdcP adc{};
+  xbs::FcmP fcm{};
+  bool tile_engine = false;     // fcm / interp_fcm with parasitics: per-tile regeneration kernels
+  uint64_t update_count = 0;    // layers.cpp:389 (interp refresh schedule)
   cudaStream_t stream = nullptr;
   bool own_stream = true;  // false after xbs_core_set_stream(caller's stream)
   int kernel = 0;  // 0 tcgen05, 1 SIMT
@@ -113,6 +127,11 @@ struct xbs_core {
   uint8_t* d_digits = nullptr;
   uint32_t* d_qmin = nullptr;  // sigma == 0: snapped q of g_min per tile position
   double* d_varm = nullptr;    // sigma != 0: variation multipliers [s][p][Kp][Np]
+  double* d_fcm_scratch = nullptr;  // FCM per-CTA node voltages / coefficients
+  size_t fcm_scratch_bytes = 0;
+  double* d_cache_d = nullptr;      // interp_fcm: distortion profile, g and converted g at refresh [s][p][Kp][Np]
+  double* d_cache_g = nullptr;
+  double* d_cache_gn = nullptr;
   unsigned long long* d_adc_tab = nullptr;  // T[k] = min column current n (units 2^-e) with code >= k
   double* d_master = nullptr;
   double* d_dW = nullptr;
@@ -168,7 +187,10 @@ void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st
 void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
 void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* d_dx, cudaStream_t st);
 void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
-void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st);
+void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only = false);
+void launch_fcm_regen(xbs_core* c, bool refresh_interp, cudaStream_t st);
+void launch_interp_apply(const xbs_core* c, cudaStream_t st);
+void ck_cuda(cudaError_t e, const char* what);  // throws the C-ABI error
 void launch_qmin(const xbs_core* c, cudaStream_t st);
 void launch_varm(const xbs_core* c, cudaStream_t st);
 void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);

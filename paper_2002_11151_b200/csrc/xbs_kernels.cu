@@ -242,7 +242,7 @@ __device__ __forceinline__ void st_vec(double* p, const double (&v)[JPT]) {
   *reinterpret_cast<typename VecT<JPT>::D*>(p) = t;
 }
 
-template <int S_T, int JPT, bool VAR, bool NL, bool NOISE, bool AAM>
+template <int S_T, int JPT, bool VAR, bool NL, bool NOISE, bool AAM, bool CONV = true>
 __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
                                                 double* __restrict__ master, uint8_t* __restrict__ digits,
                                                 DevScalars* sc, const uint32_t* __restrict__ qmin) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
       }
       double* mrow = master + size_t(i) * g.Np + j0;
       uint32_t qi[JPT];
-      if constexpr (!VAR) {
+      if constexpr (!VAR && CONV) {
         const typename VecT<JPT>::Q t =
             *reinterpret_cast<const typename VecT<JPT>::Q*>(qmin + size_t(r) * g.tile_cols + c0);
         qi[0] = t.x;
@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
           nu = nu < -range ? -range : nu;
           u[qs][jj] = nu;
           acc[jj] = acc[jj] * double(1u << g.db) + nu;
+          if constexpr (!CONV) continue;  // tile engines regenerate per tile afterwards
           const double rpath = AAM ? (rrow[jj] + rcol) + rp.r_sense : 0.0;
           const uint64_t idx = uint64_t(i) * g.Np + j0 + jj;
           if constexpr (VAR) {
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
           }
         }
         st_vec<JPT>(mrow + s * sstride, u[qs]);
+        if constexpr (!CONV) continue;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           typename VecT<JPT>::B w[4] = {0, 0, 0, 0};
@@ -408,7 +410,8 @@ __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, c
         if (nu < -range) nu = -range;
         *mp = nu;
         acc = acc * double(1u << g.db) + nu;
-        for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_q(rp, nu, s, p, idx, rpath));
+        if (digits)
+          for (int p = 0; p < 2; ++p) store_digits(digits, g, s, p, i, j, convert_q(rp, nu, s, p, idx, rpath));
       }
       wmax = fmax(wmax, fabs(up.wfactor * acc));
     }
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, c
 }
 
 template <int S, int JPT>
-static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st) {
+static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
   const dim3 grid((c->g.N / JPT + 255) / 256, std::min(c->g.K, 65535));
   const bool var = c->rp.sigma != 0.0, nl = !up.linear, noise = up.gamma != 0.0;
   // AAM with a zero path resistance everywhere is the identity conversion
@@ -431,7 +434,10 @@ static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st) 
     kern<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
   };
 #define XBS_UPD(V, N, A) go(k_update<S, JPT, V, N, N, A>)
-  if (aam) {
+  if (master_only) {
+    if (!nl && !noise) go(k_update<S, JPT, false, false, false, false, false>);
+    else go(k_update<S, JPT, false, true, true, false, false>);
+  } else if (aam) {
     if (!var && !nl && !noise) XBS_UPD(false, false, true);
     else if (var && !nl && !noise) XBS_UPD(true, false, true);
     else if (!var) XBS_UPD(false, true, true);
@@ -446,22 +452,23 @@ static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st) 
 }
 
 template <int JPT>
-static bool launch_update_j(const xbs_core* c, const UpdP& up, cudaStream_t st) {
+static bool launch_update_j(const xbs_core* c, const UpdP& up, cudaStream_t st, bool mo) {
   if (c->g.N % JPT || c->g.tile_cols % JPT || c->g.C % JPT) return false;
   switch (c->g.S) {
-    case 1: launch_update_s<1, JPT>(c, up, st); return true;
-    case 2: launch_update_s<2, JPT>(c, up, st); return true;
-    case 4: launch_update_s<4, JPT>(c, up, st); return true;
-    case 8: launch_update_s<8, JPT>(c, up, st); return true;
+    case 1: launch_update_s<1, JPT>(c, up, st, mo); return true;
+    case 2: launch_update_s<2, JPT>(c, up, st, mo); return true;
+    case 4: launch_update_s<4, JPT>(c, up, st, mo); return true;
+    case 8: launch_update_s<8, JPT>(c, up, st, mo); return true;
     default: return false;
   }
 }
 
-void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st) {
-  if (launch_update_j<4>(c, up, st)) return;
-  if (launch_update_j<2>(c, up, st)) return;
+void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
+  if (launch_update_j<4>(c, up, st, master_only)) return;
+  if (launch_update_j<2>(c, up, st, master_only)) return;
   const dim3 grid((c->g.N + 255) / 256, std::min(c->g.K, 65535));
-  k_update_any<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc);
+  k_update_any<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, master_only ? nullptr : c->d_digits,
+                                     c->d_sc);
 }
 
 // q(g_min) per tile position (sigma == 0 only): tile_rows x tile_cols

@@ -81,7 +81,7 @@ def test_nonfinite_and_empty_weights_rejected():
 @pytest.mark.parametrize(
     "mutate",
     [
-        lambda o: setattr(o, "engine", xb.EngineKind.fcm),  # FCM with parasitics: next row
+        lambda o: setattr(o, "engine", xb.EngineKind.oracle),  # dense nodal solve with parasitics (8f-4)
         lambda o: setattr(o.adc, "i_fs", 0.0),  # auto-calibration
         lambda o: setattr(o.adc, "transfer", [0.0, 1e-6, 2e-6, 3e-6]),
     ],
@@ -90,4 +90,14 @@ def test_out_of_scope_configs_fail_loudly(mutate):
     o = aam_options(tile=64)
     mutate(o)
     with pytest.raises(xb.ConfigError):
+        _create(o, np.zeros((8, 8)))
+
+
+@pytest.mark.parametrize("field,value", [("fcm_tol", 0.0), ("fcm_max_iter", 0)])
+def test_fcm_arguments_validated_before_any_device_work(field, value):
+    """fcm.cpp:170-173: bad FCM options raise std::invalid_argument."""
+    o = aam_options(tile=8)
+    o.engine = xb.EngineKind.fcm
+    setattr(o, field, value)
+    with pytest.raises(ValueError):
         _create(o, np.zeros((8, 8)))

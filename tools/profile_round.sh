@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
     --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k 'regex:k_fwd_tc|k_bwd_tc|k_dw_tc|k_update4' \
+ncu --set full --clock-control none --import-source on -k 'regex:k_fwd_tc|k_bwd_tc|k_dw_tc|k_update' \
     -s 12 -c 4 -o gpurun_out/prof_$CFG -f $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full capture rc=$?"
