@@ -89,6 +89,15 @@ struct CrossbarLayerOptions {
   }
 };
 
+namespace core_detail {
+struct CoreDeleter {
+  bool owns = true;  // false: a view of a core owned by a CrossbarConv2d
+  void operator()(xbs_core* c) const {
+    if (owns) xbs_core_destroy(c);
+  }
+};
+}  // namespace core_detail
+
 /// reference layers.hpp:49-111 (layers.cpp:68-391).
 class CrossbarCore {
  public:
@@ -98,6 +107,8 @@ class CrossbarCore {
     detail::check(xbs_core_create(&o, W0.data(), W0.rows(), W0.cols(), W0.rows() > 0 ? W0.rows() : 1, &h));
     h_.reset(h);
   }
+  /// View of a core owned by another object (CrossbarConv2d's core).
+  static CrossbarCore borrow(xbs_core* h) { return CrossbarCore(h); }
 
   MatrixXd forward(const MatrixXd& x, bool training) {
     MatrixXd y(x.rows(), out_features());
@@ -158,16 +169,14 @@ class CrossbarCore {
   xbs_core* handle() const { return h_.get(); }
 
  private:
-  struct Deleter {
-    void operator()(xbs_core* c) const { xbs_core_destroy(c); }
-  };
+  explicit CrossbarCore(xbs_core* borrowed) : h_(borrowed, core_detail::CoreDeleter{false}) {}
   static std::int64_t ld(const MatrixXd& m) { return m.rows() > 0 ? m.rows() : 1; }
   xbs_core_info info() const {
     xbs_core_info i{};
     detail::check(xbs_core_get_info(h_.get(), &i));
     return i;
   }
-  std::unique_ptr<xbs_core, Deleter> h_;
+  std::unique_ptr<xbs_core, core_detail::CoreDeleter> h_;
   mutable MatrixXd dW_, tile_;
   mutable bool grad_valid_ = false;
 };
@@ -205,6 +214,58 @@ class CrossbarLinear : public Layer {
 
  private:
   CrossbarCore core_;
+};
+
+/// reference layers.hpp:136-152 (layers.cpp:415-505): im2col lowering onto
+/// one core, done on the device; features ordered (c, y, x).
+class CrossbarConv2d : public Layer {
+ public:
+  CrossbarConv2d(const MatrixXd& W0, int in_c, int out_c, int kernel, int stride, int padding,
+                 const CrossbarLayerOptions& opt)
+      : h_(make(W0, in_c, out_c, kernel, stride, padding, opt)), core_(CrossbarCore::borrow(xbs_conv2d_core(h_.get()))) {}
+  Tensor forward(const Tensor& x, bool training) override {
+    if (x.dims.size() != 3) throw std::invalid_argument("CrossbarConv2d: expected (c, h, w) input");
+    std::int32_t oh = 0, ow = 0;
+    detail::check(xbs_conv2d_output_dims(h_.get(), x.dims[1], x.dims[2], &oh, &ow));
+    Tensor y;
+    y.values.resize(x.values.rows(), static_cast<MatrixXd::Index>(core_.out_features()) * oh * ow);
+    detail::check(xbs_conv2d_forward(h_.get(), x.values.data(), x.values.rows(), x.dims[0], x.dims[1], x.dims[2],
+                                     ld(x.values), training ? 1 : 0, y.values.data(), ld(y.values)));
+    y.dims = {core_.out_features(), oh, ow};
+    in_dims_ = x.dims;
+    return y;
+  }
+  Tensor backward(const Tensor& dy) override {
+    Tensor dx;
+    if (in_dims_.size() != 3) throw StateError("CrossbarConv2d::backward before forward");
+    dx.values.resize(dy.values.rows(), static_cast<MatrixXd::Index>(in_dims_[0]) * in_dims_[1] * in_dims_[2]);
+    detail::check(xbs_conv2d_backward(h_.get(), dy.values.data(), dy.values.rows(), ld(dy.values), dx.values.data(),
+                                      ld(dx.values)));
+    dx.dims = in_dims_;
+    return dx;
+  }
+  void apply_updates(std::uint64_t iteration) override { detail::check(xbs_conv2d_apply_updates(h_.get(), iteration)); }
+  CrossbarCore* core() override { return &core_; }
+  std::string name() const override { return "conv2d"; }
+
+ private:
+  struct Deleter {
+    void operator()(xbs_conv2d* c) const { xbs_conv2d_destroy(c); }
+  };
+  static xbs_conv2d* make(const MatrixXd& W0, int in_c, int out_c, int kernel, int stride, int padding,
+                          const CrossbarLayerOptions& opt) {
+    if (W0.rows() != static_cast<MatrixXd::Index>(in_c) * kernel * kernel || W0.cols() != out_c)
+      throw std::invalid_argument("CrossbarConv2d: kernel matrix must be (in_c*k*k) x out_c");
+    const xbs_layer_options o = opt.to_c();
+    xbs_conv2d* h = nullptr;
+    detail::check(xbs_conv2d_create(&o, W0.data(), W0.rows() > 0 ? W0.rows() : 1, in_c, out_c, kernel, stride, padding,
+                                    &h));
+    return h;
+  }
+  static std::int64_t ld(const MatrixXd& m) { return m.rows() > 0 ? m.rows() : 1; }
+  std::unique_ptr<xbs_conv2d, Deleter> h_;
+  CrossbarCore core_;
+  std::vector<int> in_dims_;
 };
 
 }  // namespace xbarsim::nn

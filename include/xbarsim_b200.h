@@ -158,6 +158,25 @@ void* xbs_core_stream(xbs_core* core);
  * to a private stream.  Waits for work queued on the previous stream. */
 int xbs_core_set_stream(xbs_core* core, void* stream);
 
+/* CrossbarConv2d (layers.hpp:136-152, layers.cpp:415-505): im2col lowering
+ * onto one core, on the device.  W0 is (in_c*kernel*kernel) x out_c
+ * column-major; tensors are batch x features column-major with features
+ * ordered (c, y, x).  Backward uses grad_divisor 1.0 and the reference's
+ * col2im summation order. */
+typedef struct xbs_conv2d xbs_conv2d;
+int xbs_conv2d_create(const xbs_layer_options* opt, const double* W0, int64_t ldw, int32_t in_c, int32_t out_c,
+                      int32_t kernel, int32_t stride, int32_t padding, xbs_conv2d** out);
+void xbs_conv2d_destroy(xbs_conv2d* conv);
+xbs_core* xbs_conv2d_core(xbs_conv2d* conv);  /* borrowed; owned by the conv */
+int xbs_conv2d_output_dims(xbs_conv2d* conv, int32_t h, int32_t w, int32_t* out_h, int32_t* out_w);
+int xbs_conv2d_forward(xbs_conv2d* conv, const double* x, int64_t batch, int32_t c, int32_t h, int32_t w, int64_t ldx,
+                       int32_t training, double* y, int64_t ldy);
+int xbs_conv2d_backward(xbs_conv2d* conv, const double* dy, int64_t batch, int64_t lddy, double* dx, int64_t lddx);
+int xbs_conv2d_forward_device(xbs_conv2d* conv, const double* d_x, int64_t batch, int32_t c, int32_t h, int32_t w,
+                              int32_t training, double* d_y);
+int xbs_conv2d_backward_device(xbs_conv2d* conv, const double* d_dy, int64_t batch, double* d_dx);
+int xbs_conv2d_apply_updates(xbs_conv2d* conv, uint64_t iteration);
+
 /* Per-stage device timing (CUDA events recorded on the core's stream around
  * each stage while enabled).  Stages: 0 prep_x (K0a), 1 forward VMM (K1),
  * 2 prep_dy (K0b), 3 dW (K3a), 4 backward VMM (K2), 5 update+regeneration

@@ -62,6 +62,13 @@ def lib():
         L.orc_aam_convert.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_double] * 4 + [_D, _D]
         L.orc_calibrate.argtypes = [_D, ctypes.c_long, ctypes.c_double]
         L.orc_calibrate.restype = ctypes.c_double
+        L.orc_conv2d_create.argtypes = [ctypes.c_void_p, ctypes.c_int, _D, ctypes.c_long, ctypes.c_long] + \
+            [ctypes.c_int] * 5 + [ctypes.POINTER(ctypes.c_void_p)]
+        L.orc_conv2d_destroy.argtypes = [ctypes.c_void_p]
+        L.orc_conv2d_forward.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, _D, ctypes.POINTER(ctypes.c_int)]
+        L.orc_conv2d_backward.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_long, _D]
+        L.orc_conv2d_apply_updates.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
     return _lib
 
 
@@ -183,6 +190,42 @@ class OracleCore:
         out = np.zeros(n, dtype=np.uint16)
         lib().orc_core_last_codes(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), n)
         return out
+
+
+class OracleConv2d:
+    """CrossbarConv2d restated (layers.cpp:415-505); x: batch x (c*h*w)."""
+
+    def __init__(self, W0, in_c, out_c, kernel, stride, padding, opt, snapped: bool = True):
+        W = _f(W0)
+        self._copt = opt.to_c()
+        h = ctypes.c_void_p()
+        _check(lib().orc_conv2d_create(ctypes.byref(self._copt), int(snapped), _p(W), W.shape[0], W.shape[1], in_c,
+                                       out_c, kernel, stride, padding, ctypes.byref(h)))
+        self._h = h
+        self._feat_in = None
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_conv2d_destroy(self._h)
+            self._h = None
+
+    def forward(self, x, c, h, w, training=False):
+        x = _f(x)
+        dims = (ctypes.c_int * 3)()
+        _check(lib().orc_conv2d_forward(self._h, _p(x), x.shape[0], c, h, w, int(training), None, dims))
+        y = np.zeros((x.shape[0], dims[0] * dims[1] * dims[2]), order="F")
+        _check(lib().orc_conv2d_forward(self._h, _p(x), x.shape[0], c, h, w, int(training), _p(y), dims))
+        self._feat_in = c * h * w
+        return y, tuple(dims)
+
+    def backward(self, dy):
+        dy = _f(dy)
+        dx = np.zeros((dy.shape[0], self._feat_in), order="F")
+        _check(lib().orc_conv2d_backward(self._h, _p(dy), dy.shape[0], dy.shape[1], _p(dx)))
+        return dx
+
+    def apply_updates(self, it):
+        _check(lib().orc_conv2d_apply_updates(self._h, it))
 
 
 def rng_draws(seed, a, b, c, n):

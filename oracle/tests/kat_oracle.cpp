@@ -1378,4 +1378,34 @@ TEST_CASE("distortion: applying a stored profile to an updated tile scales it") 
   for (size_t k = 0; k < g.v.size(); ++k) CHECK(approx.v[k] == Approx(moved.v[k] * (1.0 - cache.d.v[k])).epsilon(1e-15));
 }
 
+
+TEST_CASE("conv2d lowers to the dense pipeline and matches direct convolution") {  // test_nn.cpp:399-430
+  std::mt19937_64 rng(11);
+  const int in_c = 2, out_c = 3, k = 3, h = 6, w = 6;
+  Matrix K = random_matrix(in_c * k * k, out_c, rng, 0.5);
+  auto opt = ideal_options(in_c * k * k, out_c, 16);
+  opt.act_bits = 16;
+  opt.error_bits = 16;
+  CrossbarConv2d conv(K, in_c, out_c, k, 1, 0, opt);
+  Tensor x;
+  x.dims = {in_c, h, w};
+  x.values = random_matrix(2, in_c * h * w, rng, 1.0);
+  for (double& v : x.values.v) v = std::fabs(v);
+  Tensor y = conv.forward(x, false);
+  REQUIRE(y.dims == std::vector<int>({out_c, 4, 4}));
+  Matrix kq = ref_quantize_weights(K, 16, 1.0);
+  Matrix xq = ref_quantize_acts(x.values, 16, 1.0);
+  for (int b = 0; b < 2; ++b)
+    for (int oc = 0; oc < out_c; ++oc)
+      for (int oy = 0; oy < 4; ++oy)
+        for (int ox = 0; ox < 4; ++ox) {
+          double acc = 0.0;
+          for (int c = 0; c < in_c; ++c)
+            for (int ky = 0; ky < k; ++ky)
+              for (int kx = 0; kx < k; ++kx)
+                acc += xq(b, (c * h + oy + ky) * w + ox + kx) * kq((c * k + ky) * k + kx, oc);
+          CHECK(y.values(b, (oc * 4 + oy) * 4 + ox) == Approx(acc).epsilon(1e-12));
+        }
+}
+
 MT_MAIN

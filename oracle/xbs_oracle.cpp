@@ -1157,6 +1157,79 @@ void CrossbarCore::apply_updates(uint64_t iteration) {
 }
 
 // layers.cpp:397-409
+// layers.cpp:415-429
+CrossbarConv2d::CrossbarConv2d(const Matrix& W0, int in_c, int out_c, int kernel, int stride, int padding,
+                               const CrossbarLayerOptions& opt)
+    : core_(W0, opt), in_c_(in_c), out_c_(out_c), kernel_(kernel), stride_(stride), padding_(padding) {
+  if (W0.rows != long(in_c) * kernel * kernel || W0.cols != out_c)
+    throw std::invalid_argument("CrossbarConv2d: kernel matrix must be (in_c*k*k) x out_c");
+  if (stride < 1 || kernel < 1 || padding < 0) throw std::invalid_argument("CrossbarConv2d: bad geometry");
+}
+
+// layers.cpp:431-469: im2col (one row per output position per sample), the
+// dense pipeline, then (b, oc, oy, ox) order
+Tensor CrossbarConv2d::forward(const Tensor& x, bool training) {
+  if (x.dims.size() != 3 || x.dims[0] != in_c_) throw std::invalid_argument("CrossbarConv2d: expected (c, h, w) input");
+  in_h_ = x.dims[1];
+  in_w_ = x.dims[2];
+  out_h_ = (in_h_ + 2 * padding_ - kernel_) / stride_ + 1;
+  out_w_ = (in_w_ + 2 * padding_ - kernel_) / stride_ + 1;
+  if (out_h_ < 1 || out_w_ < 1) throw std::invalid_argument("CrossbarConv2d: kernel does not fit the input");
+  batch_ = x.values.rows;
+  const long rows = batch_ * out_h_ * out_w_;
+  Matrix patches(rows, long(in_c_) * kernel_ * kernel_, 0.0);
+  for (long b = 0; b < batch_; ++b)
+    for (int oy = 0; oy < out_h_; ++oy)
+      for (int ox = 0; ox < out_w_; ++ox) {
+        const long r = (b * out_h_ + oy) * out_w_ + ox;
+        for (int c = 0; c < in_c_; ++c)
+          for (int ky = 0; ky < kernel_; ++ky)
+            for (int kx = 0; kx < kernel_; ++kx) {
+              const int iy = oy * stride_ + ky - padding_, ix = ox * stride_ + kx - padding_;
+              if (iy < 0 || iy >= in_h_ || ix < 0 || ix >= in_w_) continue;
+              patches(r, (c * kernel_ + ky) * kernel_ + kx) = x.values(b, (long(c) * in_h_ + iy) * in_w_ + ix);
+            }
+      }
+  const Matrix flat = core_.forward(patches, training);
+  Tensor y;
+  y.dims = {out_c_, out_h_, out_w_};
+  y.values = Matrix(batch_, long(out_c_) * out_h_ * out_w_);
+  for (long b = 0; b < batch_; ++b)
+    for (int oc = 0; oc < out_c_; ++oc)
+      for (int oy = 0; oy < out_h_; ++oy)
+        for (int ox = 0; ox < out_w_; ++ox)
+          y.values(b, (long(oc) * out_h_ + oy) * out_w_ + ox) = flat((b * out_h_ + oy) * out_w_ + ox, oc);
+  return y;
+}
+
+// layers.cpp:471-500: col2im accumulates in (b, oy, ox, c, ky, kx) order
+Tensor CrossbarConv2d::backward(const Tensor& dy) {
+  const long rows = batch_ * out_h_ * out_w_;
+  Matrix flat(rows, out_c_);
+  for (long b = 0; b < batch_; ++b)
+    for (int oc = 0; oc < out_c_; ++oc)
+      for (int oy = 0; oy < out_h_; ++oy)
+        for (int ox = 0; ox < out_w_; ++ox)
+          flat((b * out_h_ + oy) * out_w_ + ox, oc) = dy.values(b, (long(oc) * out_h_ + oy) * out_w_ + ox);
+  const Matrix dp = core_.backward(flat, 1.0);
+  Tensor dx;
+  dx.dims = {in_c_, in_h_, in_w_};
+  dx.values = Matrix(batch_, long(in_c_) * in_h_ * in_w_, 0.0);
+  for (long b = 0; b < batch_; ++b)
+    for (int oy = 0; oy < out_h_; ++oy)
+      for (int ox = 0; ox < out_w_; ++ox) {
+        const long r = (b * out_h_ + oy) * out_w_ + ox;
+        for (int c = 0; c < in_c_; ++c)
+          for (int ky = 0; ky < kernel_; ++ky)
+            for (int kx = 0; kx < kernel_; ++kx) {
+              const int iy = oy * stride_ + ky - padding_, ix = ox * stride_ + kx - padding_;
+              if (iy < 0 || iy >= in_h_ || ix < 0 || ix >= in_w_) continue;
+              dx.values(b, (long(c) * in_h_ + iy) * in_w_ + ix) += dp(r, (c * kernel_ + ky) * kernel_ + kx);
+            }
+      }
+  return dx;
+}
+
 Tensor CrossbarLinear::forward(const Tensor& x, bool training) {
   Tensor y;
   y.values = core_.forward(x.values, training);

@@ -375,6 +375,22 @@ class CrossbarLinear {  // layers.cpp:393-413
   CrossbarCore core_;
 };
 
+class CrossbarConv2d {  // layers.cpp:415-505 (im2col lowering onto one core)
+ public:
+  CrossbarConv2d(const Matrix& W0, int in_c, int out_c, int kernel, int stride, int padding,
+                 const CrossbarLayerOptions& opt);
+  Tensor forward(const Tensor& x, bool training);
+  Tensor backward(const Tensor& dy);
+  void apply_updates(uint64_t iteration) { core_.apply_updates(iteration); }
+  CrossbarCore* core() { return &core_; }
+
+ private:
+  CrossbarCore core_;
+  int in_c_, out_c_, kernel_, stride_, padding_;
+  int in_h_ = 0, in_w_ = 0, out_h_ = 0, out_w_ = 0;
+  long batch_ = 0;
+};
+
 // train.cpp:11-33
 double softmax_cross_entropy(const Matrix& logits, const std::vector<int>& labels, Matrix& dlogits);
 

@@ -129,6 +129,38 @@ int orc_core_create(const orc_options* o, int snapped, const double* W, long K, 
 }
 void orc_core_destroy(void* h) { delete static_cast<orc::CrossbarCore*>(h); }
 
+// CrossbarConv2d (layers.cpp:415-505); x: batch x (c*h*w) column-major
+int orc_conv2d_create(const orc_options* o, int snapped, const double* W, long K, long N, int in_c, int out_c,
+                      int kernel, int stride, int padding, void** out) {
+  return guard([&] {
+    *out = new orc::CrossbarConv2d(wrap(W, K, N), in_c, out_c, kernel, stride, padding, to_opts(o, snapped));
+  });
+}
+void orc_conv2d_destroy(void* h) { delete static_cast<orc::CrossbarConv2d*>(h); }
+int orc_conv2d_forward(void* h, const double* x, long batch, int c, int hh, int ww, int training, double* y,
+                       int* dims3) {
+  return guard([&] {
+    orc::Tensor t;
+    t.values = wrap(x, batch, long(c) * hh * ww);
+    t.dims = {c, hh, ww};
+    orc::Tensor r = static_cast<orc::CrossbarConv2d*>(h)->forward(t, training != 0);
+    for (int k = 0; k < 3; ++k) dims3[k] = r.dims[size_t(k)];
+    if (y) unwrap(r.values, y);
+  });
+}
+int orc_conv2d_backward(void* h, const double* dy, long batch, long feat, double* dx) {
+  return guard([&] {
+    orc::Tensor t;
+    t.values = wrap(dy, batch, feat);
+    unwrap(static_cast<orc::CrossbarConv2d*>(h)->backward(t).values, dx);
+  });
+}
+int orc_conv2d_apply_updates(void* h, uint64_t it) {
+  return guard([&] { static_cast<orc::CrossbarConv2d*>(h)->apply_updates(it); });
+}
+void* orc_conv2d_core(void* h) { return static_cast<orc::CrossbarConv2d*>(h)->core(); }
+
+
 static orc::CrossbarCore* C(void* h) { return static_cast<orc::CrossbarCore*>(h); }
 
 int orc_core_forward(void* h, const double* x, long M, long K, int training, double* y) {

@@ -8,15 +8,21 @@ from . import xbarsim  # noqa: F401
 from .xbarsim import (  # noqa: F401
     AdcSpec,
     ConfigError,
+    ConvergenceError,
     CrossbarConfig,
+    CrossbarConv2d,
     CrossbarCore,
     CrossbarLayerOptions,
     CrossbarLinear,
     DacSpec,
     EngineKind,
+    Flatten,
     MappingSpec,
+    MaxPool2d,
     Polarity,
+    ReLU,
     StateError,
     Tensor,
     UpdateSpec,
+    softmax_cross_entropy,
 )

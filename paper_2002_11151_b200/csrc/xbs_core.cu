@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -375,6 +376,18 @@ void finish_update_stats(xbs_core* c) {
 }
 
 }  // namespace
+
+namespace xbs {  // error plumbing shared with the conv layer (xbs_conv.cu)
+int set_error(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+void fail_conv(int code, const std::string& m) { fail(code, m); }
+void check_rc(int rc) {
+  if (rc != XBS_OK) throw XbsError(rc, g_err);
+}
+int guard_conv(const std::function<void()>& f) { return guard(f); }
+}  // namespace xbs
 
 extern "C" {
 

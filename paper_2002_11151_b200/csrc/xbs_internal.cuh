@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -191,6 +192,10 @@ void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st, bool mast
 void launch_fcm_regen(xbs_core* c, bool refresh_interp, cudaStream_t st);
 void launch_interp_apply(const xbs_core* c, cudaStream_t st);
 void ck_cuda(cudaError_t e, const char* what);  // throws the C-ABI error
+int set_error(int code, const std::string& m);   // sets xbs_last_error, returns code
+[[noreturn]] void fail_conv(int code, const std::string& m);
+void check_rc(int rc);                            // rethrows a C-ABI status
+int guard_conv(const std::function<void()>& f);   // runs f, mapping exceptions to statuses
 void launch_qmin(const xbs_core* c, cudaStream_t st);
 void launch_varm(const xbs_core* c, cudaStream_t st);
 void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);

@@ -249,6 +249,19 @@ SYMBOLS = {
     "xbs_core_select_kernel": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stream": (_P, [_P]),
     "xbs_core_set_stream": (ctypes.c_int, [_P, _P]),
+    "xbs_conv2d_create": (ctypes.c_int, [_P, _D, _I64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_int32, _P]),
+    "xbs_conv2d_destroy": (None, [_P]),
+    "xbs_conv2d_core": (_P, [_P]),
+    "xbs_conv2d_output_dims": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                              ctypes.POINTER(ctypes.c_int32)]),
+    "xbs_conv2d_forward": (ctypes.c_int, [_P, _D, _I64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I64,
+                                          ctypes.c_int32, _D, _I64]),
+    "xbs_conv2d_backward": (ctypes.c_int, [_P, _D, _I64, _I64, _D, _I64]),
+    "xbs_conv2d_forward_device": (ctypes.c_int, [_P, _P, _I64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int32, _P]),
+    "xbs_conv2d_backward_device": (ctypes.c_int, [_P, _P, _I64, _P]),
+    "xbs_conv2d_apply_updates": (ctypes.c_int, [_P, ctypes.c_uint64]),
     "xbs_core_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(_I64), ctypes.c_int32]),
     "xbs_core_launch_count": (_I64, [_P]),
@@ -305,9 +318,18 @@ class CrossbarCore:
         self._h = h
         self._K, self._N = W.shape
 
+    @classmethod
+    def _view(cls, handle, K: int, N: int, opt: CrossbarLayerOptions, owner) -> "CrossbarCore":
+        """Non-owning view of a core owned by another object (a conv layer)."""
+        core = cls.__new__(cls)
+        core._opt, core._copt = opt, opt.to_c()
+        core._h, core._K, core._N = handle, K, N
+        core._owner = owner  # keeps the owner (and the handle) alive
+        return core
+
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib is not None:
+        if h and _lib is not None and getattr(self, "_owner", None) is None:
             _lib.xbs_core_destroy(h)
             self._h = None
 
@@ -488,3 +510,144 @@ class CrossbarLinear(Layer):
 
     def name(self) -> str:
         return "linear"
+
+
+class CrossbarConv2d(Layer):
+    """layers.hpp:136-152, layers.cpp:415-505: im2col lowering onto one core,
+    on the device (xbs_conv2d_*).  W0 is (in_c*kernel*kernel) x out_c."""
+
+    def __init__(self, W0: np.ndarray, in_c: int, out_c: int, kernel: int, stride: int, padding: int,
+                 opt: CrossbarLayerOptions):
+        lib = load_library()
+        W = _fortran(W0)
+        if W.ndim != 2 or W.shape[0] != in_c * kernel * kernel or W.shape[1] != out_c:
+            raise ValueError("CrossbarConv2d: kernel matrix must be (in_c*k*k) x out_c")
+        self._copt = opt.to_c()
+        h = ctypes.c_void_p()
+        _check(lib.xbs_conv2d_create(ctypes.byref(self._copt), _ptr(W), max(1, W.shape[0]), in_c, out_c, kernel, stride,
+                                     padding, ctypes.byref(h)))
+        self._h = h
+        self.in_c, self.out_c = in_c, out_c
+        self._core = CrossbarCore._view(lib.xbs_conv2d_core(h), W.shape[0], out_c, opt, self)
+        self._in_dims = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.xbs_conv2d_destroy(h)
+            self._h = None
+
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        if len(x.dims) != 3 or x.dims[0] != self.in_c:
+            raise ValueError("CrossbarConv2d: expected (c, h, w) input")
+        c, hh, ww = x.dims
+        oh, ow = ctypes.c_int32(), ctypes.c_int32()
+        _check(load_library().xbs_conv2d_output_dims(self._h, hh, ww, ctypes.byref(oh), ctypes.byref(ow)))
+        v = _fortran(x.values)
+        b = v.shape[0]
+        y = np.zeros((b, self.out_c * oh.value * ow.value), order="F")
+        _check(load_library().xbs_conv2d_forward(self._h, _ptr(v), b, c, hh, ww, max(1, b), int(bool(training)), _ptr(y),
+                                                 max(1, b)))
+        self._in_dims = list(x.dims)
+        return Tensor(y, [self.out_c, oh.value, ow.value])
+
+    def backward(self, dy: Tensor) -> Tensor:
+        v = _fortran(dy.values)
+        b = v.shape[0]
+        c, hh, ww = self._in_dims if self._in_dims else (self.in_c, 0, 0)
+        dx = np.zeros((b, c * hh * ww), order="F")
+        _check(load_library().xbs_conv2d_backward(self._h, _ptr(v), b, max(1, b), _ptr(dx), max(1, b)))
+        return Tensor(dx, [c, hh, ww])
+
+    def apply_updates(self, iteration: int) -> None:
+        _check(load_library().xbs_conv2d_apply_updates(self._h, int(iteration)))
+
+    def core(self) -> CrossbarCore:
+        return self._core
+
+    def name(self) -> str:
+        return "conv2d"
+
+
+# ---- host-side step glue of the reference (layers.cpp:507-587, train.cpp:11-33);
+# not on the crossbar path, kept with the reference's exact semantics so a
+# Network of these layers steps like the reference's.
+class ReLU(Layer):
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        self._mask = (x.values > 0.0).astype(np.float64)
+        return Tensor(x.values * self._mask, list(x.dims), x.bits, x.full_scale)
+
+    def backward(self, dy: Tensor) -> Tensor:
+        return Tensor(dy.values * self._mask, list(dy.dims), dy.bits, dy.full_scale)
+
+    def name(self) -> str:
+        return "relu"
+
+
+class MaxPool2d(Layer):
+    def __init__(self, kernel: int, stride: int):
+        if kernel < 1 or stride < 1:
+            raise ValueError("MaxPool2d: bad kernel/stride")
+        self.kernel, self.stride = kernel, stride
+
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        if len(x.dims) != 3:
+            raise ValueError("MaxPool2d: expected (c, h, w)")
+        c, h, w = x.dims
+        k, s = self.kernel, self.stride
+        oh, ow = (h - k) // s + 1, (w - k) // s + 1
+        v = x.values.reshape(x.values.shape[0], c, h, w)
+        best = np.full((v.shape[0], c, oh, ow), -np.inf)
+        arg = np.zeros((v.shape[0], c, oh, ow), dtype=np.int64)
+        for ky in range(k):  # strict '>' keeps the first maximum in (ky, kx) order
+            for kx in range(k):
+                cand = v[:, :, ky:ky + s * (oh - 1) + 1:s, kx:kx + s * (ow - 1) + 1:s]
+                idx = (np.arange(c)[None, :, None, None] * h + (np.arange(oh)[None, None, :, None] * s + ky)) * w + \
+                      (np.arange(ow)[None, None, None, :] * s + kx)
+                upd = cand > best
+                best = np.where(upd, cand, best)
+                arg = np.where(upd, idx, arg)
+        self._arg, self._in = arg.reshape(arg.shape[0], -1), (list(x.dims), x.values.shape[1])
+        return Tensor(best.reshape(best.shape[0], -1), [c, oh, ow])
+
+    def backward(self, dy: Tensor) -> Tensor:
+        dims, feat = self._in
+        dx = np.zeros((dy.values.shape[0], feat))
+        for b in range(dx.shape[0]):
+            np.add.at(dx[b], self._arg[b], dy.values[b])
+        return Tensor(dx, dims)
+
+    def name(self) -> str:
+        return "maxpool2d"
+
+
+class Flatten(Layer):
+    def forward(self, x: Tensor, training: bool) -> Tensor:
+        self._dims = list(x.dims)
+        return Tensor(x.values, [x.values.shape[1]], x.bits, x.full_scale)
+
+    def backward(self, dy: Tensor) -> Tensor:
+        return Tensor(dy.values, list(self._dims), dy.bits, dy.full_scale)
+
+    def name(self) -> str:
+        return "flatten"
+
+
+def softmax_cross_entropy(logits: np.ndarray, labels) -> "tuple[float, np.ndarray]":
+    """train.cpp:11-33: mean loss and dlogits (same expression order)."""
+    n, _ = logits.shape
+    if len(labels) != n:
+        raise ValueError("softmax_cross_entropy: label count mismatch")
+    d = np.zeros_like(logits)
+    total = 0.0
+    for i in range(n):
+        row = logits[i]
+        m = row.max()
+        z = 0.0
+        for v in row:
+            z += np.exp(v - m)
+        y = int(labels[i])
+        total += -(row[y] - m - np.log(z))
+        for j, v in enumerate(row):
+            d[i, j] = (np.exp(v - m) / z - (1.0 if j == y else 0.0)) / float(n)
+    return total / float(n), d

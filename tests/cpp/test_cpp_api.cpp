@@ -23,6 +23,13 @@ int orc_core_gradient(void* h, double* out);
 int orc_core_set_nonideal(void* h, int s, int p, int t, const double* g);
 int orc_core_master(void* h, int s, double* u);
 int orc_core_apply_updates(void* h, uint64_t it);
+int orc_conv2d_create(const void* o, int snapped, const double* W, long K, long N, int in_c, int out_c, int k,
+                      int stride, int pad, void** out);
+void orc_conv2d_destroy(void* h);
+int orc_conv2d_forward(void* h, const double* x, long batch, int c, int hh, int ww, int training, double* y,
+                       int* dims3);
+int orc_conv2d_backward(void* h, const double* dy, long batch, long feat, double* dx);
+int orc_conv2d_apply_updates(void* h, uint64_t it);
 }
 
 using xbarsim::MatrixXd;
@@ -156,10 +163,55 @@ static void gpu_cases() {
   orc_core_destroy(orc);
 }
 
+// CrossbarConv2d through the C++ API (test_nn.cpp's conv cases use the same
+// calls): y, dx, dW bit-exact against the oracle's conv over two steps.
+static void gpu_conv_cases() {
+  const int in_c = 3, out_c = 8, k = 3, stride = 2, pad = 1, H = 9, Wd = 7;
+  const long B = 2;
+  const CrossbarLayerOptions o = aam_options();
+  const MatrixXd W = seeded(in_c * k * k, out_c, 5, -0.2, 0.2);
+  CHECK(throws<std::invalid_argument>([&] { CrossbarConv2d bad(W, in_c, out_c + 1, k, stride, pad, o); }));
+  CrossbarConv2d conv(W, in_c, out_c, k, stride, pad, o);
+  CHECK(conv.name() == "conv2d");
+  CHECK(conv.core()->in_features() == in_c * k * k);
+  const xbs_layer_options co = o.to_c();
+  void* orc = nullptr;
+  CHECK(orc_conv2d_create(&co, 1, W.data(), W.rows(), W.cols(), in_c, out_c, k, stride, pad, &orc) == 0);
+  Tensor x;
+  x.values = seeded(B, in_c * H * Wd, 6, -0.3, 1.1);
+  x.dims = {in_c, H, Wd};
+  for (int it = 0; it < 2; ++it) {
+    const Tensor y = conv.forward(x, true);
+    int dims[3] = {0, 0, 0};
+    MatrixXd y_o(B, y.values.cols());
+    CHECK(orc_conv2d_forward(orc, x.values.data(), B, in_c, H, Wd, 1, y_o.data(), dims) == 0);
+    CHECK(y.dims.size() == 3 && y.dims[0] == dims[0] && y.dims[1] == dims[1] && y.dims[2] == dims[2]);
+    CHECK(y.values == y_o);
+    Tensor dy;
+    dy.values = seeded(B, y.values.cols(), 7 + it, -1.0, 1.0);
+    dy.dims = y.dims;
+    const Tensor dx = conv.backward(dy);
+    MatrixXd dx_o(B, x.values.cols());
+    CHECK(orc_conv2d_backward(orc, dy.values.data(), B, dy.values.cols(), dx_o.data()) == 0);
+    CHECK(dx.values == dx_o);
+    CHECK(dx.dims == x.dims);
+    conv.apply_updates(it);
+    CHECK(orc_conv2d_apply_updates(orc, it) == 0);
+  }
+  Tensor bad;
+  bad.values = MatrixXd(B, 2 * H * Wd);
+  bad.dims = {2, H, Wd};
+  CHECK(throws<std::invalid_argument>([&] { conv.forward(bad, false); }));
+  orc_conv2d_destroy(orc);
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   cpu_cases();
-  if (mode == "gpu") gpu_cases();
+  if (mode == "gpu") {
+    gpu_cases();
+    gpu_conv_cases();
+  }
   std::printf("%s: %d failure(s)\n", mode.c_str(), failures);
   return failures == 0 ? 0 : 1;
 }
