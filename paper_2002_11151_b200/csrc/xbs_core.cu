@@ -139,8 +139,6 @@ void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, 
     if (o.fcm_max_iter < 1) fail(XBS_INVALID_ARGUMENT, "fcm_convert: max_iter must be >= 1");
   }
   if (o.engine < 0 || o.engine > 4) fail(XBS_INVALID_ARGUMENT, "unknown engine");
-  if (o.adc_bits > 0 && adc_tr.empty() && !(o.adc_i_fs > 0))
-    fail(XBS_UNSUPPORTED, "ADC auto-calibration (adc.i_fs <= 0) is not on this path: pin adc.i_fs (SURVEY §8f-3)");
   if (!adc_tr.empty()) fail(XBS_UNSUPPORTED, "ADC transfer tables are not on this path");
   if (!dac_tr.empty()) fail(XBS_UNSUPPORTED, "DAC transfer tables are not on this path");
   if (o.adc_bits > 16) fail(XBS_UNSUPPORTED, "adc.bits > 16 is not on this path");
@@ -297,9 +295,74 @@ void collect_stage_times(xbs_core* c) {
   c->pending.clear();
 }
 
+// Quantising ADC with full scale i_fs for one direction (0 forward, 1
+// backward): converters.cpp:79-87 on the snapped current I = n 2^sh is
+// monotone in n, so T[k] = min{n : code(n) >= k} decides every code exactly;
+// the tcgen05 epilogues use it for the boundary cases.
+void set_adc(xbs_core* c, int dir, double i_fs) {
+  xbs::AdcP& a = dir == 0 ? c->adc : c->adc_b;
+  unsigned long long*& tab = dir == 0 ? c->d_adc_tab : c->d_adc_tab_b;
+  a.passthrough = 0;
+  a.i_fs = i_fs;
+  const double fac = i_fs / (std::pow(2.0, c->opt.adc_bits) - 1.0);
+  (dir == 0 ? c->ifs_fac : c->ifs_fac_b) = fac;
+  if (tab) {
+    sync(c);
+    cudaFree(tab);
+    tab = nullptr;
+  }
+  if (!(i_fs > 0)) return;  // calibrated without observations: adc_quantize throws on use
+  auto code = [&](uint64_t n) {
+    const double scaled = std::ldexp(double(n), a.sh) / a.i_fs * a.maxc_d;
+    return scaled >= a.maxc_d ? int64_t(a.maxc) : int64_t(std::llround(scaled));
+  };
+  std::vector<unsigned long long> T(size_t(a.maxc) + 1, 0ull);
+  const uint64_t top = uint64_t(1) << 44;  // > 65025^2 * 256 >= any column current
+  for (int k = 1; k <= a.maxc; ++k) {
+    uint64_t lo = k > 1 ? T[size_t(k) - 1] : 0, hi = top;
+    if (code(hi) < k) {
+      T[size_t(k)] = top;
+      continue;
+    }
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if (code(mid) >= k) hi = mid;
+      else lo = mid + 1;
+    }
+    T[size_t(k)] = lo;
+  }
+  ck(cudaMalloc(&tab, T.size() * 8), "cudaMalloc adc table");
+  ck(cudaMemcpy(tab, T.data(), T.size() * 8, cudaMemcpyHostToDevice), "H2D adc table");
+}
+
+// layers.cpp:189-197: after adc_cal_batches training forwards, each
+// direction's i_fs becomes the nearest-rank clip_percentile quantile of the
+// currents it observed (converters.cpp:96-107), chosen on the device by an
+// exact radix select over the recorded n.
+void maybe_freeze_adc(xbs_core* c) {
+  if (!c->adc_auto || c->adc_frozen) return;
+  if (c->training_batches < c->opt.adc_cal_batches) return;
+  double ifs[2] = {0.0, 0.0};  // adc.i_fs as configured (<= 0) stays "unset"
+  for (int dir = 0; dir < 2; ++dir) {
+    uint64_t n = 0;
+    ifs[dir] = xbs::calib_select(c, dir, c->opt.adc_clip_percentile, &n) ? std::ldexp(double(n), c->adc.sh)
+                                                                         : c->opt.adc_i_fs;
+  }
+  xbs::calib_release(c);
+  c->adc_frozen = true;
+  set_adc(c, 0, ifs[0]);
+  set_adc(c, 1, ifs[1]);
+  c->adc_scaled = true;
+  c->k_out_fwd = c->sx * c->F / c->vu * c->ifs_fac;  // layers.cpp:278-281
+}
+
+bool calibrating(const xbs_core* c) { return c->adc_auto && !c->adc_frozen; }
+
 void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y) {
-  (void)training;  // training only feeds ADC auto-calibration (out of scope)
   if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
+  maybe_freeze_adc(c);
+  if (c->adc_auto && c->adc_frozen && !(c->adc.i_fs > 0) && M > 0)
+    fail(XBS_STATE_ERROR, "adc_quantize: i_fs not set (calibrate first)");  // converters.cpp:83-84
   ensure_batch(c, std::max<int64_t>(M, 1));
   {
     StageScope st(c, XBS_STAGE_PREP_X);
@@ -308,7 +371,9 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, do
   }
   c->have_forward = true;
   c->M_fwd = M;
+  if (training) ++c->training_batches;  // layers.cpp:224
   if (M == 0) return;
+  if (calibrating(c) && training) xbs::calib_observe_fwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_FWD);
   c->launches += 1;
   if (c->fully_ideal) {
@@ -321,6 +386,7 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, do
 void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
   if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
   if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
+  maybe_freeze_adc(c);
   {
     StageScope st(c, XBS_STAGE_PREP_DY);
     xbs::launch_prep_dy(c, d_dy, M, c->stream);
@@ -333,6 +399,14 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, doub
   }
   c->have_grad = true;
   if (M == 0) return;
+  if (c->adc_auto && c->adc_frozen && !(c->adc_b.i_fs > 0)) {
+    double se = 0.0;  // layers.cpp:308: a zero error never reaches the ADC
+    ck(cudaMemcpyAsync(&c->h_sc->se, &c->d_sc->se, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H se");
+    sync(c);
+    se = c->h_sc->se;
+    if (se > 0) fail(XBS_STATE_ERROR, "adc_quantize: i_fs not set (calibrate first)");
+  }
+  if (calibrating(c)) xbs::calib_observe_bwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_BWD);
   c->launches += 1;
   if (c->fully_ideal) {
@@ -520,55 +594,32 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     c->F = F;
     c->sx = o.act_full_scale / double((1 << o.act_bits) - 1);  // tensor.cpp:29 (codes_to_values)
     c->lev_e = std::pow(2.0, o.error_bits) - 1.0;
-    c->adc_scaled = o.adc_bits > 0 && c->adc_tr.empty();  // frozen or explicit (no auto-cal on this path)
+    c->adc_auto = o.adc_bits > 0 && !(o.adc_i_fs > 0) && c->adc_tr.empty();  // layers.cpp:74
+    c->adc_scaled = o.adc_bits > 0 && c->adc_tr.empty() && !c->adc_auto;      // layers.cpp:280
     c->ifs_fac = c->adc_scaled ? o.adc_i_fs / (std::pow(2.0, o.adc_bits) - 1.0) : 1.0;
+    c->ifs_fac_b = c->ifs_fac;
     double k_out = sx * F / vu;
     if (c->adc_scaled) k_out *= c->ifs_fac;
     c->k_out_fwd = k_out;
 
     xbs::AdcP& a = c->adc;
-    a.passthrough = o.adc_bits == 0;
+    a.passthrough = o.adc_bits == 0 || c->adc_auto;  // calibration batches pass currents through
     a.maxc = o.adc_bits > 0 ? int((1u << o.adc_bits) - 1) : 0;
     a.maxc_d = double(a.maxc);
     a.i_fs = o.adc_i_fs;
     int lv;
     (void)std::frexp(o.dac_v_fs, &lv);
     a.sh = (lv - 1) - rp.snap_e;
-    if (a.passthrough && !c->fully_ideal) {
-      // pass-through totals must stay exact in fp64 (< 2^53 units of 2^-e)
-      const double qmax = std::ldexp(o.g_max, rp.snap_e), sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
-      const double fwd = double(g.GR) * o.tile_rows * qmax * (std::pow(2.0, g.Ti) - 1) * sw;
-      const double bwd = 2.0 * double(g.GC) * o.tile_cols * qmax * (std::pow(2.0, g.Te) - 1) * sw;
-      if (std::max(fwd, bwd) >= 9007199254740992.0)
-        fail(XBS_UNSUPPORTED, "pass-through ADC totals exceed 2^53 on this layer (inexact in the reference)");
-    }
+    c->adc_b = a;
 
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     if (!a.passthrough) {
-      // code(n) of converters.cpp:79-87 on the snapped current I = n 2^sh is
-      // monotone in n, so T[k] = min{n : code(n) >= k} decides every code
-      // exactly; the tcgen05 epilogues use it for the boundary cases.
-      auto code = [&](uint64_t n) {
-        const double scaled = std::ldexp(double(n), a.sh) / a.i_fs * a.maxc_d;
-        return scaled >= a.maxc_d ? int64_t(a.maxc) : int64_t(std::llround(scaled));
-      };
-      std::vector<unsigned long long> T(size_t(a.maxc) + 1, 0ull);
-      const uint64_t top = uint64_t(1) << 44;  // > 65025^2 * 256 >= any column current
-      for (int k = 1; k <= a.maxc; ++k) {
-        uint64_t lo = k > 1 ? T[size_t(k) - 1] : 0, hi = top;
-        if (code(hi) < k) {
-          T[size_t(k)] = top;
-          continue;
-        }
-        while (lo < hi) {
-          const uint64_t mid = lo + (hi - lo) / 2;
-          if (code(mid) >= k) hi = mid;
-          else lo = mid + 1;
-        }
-        T[size_t(k)] = lo;
-      }
-      ck(cudaMalloc(&c->d_adc_tab, T.size() * 8), "cudaMalloc adc table");
-      ck(cudaMemcpy(c->d_adc_tab, T.data(), T.size() * 8, cudaMemcpyHostToDevice), "H2D adc table");
+      set_adc(c.get(), 0, o.adc_i_fs);
+      set_adc(c.get(), 1, o.adc_i_fs);
+    }
+    if (c->adc_auto) {
+      ck(cudaMalloc(&c->d_obs_count, 2 * sizeof(unsigned long long)), "cudaMalloc calibration counters");
+      ck(cudaMemsetAsync(c->d_obs_count, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
     }
     ck(cudaMalloc(&c->d_master, size_t(g.S) * g.Kp * g.Np * 8), "cudaMalloc master");
     ck(cudaMalloc(&c->d_digits, g.digits_bytes()), "cudaMalloc digits");
@@ -619,6 +670,9 @@ void xbs_core_destroy(xbs_core* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_digits);
   cudaFree(c->d_adc_tab);
+  cudaFree(c->d_adc_tab_b);
+  xbs::calib_release(c);
+  cudaFree(c->d_obs_count);
   cudaFree(c->d_qmin);
   cudaFree(c->d_varm);
   cudaFree(c->d_fcm_scratch);
@@ -745,7 +799,7 @@ int xbs_core_get_info(xbs_core* c, xbs_core_info* info) {
     info->conversion_seconds = c->conversion_seconds;
     info->weight_abs_max_seen = c->wmax_seen;
     info->grad_abs_max_seen = c->dwmax_seen;
-    info->forward_adc_full_scale = c->opt.adc_i_fs;
+    info->forward_adc_full_scale = c->adc_auto && c->adc_frozen ? c->adc.i_fs : c->opt.adc_i_fs;
     info->fully_ideal = c->fully_ideal ? 1 : 0;
     info->kernel = c->kernel;
   });

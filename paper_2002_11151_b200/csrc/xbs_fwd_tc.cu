@@ -308,7 +308,7 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
     a.mfast = costM <= costO ? 1 : 0;
   }
   a.k_out = c->k_out_fwd;
-  a.adc = make_adc_const(c);
+  a.adc = make_adc_const(c->adc, c->d_adc_tab);
   a.y = d_y;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;

@@ -111,7 +111,8 @@ struct xbs_core {
   std::vector<double> dac_tr, adc_tr;
   xbs::Geo g;
   xbs::RegenP rp{};
-  xbs::AdcP adc{};
+  xbs::AdcP adc{};    // forward ADC (adc_fwd_)
+  xbs::AdcP adc_b{};  // backward ADC (adc_bwd_); differs from adc only after auto-calibration
   xbs::FcmP fcm{};
   bool tile_engine = false;     // fcm / interp_fcm with parasitics: per-tile regeneration kernels
   uint64_t update_count = 0;    // layers.cpp:389 (interp refresh schedule)
@@ -124,6 +125,15 @@ struct xbs_core {
   double k_out_fwd = 0.0;     // layers.cpp:272-281
   double kb_F_over_vu = 0.0;  // backward: k = step_e * F / vu (* ifs_fac)
   double F = 0.0, vu = 0.0, ifs_fac = 1.0, sx = 0.0, lev_e = 0.0, lev_a = 0.0;
+  double ifs_fac_b = 1.0;  // backward i_fs / (2^bits - 1)
+  // ADC auto-calibration (layers.cpp:74, 189-213): pass-through VMMs that
+  // record every sensed current (as n, units 2^sh) until adc_cal_batches
+  // training forwards, then the nearest-rank quantile fixes i_fs
+  bool adc_auto = false, adc_frozen = false;
+  int64_t training_batches = 0;
+  unsigned long long* d_obs[2] = {nullptr, nullptr};  // observed n [fwd, bwd]
+  int64_t obs_cap[2] = {0, 0}, obs_used[2] = {0, 0};  // host upper bound of the device count
+  unsigned long long* d_obs_count = nullptr;          // device counts [2]
   // device buffers
   uint8_t* d_digits = nullptr;
   uint32_t* d_qmin = nullptr;  // sigma == 0: snapped q of g_min per tile position
@@ -134,6 +144,7 @@ struct xbs_core {
   double* d_cache_g = nullptr;
   double* d_cache_gn = nullptr;
   unsigned long long* d_adc_tab = nullptr;  // T[k] = min column current n (units 2^-e) with code >= k
+  unsigned long long* d_adc_tab_b = nullptr;  // same for the backward ADC
   double* d_master = nullptr;
   double* d_dW = nullptr;
   double* d_wimp = nullptr;  // implied weights (fully-ideal fast path), K x N row-major
@@ -204,4 +215,9 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
 bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
 bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
+// ADC auto-calibration (xbs_calib.cu)
+void calib_observe_fwd(xbs_core* c, int64_t M, cudaStream_t st);
+void calib_observe_bwd(xbs_core* c, int64_t M, cudaStream_t st);
+bool calib_select(xbs_core* c, int dir, double pct, uint64_t* n_out);  // false: no observations
+void calib_release(xbs_core* c);
 }  // namespace xbs

@@ -718,6 +718,36 @@ __device__ __forceinline__ int64_t adc_apply(const AdcP& a, int64_t n, unsigned 
 }
 
 // forward (layers.cpp:246-283): one thread per (b, logical output column).
+// Pass-through sensing (adc.bits = 0, or auto-calibration batches): the
+// currents themselves are summed, in fp64, so the totals follow the
+// reference's accumulation order exactly (units of 2^sh; every product is by
+// a power of two, only the additions round):
+//   forward  (layers.cpp:246-270): out += tile_out over tr; tile_out +=
+//            +-sw * acc over (s, p); acc += wk * I over k
+//   backward (layers.cpp:340-366): dx += tile_dx over tc; tile_dx += sw *
+//            (acc_pos - acc_neg) over s; acc_pos += wk * (I_pp + I_mn) over k
+__device__ double fwd_passthrough(const Geo& g, const uint8_t* A, const uint8_t* digits, int64_t b, int tc, int c) {
+  double out = 0.0;
+  for (int tr = 0; tr < g.GR; ++tr) {
+    double tile = 0.0;
+    for (int s = 0; s < g.S; ++s)
+      for (int p = 0; p < 2; ++p) {
+        double acc = 0.0;
+        for (int k = 0; k < g.Ti; ++k) {
+          const uint8_t* arow = A + (b * g.TPi + k) * g.KI + size_t(tr) * g.R;
+          int64_t nn = 0;
+          for (int r = 0; r < g.tile_rows; ++r)
+            if (arow[r]) nn += load_q(digits, g, s, p, tr, tc, r, c);
+          acc = __dadd_rn(acc, ldexp(double(nn), k));
+        }
+        const double w = ldexp(acc, s * g.db);
+        tile = __dadd_rn(tile, p == 0 ? w : -w);
+      }
+    out = __dadd_rn(out, tile);
+  }
+  return out;
+}
+
 __global__ void k_fwd_simt(Geo g, AdcP a, int64_t M, int64_t rowsF, const uint8_t* __restrict__ A,
                            const uint8_t* __restrict__ digits, double k_out, double* __restrict__ y) {
   const int64_t n = M * g.N;
@@ -725,6 +755,10 @@ __global__ void k_fwd_simt(Geo g, AdcP a, int64_t M, int64_t rowsF, const uint8_
     const int64_t b = t % M;
     const int col = int(t / M);
     const int tc = col / g.tile_cols, c = col % g.tile_cols;
+    if (a.passthrough) {
+      y[int64_t(col) * M + b] = ldexp(fwd_passthrough(g, A, digits, b, tc, c), a.sh) * k_out;
+      continue;
+    }
     int64_t total = 0;
     for (int k = 0; k < g.Ti; ++k) {
       const uint8_t* arow = A + (b * g.TPi + k) * g.KI;
@@ -739,7 +773,7 @@ __global__ void k_fwd_simt(Geo g, AdcP a, int64_t M, int64_t rowsF, const uint8_
             total += p == 0 ? w : -w;
           }
     }
-    y[int64_t(col) * M + b] = a.passthrough ? ldexp(double(total), a.sh) * k_out : double(total) * k_out;
+    y[int64_t(col) * M + b] = double(total) * k_out;
   }
 }
 
@@ -764,6 +798,32 @@ __global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__
     const int64_t b = t % M;
     const int i = int(t / M);
     const int tr = i / g.tile_rows, r = i % g.tile_rows;
+    if (a.passthrough) {
+      double acc_dx = 0.0;
+      if (se > 0)
+        for (int tc = 0; tc < g.GC; ++tc) {
+          double tile = 0.0;
+          for (int s = 0; s < g.S; ++s) {
+            double apos = 0.0, aneg = 0.0;
+            for (int k = 0; k < g.Te; ++k) {
+              const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NI + size_t(tc) * g.C;
+              const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NI + size_t(tc) * g.C;
+              int64_t pp = 0, mn = 0, pn = 0, mp = 0;
+              for (int c = 0; c < g.tile_cols; ++c) {
+                const int64_t qp = load_q(digits, g, s, 0, tr, tc, r, c), qn = load_q(digits, g, s, 1, tr, tc, r, c);
+                if (ap[c]) { pp += qp; pn += qn; }
+                if (am[c]) { mn += qn; mp += qp; }
+              }
+              apos = __dadd_rn(apos, ldexp(__dadd_rn(double(pp), double(mn)), k));
+              aneg = __dadd_rn(aneg, ldexp(__dadd_rn(double(pn), double(mp)), k));
+            }
+            tile = __dadd_rn(tile, ldexp(__dsub_rn(apos, aneg), s * g.db));
+          }
+          acc_dx = __dadd_rn(acc_dx, tile);
+        }
+      dx[int64_t(i) * M + b] = ldexp(acc_dx, a.sh) * k_out;
+      continue;
+    }
     int64_t total = 0;
     if (se > 0)
       for (int k = 0; k < g.Te; ++k) {
@@ -782,7 +842,7 @@ __global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__
             total += (v << (s * g.db)) << k;
           }
       }
-    dx[int64_t(i) * M + b] = a.passthrough ? ldexp(double(total), a.sh) * k_out : double(total) * k_out;
+    dx[int64_t(i) * M + b] = double(total) * k_out;
   }
 }
 
@@ -790,7 +850,7 @@ void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st
   const int64_t n = M * c->g.K;
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
-  k_bwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc, M, c->d_Ab, c->d_digits, c->F, c->vu, c->ifs_fac,
+  k_bwd_simt<<<blocks, 128, 0, st>>>(c->g, c->adc_b, M, c->d_Ab, c->d_digits, c->F, c->vu, c->ifs_fac_b,
                                       c->adc_scaled ? 1 : 0, c->lev_e, c->d_sc, d_dx);
 }
 

@@ -315,7 +315,7 @@ __device__ __forceinline__ void group_reduce16(int (&v)[16], int q, int G) {
 bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
                  int swizzle_bytes = 128);
 int num_sms();
-AdcConst make_adc_const(const xbs_core* c);
+AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab);
 
 }  // namespace tc
 }  // namespace xbs

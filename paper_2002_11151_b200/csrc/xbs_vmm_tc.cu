@@ -68,19 +68,19 @@ bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t oute
 }
 int num_sms() { return sm_count(); }
 
-AdcConst make_adc_const(const xbs_core* c) {
+AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab) {
   AdcConst k{};
-  const double cn = std::ldexp(1.0, c->adc.sh) / c->adc.i_fs * c->adc.maxc_d;  // codes per current unit
+  const double cn = std::ldexp(1.0, a.sh) / a.i_fs * a.maxc_d;  // codes per current unit
   k.c_lo = float(cn);
   k.c_hi = float(65025.0 * cn);
   // |x_fast - scaled| <= 3 2^-24 x (constants' rounding, FMUL, FFMA) with
   // x <= maxc + 1 wherever the code is not saturated; delta = 4x that.
-  const double maxc = double(c->adc.maxc);
+  const double maxc = double(a.maxc);
   const double delta = 4.0 * 3.0 * 0x1p-24 * (maxc + 1.0);
   k.thr = float(0.5 - delta);
-  k.maxc = float(c->adc.maxc);
-  k.maxc_i = c->adc.maxc;
-  k.tab = c->d_adc_tab;
+  k.maxc = float(a.maxc);
+  k.maxc_i = a.maxc;
+  k.tab = tab;
   return k;
 }
 
@@ -356,11 +356,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   using namespace tc;
   const Geo& g = c->g;
-  if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc.passthrough) return false;
+  if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc_b.passthrough) return false;
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
-  if (double(g.GC) * c->adc.maxc * sw * 2.0 >= 16777216.0) return false;
+  if (double(g.GC) * c->adc_b.maxc * sw * 2.0 >= 16777216.0) return false;
   // int32 (plane, phase) combine: |sum| < 2^31
-  if (double(g.GC) * c->adc.maxc * sw * 2.0 * (std::pow(2.0, g.Te) - 1) >= 2147483648.0) return false;
+  if (double(g.GC) * c->adc_b.maxc * sw * 2.0 * (std::pow(2.0, g.Te) - 1) >= 2147483648.0) return false;
   const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
   if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
@@ -393,11 +393,11 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   }
   a.F = c->F;
   a.vu = c->vu;
-  a.ifs_fac = c->ifs_fac;
+  a.ifs_fac = c->ifs_fac_b;
   a.lev_e = c->lev_e;
   a.adc_scaled = c->adc_scaled ? 1 : 0;
   a.sc = c->d_sc;
-  a.adc = make_adc_const(c);
+  a.adc = make_adc_const(c->adc_b, c->d_adc_tab_b);
   a.dx = d_dx;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;

@@ -82,13 +82,20 @@ def test_nonfinite_and_empty_weights_rejected():
     "mutate",
     [
         lambda o: setattr(o, "engine", xb.EngineKind.oracle),  # dense nodal solve with parasitics (8f-4)
-        lambda o: setattr(o.adc, "i_fs", 0.0),  # auto-calibration
         lambda o: setattr(o.adc, "transfer", [0.0, 1e-6, 2e-6, 3e-6]),
     ],
 )
 def test_out_of_scope_configs_fail_loudly(mutate):
     o = aam_options(tile=64)
     mutate(o)
+    with pytest.raises(xb.ConfigError):
+        _create(o, np.zeros((8, 8)))
+
+
+def test_auto_calibration_batches_validated():
+    """layers.cpp:45: adc_cal_batches >= 1 (ConfigError), before device work."""
+    o = aam_options(tile=8, i_fs=0.0)
+    o.adc_cal_batches = 0
     with pytest.raises(xb.ConfigError):
         _create(o, np.zeros((8, 8)))
 
