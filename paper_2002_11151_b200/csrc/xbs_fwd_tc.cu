@@ -225,7 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       for (int j = 0; j < 16; ++j) P[j] = 0.f;
       for (int c = 0; c < nchain; ++c) {
         const int sp = c % (2 * a.S);  // chains run tr-major, then slice, then polarity
-        const float w = (sp & 1) == 0 ? float(1 << ((sp >> 1) * a.db)) : -float(1 << ((sp >> 1) * a.db));
+        const float w0 = (sp & 1) == 0 ? float(1 << ((sp >> 1) * a.db)) : -float(1 << ((sp >> 1) * a.db));
+        const float w = __fmul_rn(w0, k.unscale);
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         uint32_t lo[16], hi[16];
@@ -309,6 +310,7 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   }
   a.k_out = c->k_out_fwd;
   a.adc = make_adc_const(c->adc, c->d_adc_tab);
+  if (a.adc.unscale == 0.0f) return false;
   a.y = d_y;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;

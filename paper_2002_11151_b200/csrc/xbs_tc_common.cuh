@@ -218,22 +218,34 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 // exact fp64 expression, xbs_core.cu).
 //
 // Fast path (every conversion): x = hi c_hi + lo c_lo in fp32 with
-// |x - scaled| <= 3 2^-24 (maxc + 1) on the unsaturated range; t = rint(x)
-// clamped to maxc.  Whenever |x - t| > 0.5 - delta (delta = 4x that bound)
+// |x - scaled| <= ~3 2^-24 (maxc + 1) on the unsaturated range; t = rint(x)
+// clamped to maxc.  Whenever |x - t| > 0.5 - delta (delta = 3.5 2^-24 (maxc + 1))
 // the fast code may be off by one and the conversion is decided exactly by
 // the thresholds (adc_fix).  So every code equals the reference's.
+//
+// No int->float conversion: an accumulator value n < 2^24, read as fp32 bits,
+// is exactly n 2^-149 (subnormal below 2^23; exponent field 1 up to 2^24 is
+// the same linear map).  The FMAs take subnormal inputs at full rate, so with
+// constants pre-scaled by 2^(149 - s) the kernel computes x' = x 2^-s
+// exactly (every step is the unscaled one times a power of two; s is chosen
+// on the host so that no constant overflows and no x' is subnormal).  The
+// rounding magic, clamp and threshold are scaled alike, and the shift-add
+// weights by 2^s, so P still sums true codes.
 struct AdcConst {
-  float c_hi, c_lo, maxc;
-  float thr;  // 0.5 - delta
+  float c_hi, c_lo, maxc;  // scaled: c * 2^(149 - s), maxc * 2^-s
+  float thr;               // (0.5 - delta) * 2^-s
+  float rint;              // 1.5 * 2^(23 - s): x' + rint - rint = rint(x) 2^-s for 0 <= x < 2^22
+  float unscale, scale;    // 2^s, 2^-s
   int maxc_i;
   const unsigned long long* tab;  // T[0..maxc], T[0] = 0
 };
-constexpr float kRint = 12582912.0f;  // 1.5 * 2^23: x + kRint - kRint = rint(x) for 0 <= x < 2^22
 
 __device__ __forceinline__ float adc_x(uint32_t hi, uint32_t lo, const AdcConst& k) {
-  return __fmaf_rn(__uint2float_rn(hi), k.c_hi, __fmul_rn(__uint2float_rn(lo), k.c_lo));
+  return __fmaf_rn(__uint_as_float(hi), k.c_hi, __fmul_rn(__uint_as_float(lo), k.c_lo));
 }
-__device__ __forceinline__ float rint_magic(float x) { return __fsub_rn(__fadd_rn(x, kRint), kRint); }
+__device__ __forceinline__ float rint_magic(float x, const AdcConst& k) {
+  return __fsub_rn(__fadd_rn(x, k.rint), k.rint);
+}
 
 // Exact code of the current n = hi*65025 + lo given a fast candidate t that
 // is off by at most one.
@@ -246,7 +258,8 @@ static __device__ __noinline__ float adc_fix(uint32_t hi, uint32_t lo, float t, 
   return float(c);
 }
 
-// Eight conversions lo/hi[OFF .. OFF+8) -> P[b+j] += w * code.  If any lane
+// Eight conversions lo/hi[OFF .. OFF+8) -> P[b+j] += w * code (w: the
+// shift-add weight times k.unscale).  If any lane
 // saw a fraction beyond thr, the warp re-checks the eight and replaces the
 // flagged codes (P += w * (exact - fast); all operands exact integers).
 template <int OFF, int NL, int kN>
@@ -257,7 +270,7 @@ __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32
   for (int j = 0; j < 8; j += 2) {
     const float x0 = fminf(adc_x(hi[OFF + j], lo[OFF + j], k), k.maxc);
     const float x1 = fminf(adc_x(hi[OFF + j + 1], lo[OFF + j + 1], k), k.maxc);
-    const float t0 = rint_magic(x0), t1 = rint_magic(x1);
+    const float t0 = rint_magic(x0, k), t1 = rint_magic(x1, k);
     mr = fmaxf(mr, fmaxf(fabsf(__fsub_rn(x0, t0)), fabsf(__fsub_rn(x1, t1))));
     P[b + j] = __fmaf_rn(t0, w, P[b + j]);
     P[b + j + 1] = __fmaf_rn(t1, w, P[b + j + 1]);
@@ -266,10 +279,11 @@ __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float x = fminf(adc_x(hi[OFF + j], lo[OFF + j], k), k.maxc);
-      const float t = rint_magic(x);
+      const float t = rint_magic(x, k);
       if (fabsf(__fsub_rn(x, t)) > k.thr) {
         ++exact_ctr;
-        const float d = __fsub_rn(adc_fix(hi[OFF + j], lo[OFF + j], t, k.tab, k.maxc_i), t);
+        const float code = adc_fix(hi[OFF + j], lo[OFF + j], __fmul_rn(t, k.unscale), k.tab, k.maxc_i);
+        const float d = __fsub_rn(__fmul_rn(code, k.scale), t);
         P[b + j] = __fmaf_rn(d, w, P[b + j]);
       }
     }

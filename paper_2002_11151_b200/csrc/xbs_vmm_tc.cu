@@ -71,14 +71,28 @@ int num_sms() { return sm_count(); }
 AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab) {
   AdcConst k{};
   const double cn = std::ldexp(1.0, a.sh) / a.i_fs * a.maxc_d;  // codes per current unit
-  k.c_lo = float(cn);
-  k.c_hi = float(65025.0 * cn);
-  // |x_fast - scaled| <= 3 2^-24 x (constants' rounding, FMUL, FFMA) with
-  // x <= maxc + 1 wherever the code is not saturated; delta = 4x that.
+  const float c_lo = float(cn), c_hi = float(65025.0 * cn);
+  // x_fast = (hi c_hi (1+e2) + lo c_lo (1+e1)(1+e3))(1+e4), |e| <= u = 2^-24
+  // (constants' rounding, FMUL, FFMA), so |x_fast - x| <= ((1+u)^3 - 1) x
+  // with x <= maxc + 1 wherever the code is not saturated.  delta = 3.5 u
+  // (maxc + 1) covers that, the fp64 host constants (~2^-52 relative) and
+  // the rounding of thr to fp32 (<= 2^-25).
   const double maxc = double(a.maxc);
-  const double delta = 4.0 * 3.0 * 0x1p-24 * (maxc + 1.0);
-  k.thr = float(0.5 - delta);
-  k.maxc = float(a.maxc);
+  const double delta = 3.5 * 0x1p-24 * (maxc + 1.0);
+  // scale 2^-s (xbs_tc_common.cuh): c_hi 2^(149 - s) <= 2^126, and the
+  // smallest nonzero term lo c_lo 2^-s >= 2^-100 stays normal
+  int e_hi;
+  (void)std::frexp(double(c_hi), &e_hi);  // c_hi < 2^e_hi
+  const int s = e_hi + 23;
+  if (!(c_lo > 0.0f) || std::ldexp(double(c_lo), -s) < 0x1p-100 || s > 110 || s < -100)
+    return AdcConst{};  // out of the scaled range: caller falls back
+  k.c_lo = std::ldexp(c_lo, 149 - s);
+  k.c_hi = std::ldexp(c_hi, 149 - s);
+  k.thr = std::ldexp(float(0.5 - delta), -s);
+  k.maxc = std::ldexp(float(a.maxc), -s);
+  k.rint = std::ldexp(1.5f, 23 - s);
+  k.unscale = std::ldexp(1.0f, s);
+  k.scale = std::ldexp(1.0f, -s);
   k.maxc_i = a.maxc;
   k.tab = tab;
   return k;
@@ -299,7 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
       for (int c = 0; c < nchain; ++c) {
         const int s = c % a.S;  // chains run tc-major, then slice
-        const float w = float(1 << (s * a.db));
+        const float w = __fmul_rn(float(1 << (s * a.db)), k.unscale);
         const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
         const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
         mbar_wait_hint(&t_full[ab], abph);
@@ -398,6 +412,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   a.adc_scaled = c->adc_scaled ? 1 : 0;
   a.sc = c->d_sc;
   a.adc = make_adc_const(c->adc_b, c->d_adc_tab_b);
+  if (a.adc.unscale == 0.0f) return false;
   a.dx = d_dx;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
