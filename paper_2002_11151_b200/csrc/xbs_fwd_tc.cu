@@ -223,10 +223,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       float P[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) P[j] = 0.f;
+      // chains run tr-major, then slice, then polarity: weight +-2^(s db)
+      // (times k.unscale), stepped without integer division
+      const float wstep = float(1 << a.db);
+      float wmag = k.unscale;
+      int sp = 0;
       for (int c = 0; c < nchain; ++c) {
-        const int sp = c % (2 * a.S);  // chains run tr-major, then slice, then polarity
-        const float w0 = (sp & 1) == 0 ? float(1 << ((sp >> 1) * a.db)) : -float(1 << ((sp >> 1) * a.db));
-        const float w = __fmul_rn(w0, k.unscale);
+        const float w = (sp & 1) == 0 ? wmag : -wmag;
+        if (++sp == 2 * a.S) {
+          sp = 0;
+          wmag = k.unscale;
+        } else if ((sp & 1) == 0) {
+          wmag = __fmul_rn(wmag, wstep);
+        }
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         uint32_t lo[16], hi[16];

@@ -311,9 +311,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float P[kRows];
 #pragma unroll
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
+      const float wstep = float(1 << a.db);
+      float wmag = k.unscale;
+      int s = 0;
       for (int c = 0; c < nchain; ++c) {
-        const int s = c % a.S;  // chains run tc-major, then slice
-        const float w = __fmul_rn(float(1 << (s * a.db)), k.unscale);
+        // chains run tc-major, then slice: weight 2^(s db) k.unscale
+        const float w = wmag;
+        if (++s == a.S) {
+          s = 0;
+          wmag = k.unscale;
+        } else {
+          wmag = __fmul_rn(wmag, wstep);
+        }
         const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
         const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
         mbar_wait_hint(&t_full[ab], abph);
