@@ -40,7 +40,11 @@ namespace xbs {
 namespace tc {
 
 namespace fw {
-constexpr int kEpiWarps = 16;
+#ifndef XBS_FWD_EPI_WARPS
+#define XBS_FWD_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = XBS_FWD_EPI_WARPS;
+constexpr int kCPW = 64 / (kEpiWarps / 4);  // unit columns per epilogue warp (16, 32 or 64)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kCW = 64;             // device columns per unit
 constexpr int kABox = 128 * 128;    // 128 rows x 128 B (one k-block), SW128
@@ -209,20 +213,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
-    const int lg = warp & 3, q = (warp - 2) >> 2;  // TMEM lane quarter, 16-column quarter
+    // warp -> (TMEM lane quarter lg, kCPW-column slice q of the unit's 64)
+    const int lg = warp & 3, q = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
-    const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + 16 * q;
-    uint32_t te[kTBufs];
-#pragma unroll
-    for (int i = 0; i < kTBufs; ++i) te[i] = mapa(smem_u32(&t_empty[i]), 0);
+    const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kCPW * q;
+    const uint32_t te0 = mapa(smem_u32(&t_empty[0]), 0);  // leader's barriers, 8 B apart
     const int nchain = a.GR * a.S * 2;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     for (int u = cid; u < a.num_units; u += ncl) {
       const int mbp = a.mfast ? u % a.num_mbp : u / a.n_nb, nb = a.mfast ? u / a.num_mbp : u % a.n_nb;
-      float P[16];
+      float P[kCPW];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) P[j] = 0.f;
+      for (int j = 0; j < kCPW; ++j) P[j] = 0.f;
       // chains run tr-major, then slice, then polarity: weight +-2^(s db)
       // (times k.unscale), stepped without integer division
       const float wstep = float(1 << a.db);
@@ -238,35 +241,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         }
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
-        uint32_t lo[16], hi[16];
-        tmem_ld16(tl + ab * 128, lo);
-        tmem_ld16(tl + ab * 128 + kCW, hi);
+        uint32_t lo[kCPW], hi[kCPW];
+#pragma unroll
+        for (int h = 0; h < kCPW / 16; ++h) {
+          tmem_ld16(tl + ab * 128 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
+          tmem_ld16(tl + ab * 128 + kCW + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+        }
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_relaxed(te[ab]);
+        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
         if (++ab == kTBufs) { ab = 0; abph ^= 1; }
         adc_conv8<0>(lo, hi, k, w, P, 0, exact);
         adc_conv8<8>(lo, hi, k, w, P, 8, exact);
+        if constexpr (kCPW >= 32) {
+          adc_conv8<16>(lo, hi, k, w, P, 16, exact);
+          adc_conv8<24>(lo, hi, k, w, P, 24, exact);
+        }
+        if constexpr (kCPW >= 64) {
+          adc_conv8<32>(lo, hi, k, w, P, 32, exact);
+          adc_conv8<40>(lo, hi, k, w, P, 40, exact);
+          adc_conv8<48>(lo, hi, k, w, P, 48, exact);
+          adc_conv8<56>(lo, hi, k, w, P, 56, exact);
+        }
       }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
-      // (exact in int32: host-checked bound); lane q ends with the totals of
-      // columns q * (16 / TPi) + i
+      // (exact in int32: host-checked bound); per 16 columns, lane q ends
+      // with the totals of columns q * (16 / TPi) + i
       const int kk = ml % a.TPi;
       const int64_t b = (int64_t(2 * mbp + int(rank)) * 128 + ml) / a.TPi;
-      int tc, h;
-      col_unit(nb, a, tc, h);
-      int v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[j]) * (1 << kk);
-      group_reduce16(v, kk, a.TPi);
+      int tc, hcol;
+      col_unit(nb, a, tc, hcol);
       const int per = 16 / a.TPi;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (i >= per) break;
-        const int cc = h * kCW + 16 * q + kk * per + i;
-        const int jg = tc * a.tile_cols + cc;
-        if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v[i]) * a.k_out;
+      for (int h = 0; h < kCPW / 16; ++h) {
+        int v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[16 * h + j]) * (1 << kk);
+        group_reduce16(v, kk, a.TPi);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= per) break;
+          const int cc = hcol * kCW + kCPW * q + 16 * h + kk * per + i;
+          const int jg = tc * a.tile_cols + cc;
+          if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v[i]) * a.k_out;
+        }
       }
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);

@@ -236,6 +236,7 @@ struct AdcConst {
   float thr;               // (0.5 - delta) * 2^-s
   float rint;              // 1.5 * 2^(23 - s): x' + rint - rint = rint(x) 2^-s for 0 <= x < 2^22
   float unscale, scale;    // 2^s, 2^-s
+  uint64_t c_lo2, c_hi2, rint2;  // (c_lo, c_lo), (c_hi, c_hi), (rint, rint) for the f32x2 path
   int maxc_i;
   const unsigned long long* tab;  // T[0..maxc], T[0] = 0
 };
@@ -262,19 +263,30 @@ static __device__ __noinline__ float adc_fix(uint32_t hi, uint32_t lo, float t, 
 // shift-add weight times k.unscale).  If any lane
 // saw a fraction beyond thr, the warp re-checks the eight and replaces the
 // flagged codes (P += w * (exact - fast); all operands exact integers).
+// Two conversions with packed f32x2 arithmetic (one issue slot per pair):
+// the same operations, in the same order and rounding, as adc_x / fminf /
+// rint_magic / x - t / P += t w on each element.
+__device__ __forceinline__ void adc_pair(uint32_t lo0, uint32_t lo1, uint32_t hi0, uint32_t hi1, const AdcConst& k,
+                                         uint64_t w2, float& p0, float& p1, float& mr) {
+  asm("{\n\t.reg .b64 L, H, T, X, Y, TT, RR, PP;\n\t.reg .f32 x0, x1, r0, r1;\n\t"
+      "mov.b64 L, {%3, %4};\n\tmov.b64 H, {%5, %6};\n\t"
+      "mul.rn.f32x2 T, L, %7;\n\tfma.rn.f32x2 X, H, %8, T;\n\t"
+      "mov.b64 {x0, x1}, X;\n\tmin.f32 x0, x0, %9;\n\tmin.f32 x1, x1, %9;\n\tmov.b64 X, {x0, x1};\n\t"
+      "add.rn.f32x2 Y, X, %10;\n\tsub.rn.f32x2 TT, Y, %10;\n\tsub.rn.f32x2 RR, X, TT;\n\t"
+      "mov.b64 {r0, r1}, RR;\n\tabs.f32 r0, r0;\n\tabs.f32 r1, r1;\n\tmax.f32 r0, r0, r1;\n\tmax.f32 %2, %2, r0;\n\t"
+      "mov.b64 PP, {%0, %1};\n\tfma.rn.f32x2 PP, TT, %11, PP;\n\tmov.b64 {%0, %1}, PP;\n\t}"
+      : "+f"(p0), "+f"(p1), "+f"(mr)
+      : "r"(lo0), "r"(lo1), "r"(hi0), "r"(hi1), "l"(k.c_lo2), "l"(k.c_hi2), "f"(k.maxc), "l"(k.rint2), "l"(w2));
+}
+
 template <int OFF, int NL, int kN>
 __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32_t (&hi)[NL], const AdcConst& k,
                                           float w, float (&P)[kN], int b, uint32_t& exact_ctr) {
   float mr = 0.f;
+  const uint64_t w2 = (uint64_t(__float_as_uint(w)) << 32) | __float_as_uint(w);
 #pragma unroll
-  for (int j = 0; j < 8; j += 2) {
-    const float x0 = fminf(adc_x(hi[OFF + j], lo[OFF + j], k), k.maxc);
-    const float x1 = fminf(adc_x(hi[OFF + j + 1], lo[OFF + j + 1], k), k.maxc);
-    const float t0 = rint_magic(x0, k), t1 = rint_magic(x1, k);
-    mr = fmaxf(mr, fmaxf(fabsf(__fsub_rn(x0, t0)), fabsf(__fsub_rn(x1, t1))));
-    P[b + j] = __fmaf_rn(t0, w, P[b + j]);
-    P[b + j + 1] = __fmaf_rn(t1, w, P[b + j + 1]);
-  }
+  for (int j = 0; j < 8; j += 2)
+    adc_pair(lo[OFF + j], lo[OFF + j + 1], hi[OFF + j], hi[OFF + j + 1], k, w2, P[b + j], P[b + j + 1], mr);
   if (__any_sync(0xffffffffu, mr > k.thr)) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {

@@ -1,5 +1,6 @@
 // K2: tcgen05 backward crossbar VMM for sm_100a, plus the tensor-map / ADC
 // constant helpers shared with K1 (xbs_fwd_tc.cu) and K3a (xbs_dw_tc.cu).
+#include <cstring>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -93,6 +94,14 @@ AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab) {
   k.rint = std::ldexp(1.5f, 23 - s);
   k.unscale = std::ldexp(1.0f, s);
   k.scale = std::ldexp(1.0f, -s);
+  auto pk = [](float v) {
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    return (uint64_t(u) << 32) | u;
+  };
+  k.c_lo2 = pk(k.c_lo);
+  k.c_hi2 = pk(k.c_hi);
+  k.rint2 = pk(k.rint);
   k.maxc_i = a.maxc;
   k.tab = tab;
   return k;
