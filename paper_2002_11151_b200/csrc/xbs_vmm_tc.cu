@@ -13,7 +13,10 @@
 namespace xbs {
 namespace tc {
 
-constexpr int kEpiWarps = 16;                 // 4 per SM sub-partition
+#ifndef XBS_BWD_EPI_WARPS
+#define XBS_BWD_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = XBS_BWD_EPI_WARPS;  // 2 or 4 per SM sub-partition
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer, MMA issuer
 constexpr int kPlane = 128 * 128;          // one 128x128 u8 box
 
@@ -296,16 +299,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
-    // Per chain a warp converts kRows = 16 device rows x 2 polarities as
-    // four 8-column chunks (lo at +0, hi at +64 within each polarity).
+    // Per chain a warp converts kRows (16 or 32) device rows x 2 polarities
+    // (lo at +0, hi at +64 within each polarity's 128 columns).
     constexpr int kRows = 64 / (kEpiWarps / 4);  // output rows per epilogue warp
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
     const int phi = ml & 1;
     const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kRows * ch;
-    uint32_t te[kTBufs];
-#pragma unroll
-    for (int i = 0; i < kTBufs; ++i) te[i] = mapa(smem_u32(&t_empty[i]), 0);
+    const uint32_t te0 = mapa(smem_u32(&t_empty[0]), 0);  // leader's barriers, 8 B apart
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     const double se = a.sc->se;
@@ -337,23 +338,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         const uint32_t ta = tl + ab * 256;
-        uint32_t lo[16], hi[16];
-        tmem_ld8(ta, *reinterpret_cast<uint32_t(*)[8]>(&lo[0]));
-        tmem_ld8(ta + 8, *reinterpret_cast<uint32_t(*)[8]>(&lo[8]));
-        tmem_ld8(ta + 64, *reinterpret_cast<uint32_t(*)[8]>(&hi[0]));
-        tmem_ld8(ta + 64 + 8, *reinterpret_cast<uint32_t(*)[8]>(&hi[8]));
-        tmem_wait_ld();
-        adc_conv8<0>(lo, hi, k, wpos, P, 0, exact);
-        adc_conv8<8>(lo, hi, k, wpos, P, 8, exact);
-        tmem_ld16(ta + 128, lo);
-        tmem_ld16(ta + 128 + 64, hi);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_relaxed(te[ab]);
-        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-        adc_conv8<0>(lo, hi, k, wneg, P, 0, exact);
-        adc_conv8<8>(lo, hi, k, wneg, P, 8, exact);
+        uint32_t lo[kRows], hi[kRows];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+#pragma unroll
+          for (int h = 0; h < kRows / 16; ++h) {
+            tmem_ld16(ta + 128 * p + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
+            tmem_ld16(ta + 128 * p + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+          }
+          tmem_wait_ld();
+          if (p == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          }
+          const float wp = p == 0 ? wpos : wneg;
+          adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
+          adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
+          if constexpr (kRows >= 32) {
+            adc_conv8<16>(lo, hi, k, wp, P, 16, exact);
+            adc_conv8<24>(lo, hi, k, wp, P, 24, exact);
+          }
+        }
       }
       // combine the 2*TPe (plane, phase) lanes of each batch row (exact in
       // int32: host-checked bound); lane q ends with the totals of rows
@@ -361,19 +368,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int grp = 2 * a.TPe;
       const int q = ml % grp, kk = q >> 1;
       const int64_t b = int64_t(2 * mbp + int(rank)) * (128 / grp) + ml / grp;
-      int v[16];
-#pragma unroll
-      for (int j = 0; j < kRows; ++j) v[j] = __float2int_rn(P[j]) * (1 << kk);
-      group_reduce16(v, q, grp);
       const int per = grp <= 16 ? 16 / grp : 1;
       const int j0 = grp <= 16 ? q * per : (q >> 1);
       const bool writer = grp <= 16 || (q & 1) == 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (i >= per) break;
-        const int rloc = rh * 64 + kRows * ch + j0 + i;
-        const int ig = tr * a.tile_rows + rloc;
-        if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v[i]) * k_out;
+      for (int h = 0; h < kRows / 16; ++h) {
+        int v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[16 * h + j]) * (1 << kk);
+        group_reduce16(v, q, grp);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= per) break;
+          const int rloc = rh * 64 + kRows * ch + 16 * h + j0 + i;
+          const int ig = tr * a.tile_rows + rloc;
+          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v[i]) * k_out;
+        }
       }
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
