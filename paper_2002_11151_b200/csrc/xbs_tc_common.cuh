@@ -254,48 +254,50 @@ static __device__ __noinline__ float adc_fix(uint32_t hi, uint32_t lo, float t, 
                                              int maxc) {
   const unsigned long long n = (unsigned long long)hi * 65025ull + lo;
   int c = int(t);
-  if (c < maxc && n >= __ldg(tab + c + 1)) ++c;
-  else if (c > 0 && n < __ldg(tab + c)) --c;
+  if (c < maxc && n >= tab[c + 1]) ++c;  // tab: shared-memory copy or global (generic loads)
+  else if (c > 0 && n < tab[c]) --c;
   return float(c);
 }
 
-// Eight conversions lo/hi[OFF .. OFF+8) -> P[b+j] += w * code (w: the
-// shift-add weight times k.unscale).  If any lane
-// saw a fraction beyond thr, the warp re-checks the eight and replaces the
-// flagged codes (P += w * (exact - fast); all operands exact integers).
 // Two conversions with packed f32x2 arithmetic (one issue slot per pair):
 // the same operations, in the same order and rounding, as adc_x / fminf /
 // rint_magic / x - t / P += t w on each element.
 __device__ __forceinline__ void adc_pair(uint32_t lo0, uint32_t lo1, uint32_t hi0, uint32_t hi1, const AdcConst& k,
-                                         uint64_t w2, float& p0, float& p1, float& mr) {
-  asm("{\n\t.reg .b64 L, H, T, X, Y, TT, RR, PP;\n\t.reg .f32 x0, x1, r0, r1;\n\t"
-      "mov.b64 L, {%3, %4};\n\tmov.b64 H, {%5, %6};\n\t"
-      "mul.rn.f32x2 T, L, %7;\n\tfma.rn.f32x2 X, H, %8, T;\n\t"
-      "mov.b64 {x0, x1}, X;\n\tmin.f32 x0, x0, %9;\n\tmin.f32 x1, x1, %9;\n\tmov.b64 X, {x0, x1};\n\t"
-      "add.rn.f32x2 Y, X, %10;\n\tsub.rn.f32x2 TT, Y, %10;\n\tsub.rn.f32x2 RR, X, TT;\n\t"
-      "mov.b64 {r0, r1}, RR;\n\tabs.f32 r0, r0;\n\tabs.f32 r1, r1;\n\tmax.f32 r0, r0, r1;\n\tmax.f32 %2, %2, r0;\n\t"
-      "mov.b64 PP, {%0, %1};\n\tfma.rn.f32x2 PP, TT, %11, PP;\n\tmov.b64 {%0, %1}, PP;\n\t}"
-      : "+f"(p0), "+f"(p1), "+f"(mr)
+                                         uint64_t w2, float& p0, float& p1, float& mr, float& t0, float& t1,
+                                         float& r0, float& r1) {
+  // outputs: %0 %1 P pair, %2 running max |x - t|, %3 %4 t pair, %5 %6 x - t pair
+  asm("{\n\t.reg .b64 L, H, T, X, Y, TT, RR, PP;\n\t.reg .f32 x0, x1, a0, a1;\n\t"
+      "mov.b64 L, {%7, %8};\n\tmov.b64 H, {%9, %10};\n\t"
+      "mul.rn.f32x2 T, L, %11;\n\tfma.rn.f32x2 X, H, %12, T;\n\t"
+      "mov.b64 {x0, x1}, X;\n\tmin.f32 x0, x0, %13;\n\tmin.f32 x1, x1, %13;\n\tmov.b64 X, {x0, x1};\n\t"
+      "add.rn.f32x2 Y, X, %14;\n\tsub.rn.f32x2 TT, Y, %14;\n\tsub.rn.f32x2 RR, X, TT;\n\t"
+      "mov.b64 {%5, %6}, RR;\n\tabs.f32 a0, %5;\n\tabs.f32 a1, %6;\n\tmax.f32 a0, a0, a1;\n\tmax.f32 %2, %2, a0;\n\t"
+      "mov.b64 PP, {%0, %1};\n\tfma.rn.f32x2 PP, TT, %15, PP;\n\tmov.b64 {%0, %1}, PP;\n\tmov.b64 {%3, %4}, TT;\n\t}"
+      : "+f"(p0), "+f"(p1), "+f"(mr), "=f"(t0), "=f"(t1), "=f"(r0), "=f"(r1)
       : "r"(lo0), "r"(lo1), "r"(hi0), "r"(hi1), "l"(k.c_lo2), "l"(k.c_hi2), "f"(k.maxc), "l"(k.rint2), "l"(w2));
 }
 
+// Eight conversions lo/hi[OFF .. OFF+8) -> P[b+j] += w * code (w: the
+// shift-add weight times k.unscale).  The rounded codes and residuals stay
+// in registers; if any lane saw a residual beyond thr, the warp visits the
+// eight and replaces the flagged codes (P += w * (exact - fast); all
+// operands exact).
 template <int OFF, int NL, int kN>
 __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32_t (&hi)[NL], const AdcConst& k,
                                           float w, float (&P)[kN], int b, uint32_t& exact_ctr) {
-  float mr = 0.f;
+  float mr = 0.f, t[8], r[8];
   const uint64_t w2 = (uint64_t(__float_as_uint(w)) << 32) | __float_as_uint(w);
 #pragma unroll
   for (int j = 0; j < 8; j += 2)
-    adc_pair(lo[OFF + j], lo[OFF + j + 1], hi[OFF + j], hi[OFF + j + 1], k, w2, P[b + j], P[b + j + 1], mr);
+    adc_pair(lo[OFF + j], lo[OFF + j + 1], hi[OFF + j], hi[OFF + j + 1], k, w2, P[b + j], P[b + j + 1], mr, t[j],
+             t[j + 1], r[j], r[j + 1]);
   if (__any_sync(0xffffffffu, mr > k.thr)) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float x = fminf(adc_x(hi[OFF + j], lo[OFF + j], k), k.maxc);
-      const float t = rint_magic(x, k);
-      if (fabsf(__fsub_rn(x, t)) > k.thr) {
+      if (fabsf(r[j]) > k.thr) {
         ++exact_ctr;
-        const float code = adc_fix(hi[OFF + j], lo[OFF + j], __fmul_rn(t, k.unscale), k.tab, k.maxc_i);
-        const float d = __fsub_rn(__fmul_rn(code, k.scale), t);
+        const float code = adc_fix(hi[OFF + j], lo[OFF + j], __fmul_rn(t[j], k.unscale), k.tab, k.maxc_i);
+        const float d = __fsub_rn(__fmul_rn(code, k.scale), t[j]);
         P[b + j] = __fmaf_rn(d, w, P[b + j]);
       }
     }

@@ -116,22 +116,24 @@ AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab) {
 // K2 backward (layers.cpp:339-379) on CTA pairs (cta_group::2).  Unit =
 // (two 128-row blocks of error bit-plane rows [(b * TPe + k) * 2 + phase], one
 // per CTA of the pair; 64 device rows of one crossbar row tile).  For each
-// crossbar column tile tc and slice s the leader issues one chain of
-// K = 2 x C (tile columns, bits | 255*bits) tcgen05.mma.cta_group::2.kind::i8
-// (M = 256, N = 256, K = 32) with the transposed tiles read K-major straight
+// crossbar column tile tc, slice s and polarity p the leader issues one chain
+// of K = 2 x C (tile columns, bits | 255*bits) tcgen05.mma.cta_group::2.kind::i8
+// (M = 256, N = 128, K = 32) with the transposed tiles read K-major straight
 // from the same digit planes:
-//     D[:, p*128 + acc*64 + r] = sum_c v_phi[c] * q_acc(s, p, tr, tc; r, c)
-// i.e. all four products vp.gp, vp.gn, vm.gp, vm.gn of the reference in one
-// accumulator (phase in M, polarity in N).  B is split along N across the
-// pair: CTA p stages polarity p's digit planes.  The epilogue converts every
-// product through the ADC and accumulates +-2^(s db) * code with sign +1
-// when phase == polarity (acc_pos) and -1 otherwise (acc_neg).
+//     D_p[:, acc*64 + r] = sum_c v_phi[c] * q_acc(s, p, tr, tc; r, c)
+// i.e. the products vp.gp and vm.gp (p = 0) or vp.gn and vm.gn (p = 1) of
+// the reference (phase in M).  B is split along N across the pair: the
+// leader stages the lo digit pairs (d0, d1) and the peer the hi pairs
+// (d2, d3) of both polarities.  Four 128-column TMEM accumulators let the
+// MMAs run up to three half-chains ahead of the epilogue.  The epilogue
+// converts every product through the ADC and accumulates +-2^(s db) * code
+// with sign +1 when phase == polarity (acc_pos) and -1 otherwise (acc_neg).
 namespace tc {
 
 namespace bw {
 constexpr int kBHalf = 64 * 128;     // one [64 rows][128 cols] digit box
-constexpr int kBStage = 4 * kBHalf;  // this CTA's polarity: [dh][acc][64 r][128 c]
-constexpr int kTBufs = 2;            // TMEM accumulators of 256 columns
+constexpr int kBStage = 4 * kBHalf;  // this CTA's digit pair acc = rank: [p][dh][64 r][128 c]
+constexpr int kTBufs = 4;            // TMEM accumulators of 128 columns (one polarity each)
 template <int KB> constexpr int kAStage = 2 * KB * kPlane;  // [dh][kb]
 template <int KB> constexpr int kAStages = 2;
 template <int KB> constexpr int kBStages = KB == 1 ? 4 : 3;
@@ -242,14 +244,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * kBStage);
                 const uint32_t fb = mapa(smem_u32(&b_full[bs]), 0);
                 uint8_t* dst = sB + bs * kBStage;
-                // this CTA's polarity p = rank; smem order [dh][acc][64 r][128 c], digit d = 2*acc + dh
+                // this CTA's digit pair acc = rank; smem order [p][dh][64 r][128 c], digit d = 2*acc + dh
 #pragma unroll
-                for (int dh = 0; dh < 2; ++dh)
+                for (int p = 0; p < 2; ++p)
 #pragma unroll
-                  for (int acc = 0; acc < 2; ++acc) {
+                  for (int dh = 0; dh < 2; ++dh) {
                     const int row =
-                        (((((s * 2 + int(rank)) * a.GR + tr) * a.GC + tc) * 4) + 2 * acc + dh) * a.R + rh * 64;
-                    tma_load_2d_pair(dst + (dh * 2 + acc) * kBHalf, &mapB, fb, kb * 128, row);
+                        (((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) + 2 * int(rank) + dh) * a.R + rh * 64;
+                    tma_load_2d_pair(dst + (p * 2 + dh) * kBHalf, &mapB, fb, kb * 128, row);
                   }
               }
               __syncwarp();
@@ -260,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0) {  // ------ MMA issuer (leader CTA; converged warp, one lane issues)
-      constexpr uint32_t idesc = idesc_i8(256, 256, /*b_mn_major=*/false);
+      constexpr uint32_t idesc = idesc_i8(256, 128, /*b_mn_major=*/false);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
         for (int tc = 0; tc < a.GC; ++tc) {
@@ -268,8 +270,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + as * kAStage);
           for (int s = 0; s < a.S; ++s) {
+            // both polarities' accumulators, then the k-blocks of one B stage
             mbar_wait(&t_empty[ab], abph ^ 1);
-            const uint32_t td = tmem + ab * 256;
+            const uint32_t ab1 = ab + 1 == kTBufs ? 0 : ab + 1;
+            const uint32_t abph1 = ab + 1 == kTBufs ? abph ^ 1 : abph;
+            mbar_wait(&t_empty[ab1], abph1 ^ 1);
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&b_full[bs], bph);
@@ -277,19 +282,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint32_t b0 = smem_u32(sB + bs * kBStage);
               if (elect_one()) {
 #pragma unroll
-                for (int dh = 0; dh < 2; ++dh)
+                for (int p = 0; p < 2; ++p) {
+                  const uint32_t td = tmem + (p == 0 ? ab : ab1) * 128;
 #pragma unroll
-                  for (int ks = 0; ks < 4; ++ks) {
-                    const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kPlane + 32 * ks, 16, 1024, 2);
-                    const uint64_t bd = sdesc(b0 + dh * 2 * kBHalf + 32 * ks, 16, 1024, 2);
-                    umma_i8_pair(td, ad, bd, idesc, (kb | dh | ks) != 0);
-                  }
+                  for (int dh = 0; dh < 2; ++dh)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                      const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kPlane + 32 * ks, 16, 1024, 2);
+                      const uint64_t bd = sdesc(b0 + (p * 2 + dh) * kBHalf + 32 * ks, 16, 1024, 2);
+                      umma_i8_pair(td, ad, bd, idesc, (kb | dh | ks) != 0);
+                    }
+                  if (kb == KB - 1) umma_commit_pair(&t_full[p == 0 ? ab : ab1]);
+                }
                 umma_commit_pair(&b_empty[bs]);
-                if (kb == KB - 1) umma_commit_pair(&t_full[ab]);
               }
               __syncwarp();
               if (++bs == kBStages) { bs = 0; bph ^= 1; }
             }
+            ab = ab1;
+            abph = abph1;
             if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           }
           if (elect_one()) umma_commit_pair(&a_empty[as]);
@@ -335,24 +346,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
         const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
-        mbar_wait_hint(&t_full[ab], abph);
-        tc_fence_after();
-        const uint32_t ta = tl + ab * 256;
         uint32_t lo[kRows], hi[kRows];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+          const uint32_t ta = tl + ab * 128;
 #pragma unroll
           for (int h = 0; h < kRows / 16; ++h) {
-            tmem_ld16(ta + 128 * p + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
-            tmem_ld16(ta + 128 * p + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+            tmem_ld16(ta + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
+            tmem_ld16(ta + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
           }
           tmem_wait_ld();
-          if (p == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           const float wp = p == 0 ? wpos : wneg;
           adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
           adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
