@@ -254,8 +254,8 @@ static __device__ __noinline__ float adc_fix(uint32_t hi, uint32_t lo, float t, 
                                              int maxc) {
   const unsigned long long n = (unsigned long long)hi * 65025ull + lo;
   int c = int(t);
-  if (c < maxc && n >= tab[c + 1]) ++c;  // tab: shared-memory copy or global (generic loads)
-  else if (c > 0 && n < tab[c]) --c;
+  if (c < maxc && n >= __ldg(tab + c + 1)) ++c;
+  else if (c > 0 && n < __ldg(tab + c)) --c;
   return float(c);
 }
 
