@@ -252,11 +252,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
         if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-        adc_conv8<0>(lo, hi, k, w, P, 0, exact);
-        adc_conv8<8>(lo, hi, k, w, P, 8, exact);
+        adc_conv8<0, kCPW, kCPW, 16>(lo, hi, k, w, P, 0, exact);
         if constexpr (kCPW >= 32) {
-          adc_conv8<16>(lo, hi, k, w, P, 16, exact);
-          adc_conv8<24>(lo, hi, k, w, P, 24, exact);
+          adc_conv8<16, kCPW, kCPW, 16>(lo, hi, k, w, P, 16, exact);
         }
         if constexpr (kCPW >= 64) {
           adc_conv8<32>(lo, hi, k, w, P, 32, exact);

@@ -282,18 +282,18 @@ __device__ __forceinline__ void adc_pair(uint32_t lo0, uint32_t lo1, uint32_t hi
 // in registers; if any lane saw a residual beyond thr, the warp visits the
 // eight and replaces the flagged codes (P += w * (exact - fast); all
 // operands exact).
-template <int OFF, int NL, int kN>
+template <int OFF, int NL, int kN, int G = 8>
 __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32_t (&hi)[NL], const AdcConst& k,
                                           float w, float (&P)[kN], int b, uint32_t& exact_ctr) {
-  float mr = 0.f, t[8], r[8];
+  float mr = 0.f, t[G], r[G];
   const uint64_t w2 = (uint64_t(__float_as_uint(w)) << 32) | __float_as_uint(w);
 #pragma unroll
-  for (int j = 0; j < 8; j += 2)
+  for (int j = 0; j < G; j += 2)
     adc_pair(lo[OFF + j], lo[OFF + j + 1], hi[OFF + j], hi[OFF + j + 1], k, w2, P[b + j], P[b + j + 1], mr, t[j],
              t[j + 1], r[j], r[j + 1]);
   if (__any_sync(0xffffffffu, mr > k.thr)) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < G; ++j) {
       if (fabsf(r[j]) > k.thr) {
         ++exact_ctr;
         const float code = adc_fix(hi[OFF + j], lo[OFF + j], __fmul_rn(t[j], k.unscale), k.tab, k.maxc_i);
