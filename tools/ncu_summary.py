@@ -17,7 +17,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = {"k_fwd_tc": "fwd_vmm", "k_bwd_tc": "bwd_vmm", "k_dw_tc": "dw", "k_dw": "dw", "k_update4": "update",
+STAGE = {"k_fwd_tc": "fwd_vmm", "k_bwd_tc": "bwd_vmm", "k_dw_tc": "dw", "k_dw": "dw", "k_update4": "update", "k_update": "update",
          "k_prep_x": "prep_x", "k_prep_dy": "prep_dy"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
