@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--all-layers", action="store_true",
                    help="every layer of the config (C1/C3/C4 networks), one core per layer on one stream")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
+    p.add_argument("--conv", action="store_true",
+                   help="C3/C4 as convolutions: CrossbarConv2d with device im2col/col2im (SURVEY 8f row 2)")
     return p.parse_args()
 
 
@@ -236,6 +238,101 @@ def run_reference(args, cfg):
 
 
 # ----------------------------------------------------------------- ours
+def run_conv(args, cfg):
+    """C3/C4 stepped as the reference's layer types: every conv layer a
+    CrossbarConv2d (device im2col -> core -> col2im, layers.cpp:415-505),
+    the fc a CrossbarLinear core, all on one stream with device tensors.
+    Reports the same metric over the same MACs as --all-layers; the time the
+    cores do not account for is the lowering glue."""
+    import torch
+    from paper_2002_11151_b200 import xbarsim as xb
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    init_dist(world, local_rank, "nccl")
+    opt = cfg.options()
+    mods, bufs = [], []
+    for li, L in enumerate(cfg.layers):
+        W = cfg.weights(L, li)
+        cv = L.conv
+        if cv is not None:
+            m = xb.CrossbarConv2d(W, cv.in_c, cv.out_c, cv.k, cv.stride, cv.pad, opt)
+            oh, ow = m.output_dims(cv.h, cv.w)
+            n_in, n_out, batch = cv.in_c * cv.h * cv.w, cv.out_c * oh * ow, cv.batch
+        else:
+            m = xb.CrossbarCore(W, opt)
+            n_in, n_out, batch = L.K, L.N, L.M
+        g = torch.Generator().manual_seed(1000 + li)
+        x = torch.randn((n_in, batch), generator=g, dtype=torch.float64).cuda()  # batch x n_in column-major
+        dy = torch.randn((n_out, batch), generator=g, dtype=torch.float64).cuda()
+        y = torch.empty((n_out, batch), dtype=torch.float64, device="cuda")
+        dx = torch.empty((n_in, batch), dtype=torch.float64, device="cuda")
+        mods.append(m)
+        bufs.append((L, batch, x, dy, y, dx))
+    cores = [m.core() if isinstance(m, xb.CrossbarConv2d) else m for m in mods]
+    for c in cores[1:]:
+        c.set_stream(cores[0].stream())
+    stream = torch.cuda.ExternalStream(cores[0].stream())
+    it = [0]
+
+    def step():
+        for m, (L, batch, x, dy, y, dx) in zip(mods, bufs):
+            if L.conv is not None:
+                m.forward_device(x.data_ptr(), batch, L.conv.in_c, L.conv.h, L.conv.w, True, y.data_ptr())
+            else:
+                m.forward_device(x.data_ptr(), batch, True, y.data_ptr())
+        for m, (L, batch, x, dy, y, dx) in reversed(list(zip(mods, bufs))):
+            if L.conv is not None:
+                m.backward_device(dy.data_ptr(), batch, dx.data_ptr())
+            else:
+                m.backward_device(dy.data_ptr(), batch, 1.0, dx.data_ptr())
+        for c in cores:
+            c.apply_updates_device(it[0])
+        it[0] += 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    for c in cores:
+        c.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, "cuda")
+    core_ms = 0.0
+    stages = {}
+    for c in cores:
+        for k, (t, n) in c.stage_times().items():
+            stages[k] = stages.get(k, 0.0) + t / args.steps
+            core_ms += t / args.steps
+    clk = clocks.stop()
+    macs = 0
+    for L in cfg.layers:
+        macs += cfg.macs(L)["total"]
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": world * macs / (ms * 1e-3), "unit": "MAC/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic N(0,1) images and errors",
+            "config": {"workload": cfg.name.replace("-im2col", "") + "-conv",
+                       "lowering": "CrossbarConv2d: device im2col / col2im around one core per layer",
+                       "layers": [[L.name, L.M, L.K, L.N] for L in cfg.layers], "parallelism": f"replicas{world}"},
+            "stage_ms": stages, "core_ms": core_ms, "glue_ms": ms - core_ms, "clocks": clk}))
+    for c in cores[1:]:  # the first core owns the shared stream: detach before teardown
+        c.set_stream(None)
+    torch.cuda.synchronize()
+    del cores
+    while mods:
+        mods.pop()
+
+
 def main():
     args = parse()
     from paper_2002_11151_b200.configs import CONFIGS
@@ -243,6 +340,9 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+        return
+    if args.conv:
+        run_conv(args, cfg)
         return
 
     import torch
@@ -426,6 +526,9 @@ def main():
                                 "sample": desc + f"; 3 steps, {3 * dt:.1f} s of CPU work"}
     if rank == 0:
         print(json.dumps(line))
+    for c in cores[1:]:  # the first core owns the shared stream: detach before teardown
+        c.set_stream(None)
+    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -20,11 +20,26 @@ from .xbarsim import CrossbarLayerOptions, EngineKind
 
 
 @dataclasses.dataclass
+class Conv:
+    """Convolution behind an im2col layer (CrossbarConv2d, layers.cpp:415-505):
+    M = batch * out_h * out_w, K = in_c * k * k, N = out_c."""
+    in_c: int
+    out_c: int
+    k: int
+    stride: int
+    pad: int
+    h: int
+    w: int
+    batch: int
+
+
+@dataclasses.dataclass
 class Layer:
     name: str
     M: int
     K: int
     N: int
+    conv: Conv | None = None
 
 
 @dataclasses.dataclass
@@ -94,24 +109,39 @@ class Config:
         return {"fwd": f, "bwd": b, "upd": u, "total": f + b + u}
 
 
+def _conv(name: str, cv: Conv) -> Layer:
+    oh = (cv.h + 2 * cv.pad - cv.k) // cv.stride + 1
+    ow = (cv.w + 2 * cv.pad - cv.k) // cv.stride + 1
+    return Layer(name, cv.batch * oh * ow, cv.in_c * cv.k * cv.k, cv.out_c, cv)
+
+
 def _c3_layers() -> List[Layer]:
-    L = [Layer("conv1", 131072, 27, 16)]
-    L += [Layer(f"s1.{i}", 131072, 144, 16) for i in range(6)]
-    L += [Layer("s2.0", 32768, 144, 32)] + [Layer(f"s2.{i}", 32768, 288, 32) for i in range(1, 6)]
-    L += [Layer("s3.0", 8192, 288, 64)] + [Layer(f"s3.{i}", 8192, 576, 64) for i in range(1, 6)]
+    """ResNet-20 on 32x32 inputs, batch 128, 3x3 convs with padding 1."""
+    B = 128
+    L = [_conv("conv1", Conv(3, 16, 3, 1, 1, 32, 32, B))]
+    L += [_conv(f"s1.{i}", Conv(16, 16, 3, 1, 1, 32, 32, B)) for i in range(6)]
+    L += [_conv("s2.0", Conv(16, 32, 3, 2, 1, 32, 32, B))]
+    L += [_conv(f"s2.{i}", Conv(32, 32, 3, 1, 1, 16, 16, B)) for i in range(1, 6)]
+    L += [_conv("s3.0", Conv(32, 64, 3, 2, 1, 16, 16, B))]
+    L += [_conv(f"s3.{i}", Conv(64, 64, 3, 1, 1, 8, 8, B)) for i in range(1, 6)]
     L += [Layer("fc", 128, 64, 10)]
     return L
 
 
 def _c4_layers() -> List[Layer]:
-    L = [Layer("conv1", 401408, 147, 64)]
-    L += [Layer(f"layer1.{i}", 100352, 576, 64) for i in range(4)]
-    L += [Layer("layer2.0", 25088, 576, 128)] + [Layer(f"layer2.{i}", 25088, 1152, 128) for i in range(1, 4)]
-    L += [Layer("layer2.ds", 25088, 64, 128)]
-    L += [Layer("layer3.0", 6272, 1152, 256)] + [Layer(f"layer3.{i}", 6272, 2304, 256) for i in range(1, 4)]
-    L += [Layer("layer3.ds", 6272, 128, 256)]
-    L += [Layer("layer4.0", 1568, 2304, 512)] + [Layer(f"layer4.{i}", 1568, 4608, 512) for i in range(1, 4)]
-    L += [Layer("layer4.ds", 1568, 256, 512)]
+    """ResNet-18 on 224x224 inputs, batch 32 (conv1 7x7/2, then 56x56 after the pool)."""
+    B = 32
+    L = [_conv("conv1", Conv(3, 64, 7, 2, 3, 224, 224, B))]
+    L += [_conv(f"layer1.{i}", Conv(64, 64, 3, 1, 1, 56, 56, B)) for i in range(4)]
+    L += [_conv("layer2.0", Conv(64, 128, 3, 2, 1, 56, 56, B))]
+    L += [_conv(f"layer2.{i}", Conv(128, 128, 3, 1, 1, 28, 28, B)) for i in range(1, 4)]
+    L += [_conv("layer2.ds", Conv(64, 128, 1, 2, 0, 56, 56, B))]
+    L += [_conv("layer3.0", Conv(128, 256, 3, 2, 1, 28, 28, B))]
+    L += [_conv(f"layer3.{i}", Conv(256, 256, 3, 1, 1, 14, 14, B)) for i in range(1, 4)]
+    L += [_conv("layer3.ds", Conv(128, 256, 1, 2, 0, 28, 28, B))]
+    L += [_conv("layer4.0", Conv(256, 512, 3, 2, 1, 14, 14, B))]
+    L += [_conv(f"layer4.{i}", Conv(512, 512, 3, 1, 1, 7, 7, B)) for i in range(1, 4)]
+    L += [_conv("layer4.ds", Conv(256, 512, 1, 2, 0, 14, 14, B))]
     L += [Layer("fc", 32, 512, 1000)]
     return L
 

@@ -562,6 +562,19 @@ class CrossbarConv2d(Layer):
     def apply_updates(self, iteration: int) -> None:
         _check(load_library().xbs_conv2d_apply_updates(self._h, int(iteration)))
 
+    # ---- B200 extensions: device tensors (batch x features column-major),
+    # enqueued on the core's stream
+    def forward_device(self, d_x: int, batch: int, c: int, h: int, w: int, training: bool, d_y: int) -> None:
+        _check(load_library().xbs_conv2d_forward_device(self._h, d_x, batch, c, h, w, int(bool(training)), d_y))
+
+    def backward_device(self, d_dy: int, batch: int, d_dx: int) -> None:
+        _check(load_library().xbs_conv2d_backward_device(self._h, d_dy, batch, d_dx))
+
+    def output_dims(self, h: int, w: int):
+        oh, ow = ctypes.c_int32(), ctypes.c_int32()
+        _check(load_library().xbs_conv2d_output_dims(self._h, h, w, ctypes.byref(oh), ctypes.byref(ow)))
+        return oh.value, ow.value
+
     def core(self) -> CrossbarCore:
         return self._core
 
