@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--all-layers", action="store_true",
                    help="every layer of the config (C1/C3/C4 networks), one core per layer on one stream")
     p.add_argument("--traffic", default=None, help="json with ncu dram bytes per launch for the dominant kernel")
+    p.add_argument("--calibrate", type=int, default=0, metavar="BATCHES",
+                   help="ADC auto-calibration (SURVEY 8f row 3): adc.i_fs unset, BATCHES calibration steps, then "
+                        "the freeze step and --steps quantised steps, each timed")
     p.add_argument("--conv", action="store_true",
                    help="C3/C4 as convolutions: CrossbarConv2d with device im2col/col2im (SURVEY 8f row 2)")
     return p.parse_args()
@@ -333,6 +336,67 @@ def run_conv(args, cfg):
         mods.pop()
 
 
+def run_calibrate(args, cfg):
+    """ADC auto-calibration on the device: pass-through calibration steps
+    (currents recorded), the freeze (exact nearest-rank select over the
+    record), then quantised steps.  Every layer of the config, one stream."""
+    import torch
+    from paper_2002_11151_b200 import xbarsim as xb
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    init_dist(world, local_rank, "nccl")
+    opt = cfg.options()
+    opt.adc.i_fs = 0.0
+    opt.adc_cal_batches = args.calibrate
+    cores, dev = [], []
+    for li, L in enumerate(cfg.layers):
+        cores.append(xb.CrossbarCore(cfg.weights(L, li), opt))
+        x, dy = cfg.inputs(L, li), cfg.errors(L, li)
+        dev.append((L, torch.from_numpy(np.ascontiguousarray(x.T)).cuda(),
+                    torch.from_numpy(np.ascontiguousarray(dy.T)).cuda(),
+                    torch.empty((L.N, L.M), dtype=torch.float64, device="cuda"),
+                    torch.empty((L.K, L.M), dtype=torch.float64, device="cuda")))
+    for c in cores[1:]:
+        c.set_stream(cores[0].stream())
+    it = [0]
+
+    def step():
+        for c, (L, x, dy, y, dx) in zip(cores, dev):
+            c.forward_device(x.data_ptr(), L.M, True, y.data_ptr())
+        for c, (L, x, dy, y, dx) in reversed(list(zip(cores, dev))):
+            c.backward_device(dy.data_ptr(), L.M, 1.0, dx.data_ptr())
+        for c in cores:
+            c.apply_updates_device(it[0])
+        it[0] += 1
+
+    def timed(n):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            step()
+        for c in cores:
+            c.synchronize()
+        return (time.perf_counter() - t0) * 1e3 / max(1, n)
+
+    cal_ms = timed(args.calibrate)       # pass-through, currents recorded
+    freeze_ms = timed(1)                 # freeze (select) + first quantised step
+    q_ms = timed(args.steps)
+    macs = sum(cfg.macs(L)["total"] for L in cfg.layers)
+    fs = [c.forward_adc_full_scale() for c in cores]
+    for c in cores[1:]:
+        c.set_stream(None)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "ADC auto-calibration step time", "unit": "ms", "higher_is_better": False,
+            "n_gpus": world, "steps": args.steps, "warmup": 0, "data": "synthetic",
+            "config": {"workload": cfg.name + "-autocal", "adc_cal_batches": args.calibrate,
+                       "layers": [[L.M, L.K, L.N] for L in cfg.layers]},
+            "calibration_step_ms": cal_ms, "freeze_step_ms": freeze_ms, "quantised_step_ms": q_ms,
+            "quantised_macs_per_s": macs / (q_ms * 1e-3), "frozen_forward_i_fs": fs,
+            "timing": "host wall clock around synchronised steps"}))
+
+
 def main():
     args = parse()
     from paper_2002_11151_b200.configs import CONFIGS
@@ -343,6 +407,9 @@ def main():
         return
     if args.conv:
         run_conv(args, cfg)
+        return
+    if args.calibrate:
+        run_calibrate(args, cfg)
         return
 
     import torch
