@@ -1,5 +1,6 @@
-// CrossbarConv2d (layers.cpp:415-505) on the device: im2col as a gather, the
-// crossbar core on the patch matrix, and the inverse layouts.  Tensors follow
+// CrossbarConv2d (layers.cpp:415-505) on the device: im2col fused into the
+// core's input quantisation (the patch matrix is never written), the crossbar
+// core, and the inverse layouts.  Tensors follow
 // the reference: values are batch x features, column-major (Eigen), features
 // ordered (c, y, x); the patch matrix is (batch * oh * ow) x (in_c * k * k)
 // with rows (b, oy, ox) and columns (c, ky, kx).
@@ -27,56 +28,63 @@ struct xbs_conv2d {
 namespace xbs {
 namespace {
 
-__global__ void k_im2col(const double* __restrict__ x, int64_t batch, int c_in, int h, int w, int k, int stride,
-                         int pad, int oh, int ow, double* __restrict__ patch) {
-  const int64_t rows = batch * oh * ow, cols = int64_t(c_in) * k * k;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < rows * cols; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = e % rows, col = e / rows;  // column-major patch matrix
-    const int ox = int(r % ow), oy = int((r / ow) % oh);
-    const int64_t b = r / (int64_t(oh) * ow);
-    const int kx = int(col % k), ky = int((col / k) % k), c = int(col / (int64_t(k) * k));
-    const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
-    double v = 0.0;
-    if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = x[((int64_t(c) * h + iy) * w + ix) * batch + b];
-    patch[e] = v;
-  }
-}
-
-// flat (rows x out_c) <-> tensor (batch x out_c*oh*ow), both column-major
-__global__ void k_flat_to_tensor(const double* __restrict__ flat, int64_t batch, int out_c, int oh, int ow,
+// flat (rows x out_c) <-> tensor (batch x out_c*oh*ow), both column-major.
+// Thread order follows the flat matrix (r fastest) so its side is coalesced.
+template <typename I>  // index type: int when every index fits, else int64_t
+__global__ void k_flat_to_tensor(const double* __restrict__ flat, I batch, int out_c, int oh, int ow,
                                  double* __restrict__ y, int to_tensor) {
-  const int64_t rows = batch * oh * ow, n = rows * out_c;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = e % batch, f = e / batch;  // tensor element (b, f), f = (oc, oy, ox)
-    const int ox = int(f % ow), oy = int((f / ow) % oh), oc = int(f / (int64_t(oh) * ow));
-    const int64_t r = (b * oh + oy) * ow + ox;
-    if (to_tensor) y[e] = flat[int64_t(oc) * rows + r];
-    else y[int64_t(oc) * rows + r] = flat[e];  // (here `flat` is the tensor and `y` the flat matrix)
+  const I hw = I(oh) * ow, rows = batch * hw, n = rows * out_c;
+  for (I e = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); e < n; e += I(gridDim.x) * I(blockDim.x)) {
+    const I oc = e / rows, r = e - oc * rows;  // flat element (r, oc), r = (b, oy, ox)
+    const I b = r / hw, pos = r - b * hw;
+    const I t = (oc * hw + pos) * batch + b;  // tensor element (b, f), f = (oc, oy, ox)
+    if (to_tensor) y[t] = flat[e];
+    else y[e] = flat[t];  // (here `flat` is the tensor and `y` the flat matrix)
   }
 }
 
-__global__ void k_col2im(const double* __restrict__ dpatch, int64_t batch, int c_in, int h, int w, int k, int stride,
+// col2im as a gather: each input element sums its patch entries in
+// increasing (oy, ox) order -- the reference's scatter order
+// (layers.cpp:486-502) -- visiting only the (oy, ox) whose window covers it.
+template <typename I>
+__global__ void k_col2im(const double* __restrict__ dpatch, I batch, int c_in, int h, int w, int k, int stride,
                          int pad, int oh, int ow, double* __restrict__ dx) {
-  const int64_t rows = batch * oh * ow, n = batch * int64_t(c_in) * h * w;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = e % batch, f = e / batch;
-    const int ix = int(f % w), iy = int((f / w) % h), c = int(f / (int64_t(h) * w));
+  const I rows = batch * oh * ow, n = batch * I(c_in) * h * w;
+  for (I e = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); e < n; e += I(gridDim.x) * I(blockDim.x)) {
+    // ix fastest: neighbouring threads read neighbouring patch rows
+    const int ix = int(e % w);
+    const I e2 = e / w;
+    const int iy = int(e2 % h);
+    const I e3 = e2 / h;
+    const int c = int(e3 % c_in);
+    const I b = e3 / c_in;
+    const int ny = iy + pad - k + 1, nx = ix + pad - k + 1;
+    const int oy0 = ny <= 0 ? 0 : (ny + stride - 1) / stride, oy1 = min(oh - 1, (iy + pad) / stride);
+    const int ox0 = nx <= 0 ? 0 : (nx + stride - 1) / stride, ox1 = min(ow - 1, (ix + pad) / stride);
     double acc = 0.0;
-    for (int oy = 0; oy < oh; ++oy) {
+    for (int oy = oy0; oy <= oy1; ++oy) {
       const int ky = iy + pad - oy * stride;
-      if (ky < 0 || ky >= k) continue;
-      for (int ox = 0; ox < ow; ++ox) {
+      for (int ox = ox0; ox <= ox1; ++ox) {
         const int kx = ix + pad - ox * stride;
-        if (kx < 0 || kx >= k) continue;
-        const int64_t r = (b * oh + oy) * ow + ox;
-        acc += dpatch[((int64_t(c) * k + ky) * k + kx) * rows + r];
+        const int64_t r = (int64_t(b) * oh + oy) * ow + ox;
+        acc += dpatch[((int64_t(c) * k + ky) * k + kx) * int64_t(rows) + r];
       }
     }
-    dx[e] = acc;
+    dx[((int64_t(c) * h + iy) * w + ix) * int64_t(batch) + b] = acc;
   }
 }
 
 int blocks_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
+
+void flat_to_tensor(const double* src, int64_t batch, int out_c, int oh, int ow, double* dst, int to_tensor,
+                    cudaStream_t st) {
+  const int64_t n = batch * oh * ow * out_c;
+  if (n <= 0) return;
+  if (n < (int64_t(1) << 31))
+    k_flat_to_tensor<int><<<blocks_for(n), 256, 0, st>>>(src, int(batch), out_c, oh, ow, dst, to_tensor);
+  else
+    k_flat_to_tensor<int64_t><<<blocks_for(n), 256, 0, st>>>(src, batch, out_c, oh, ow, dst, to_tensor);
+}
 
 void grow(double*& p, int64_t& cap, int64_t n) {
   if (cap >= n) return;
@@ -147,16 +155,13 @@ int xbs_conv2d_forward_device(xbs_conv2d* c, const double* d_x, int64_t batch, i
     c->out_w = ow;
     c->batch = batch;
     cudaStream_t st = static_cast<cudaStream_t>(xbs_core_stream(c->core));
-    const int64_t rows = batch * oh * ow, kk = int64_t(c->in_c) * c->k * c->k;
-    xbs::grow(c->d_patch, c->cap_patch, rows * kk);
+    const int64_t rows = batch * oh * ow;
     xbs::grow(c->d_flat, c->cap_flat, rows * c->out_c);
-    if (rows * kk > 0)
-      xbs::k_im2col<<<xbs::blocks_for(rows * kk), 256, 0, st>>>(d_x, batch, c->in_c, h, w, c->k, c->stride, c->pad,
-                                                                  oh, ow, c->d_patch);
-    xbs::check_rc(xbs_core_forward_device(c->core, c->d_patch, rows, training, c->d_flat));
-    if (rows * c->out_c > 0)
-      xbs::k_flat_to_tensor<<<xbs::blocks_for(rows * c->out_c), 256, 0, st>>>(c->d_flat, batch, c->out_c, oh, ow,
-                                                                               d_y, 1);
+    // im2col fused into the core's input quantisation: the patch matrix is
+    // never written (xbs_kernels.cu k_prep_x<true>)
+    const xbs::ConvSrc cs{c->in_c, h, w, c->k, c->stride, c->pad, oh, ow, batch};
+    xbs::core_forward_conv(c->core, d_x, cs, training != 0, c->d_flat);
+    xbs::flat_to_tensor(c->d_flat, batch, c->out_c, oh, ow, d_y, 1, st);
     c->have_forward = true;
   });
 }
@@ -170,15 +175,18 @@ int xbs_conv2d_backward_device(xbs_conv2d* c, const double* d_dy, int64_t batch,
     const int64_t rows = c->batch * c->out_h * c->out_w, kk = int64_t(c->in_c) * c->k * c->k;
     xbs::grow(c->d_flat, c->cap_flat, rows * c->out_c);
     xbs::grow(c->d_patch, c->cap_patch, rows * kk);
-    if (rows * c->out_c > 0)
-      xbs::k_flat_to_tensor<<<xbs::blocks_for(rows * c->out_c), 256, 0, st>>>(d_dy, c->batch, c->out_c, c->out_h,
-                                                                               c->out_w, c->d_flat, 0);
+    xbs::flat_to_tensor(d_dy, c->batch, c->out_c, c->out_h, c->out_w, c->d_flat, 0, st);
     // layers.cpp:483: grad_divisor 1.0
     xbs::check_rc(xbs_core_backward_device(c->core, c->d_flat, rows, 1.0, c->d_patch));
     const int64_t n = c->batch * int64_t(c->in_c) * c->in_h * c->in_w;
-    if (n > 0)
-      xbs::k_col2im<<<xbs::blocks_for(n), 256, 0, st>>>(c->d_patch, c->batch, c->in_c, c->in_h, c->in_w, c->k,
-                                                        c->stride, c->pad, c->out_h, c->out_w, d_dx);
+    if (n > 0) {
+      if (n < (int64_t(1) << 31))
+        xbs::k_col2im<int><<<xbs::blocks_for(n), 256, 0, st>>>(c->d_patch, int(c->batch), c->in_c, c->in_h, c->in_w,
+                                                               c->k, c->stride, c->pad, c->out_h, c->out_w, d_dx);
+      else
+        xbs::k_col2im<int64_t><<<xbs::blocks_for(n), 256, 0, st>>>(c->d_patch, c->batch, c->in_c, c->in_h, c->in_w,
+                                                                   c->k, c->stride, c->pad, c->out_h, c->out_w, d_dx);
+    }
   });
 }
 

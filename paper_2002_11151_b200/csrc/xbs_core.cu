@@ -171,6 +171,10 @@ void ensure_batch(xbs_core* c, int64_t M) {
   const int64_t rowsB = xbs::rows_bwd(cap, c->g.TPe);
   ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
   ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NI), "cudaMalloc A_bwd");
+  // the prep kernels never write 16-column groups that hold only tile
+  // padding: those plane bytes stay the zeros written here
+  ck(cudaMemsetAsync(c->d_Af, 0, size_t(2 * rowsF) * c->g.KI, c->stream), "memset A_fwd");
+  ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NI, c->stream), "memset A_bwd");
   ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
   ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int16_t)), "cudaMalloc ecodes");
   cudaFree(c->d_xc8);
@@ -358,7 +362,8 @@ void maybe_freeze_adc(xbs_core* c) {
 
 bool calibrating(const xbs_core* c) { return c->adc_auto && !c->adc_frozen; }
 
-void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y) {
+void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y,
+                    const xbs::ConvSrc* conv = nullptr) {
   if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
   maybe_freeze_adc(c);
   if (c->adc_auto && c->adc_frozen && !(c->adc.i_fs > 0) && M > 0)
@@ -366,7 +371,7 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, do
   ensure_batch(c, std::max<int64_t>(M, 1));
   {
     StageScope st(c, XBS_STAGE_PREP_X);
-    xbs::launch_prep_x(c, d_x, M, c->stream);
+    xbs::launch_prep_x(c, d_x, M, c->stream, conv);
     c->launches += M > 0 ? 1 : 0;
   }
   c->have_forward = true;
@@ -450,6 +455,14 @@ void finish_update_stats(xbs_core* c) {
 }
 
 }  // namespace
+
+namespace xbs {
+void core_forward_conv(xbs_core* c, const double* d_img, const ConvSrc& cs, bool training, double* d_y) {
+  const int64_t rows = cs.batch * cs.oh * cs.ow;
+  if (rows >= (int64_t(1) << 31)) fail(XBS_UNSUPPORTED, "CrossbarConv2d: more than 2^31 patch rows");
+  forward_device(c, d_img, rows, training, d_y, &cs);
+}
+}  // namespace xbs
 
 namespace xbs {  // error plumbing shared with the conv layer (xbs_conv.cu)
 int set_error(int code, const std::string& m) {

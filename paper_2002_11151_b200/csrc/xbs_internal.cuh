@@ -192,7 +192,18 @@ namespace xbs {
 void launch_map_weights(const xbs_core* c, const double* d_W, cudaStream_t st);
 void launch_absmax(const double* d_x, int64_t n, unsigned long long* out_bits, cudaStream_t st);
 void launch_regen_all(const xbs_core* c, cudaStream_t st);
-void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st);
+// Convolution input read in place of the patch matrix (CrossbarConv2d,
+// layers.cpp:442-458): patch row (img, oy, ox), column (c, ky, kx) is the
+// image element (c, oy*stride - pad + ky, ox*stride - pad + kx), or 0 in the
+// padding.  The image is batch x (in_c*h*w) column-major.
+struct ConvSrc {
+  int in_c, h, w, k, stride, pad, oh, ow;
+  int64_t batch;
+};
+void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st, const ConvSrc* conv = nullptr);
+// forward of a core whose input is the im2col lowering of an image (no patch
+// matrix is materialised); y is the rows x out_c column-major flat output
+void core_forward_conv(xbs_core* c, const double* d_img, const ConvSrc& cs, bool training, double* d_y);
 void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream_t st);
 void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
 void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);

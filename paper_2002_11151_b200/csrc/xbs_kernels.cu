@@ -525,19 +525,53 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 // are written as contiguous row segments.
 constexpr int kPrepTB = 64, kPrepTI = 64;
 
+template <bool CONV>
 __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF,
                                                 double step, double levels, uint16_t* __restrict__ codes,
-                                                uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8) {
+                                                uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8,
+                                                ConvSrc cv) {
   __shared__ uint16_t cs[kPrepTB][kPrepTI + 2];
+  __shared__ int coff[kPrepTI], cky[kPrepTI], ckx[kPrepTI];  // CONV: image offset and (ky, kx) per column
   const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
   const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. KI)
+  // CONV: this thread's patch row (blockDim.x is a multiple of kPrepTB, so
+  // bl = threadIdx.x % kPrepTB for every element it loads)
+  int img = 0, oys = 0, oxs = 0;
+  if constexpr (CONV) {
+    if (threadIdx.x < kPrepTI) {
+      const int col = c0 + threadIdx.x, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
+      if (r < g.tile_rows && i < g.K) {
+        const int kk = cv.k * cv.k, c = i / kk, ky = (i % kk) / cv.k, kx = i % cv.k;
+        coff[threadIdx.x] = (c * cv.h + ky) * cv.w + kx;
+        cky[threadIdx.x] = ky;
+        ckx[threadIdx.x] = kx;
+      }
+    }
+    const int64_t b = b0 + threadIdx.x % kPrepTB;
+    if (b < M) {
+      const int rb = int(b), ox = rb % cv.ow, t = rb / cv.ow, oy = t % cv.oh;
+      img = t / cv.oh;
+      oys = oy * cv.stride - cv.pad;
+      oxs = ox * cv.stride - cv.pad;
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
     const int bl = e % kPrepTB, il = e / kPrepTB;  // consecutive threads: consecutive batch rows
     const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
     const int64_t b = b0 + bl;
     uint32_t code = 0;
     if (b < M && r < g.tile_rows && i < g.K) {
-      double v = double(llround(x[int64_t(i) * M + b] / step));
+      double xv;
+      if constexpr (CONV) {
+        const int iy = oys + cky[il], ix = oxs + ckx[il];
+        xv = (iy >= 0 && iy < cv.h && ix >= 0 && ix < cv.w)
+                 ? x[int64_t(coff[il] + oys * cv.w + oxs) * cv.batch + img]
+                 : 0.0;
+      } else {
+        xv = x[int64_t(i) * M + b];
+      }
+      double v = double(llround(xv / step));
       if (v < 0) v = 0;
       if (v > levels) v = levels;
       code = uint32_t(v);
@@ -554,27 +588,43 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
       if (c8) c8[b * ld8 + i] = uint8_t(cs[bl][il]);
     }
   }
+  // bit planes: one thread per (batch row, 16 columns) packs the codes'
+  // bytes four to a word once; plane k is then (word >> k) & 0x01010101
   constexpr int Q = kPrepTI / 16;
-  for (int e = threadIdx.x; e < kPrepTB * g.TPi * Q; e += blockDim.x) {
-    const int q = e % Q, k = (e / Q) % g.TPi, bl = e / (Q * g.TPi);
+  for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
+    const int q = e % Q, bl = e / Q;
     const int64_t b = b0 + bl;
     if (b >= M) continue;
-    uint32_t w0[4];
+    {  // 16 columns of tile padding only: left as allocated (zero)
+      const int col = c0 + q * 16, r = col % g.R;
+      if (r >= g.tile_rows || (col / g.R) * g.tile_rows + r >= g.K) continue;
+    }
+    uint32_t lo8[4], hi8[4];
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t v = 0;
+      uint32_t l = 0, h = 0;
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) v |= ((uint32_t(cs[bl][q * 16 + q4 * 4 + qq]) >> k) & 1u) << (8 * qq);
-      w0[q4] = v;
+      for (int qq = 0; qq < 4; ++qq) {
+        const uint32_t v = cs[bl][q * 16 + q4 * 4 + qq];
+        l |= (v & 0xffu) << (8 * qq);
+        h |= (v >> 8) << (8 * qq);
+      }
+      lo8[q4] = l;
+      hi8[q4] = h;
     }
-    const int64_t row = b * g.TPi + k;
-    uint8_t* p0 = A + row * g.KI + c0 + q * 16;
-    *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    *reinterpret_cast<uint4*>(p0 + rowsF * g.KI) = make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
+    uint8_t* p0 = A + (b * g.TPi) * g.KI + c0 + q * 16;
+    for (int k = 0; k < g.TPi; ++k, p0 += g.KI) {
+      uint32_t w0[4];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) w0[q4] = ((k < 8 ? lo8[q4] >> k : hi8[q4] >> (k - 8))) & 0x01010101u;
+      *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+      *reinterpret_cast<uint4*>(p0 + rowsF * g.KI) =
+          make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
+    }
   }
 }
 
-void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st) {
+void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t st, const ConvSrc* conv) {
   const int64_t rowsF = rows_fwd(M, c->g.TPi);
   // zero the M-padding rows once per call (rows [M*TPi, rowsF))
   const int64_t pad0 = M * c->g.TPi;
@@ -589,8 +639,12 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
     const int64_t Mp = ((M + 127) / 128) * 128;
     if (Mp > M) cudaMemsetAsync(c->d_xc8 + M * c->KA, 0, size_t(Mp - M) * c->KA, st);
   }
-  k_prep_x<<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
-                                  c->d_Af, c->d_xc8, c->KA);
+  if (conv)
+    k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+                                          c->d_Af, c->d_xc8, c->KA, *conv);
+  else
+    k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+                                           c->d_Af, c->d_xc8, c->KA, ConvSrc{});
 }
 
 // ----------------------------------------------------------------- prep_dy
@@ -634,28 +688,50 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
       }
     }
   }
+  // bit planes of the plus / minus magnitudes, packed four bytes to a word
+  // once per (batch row, 16 columns) as in k_prep_x
   constexpr int Q = kPrepTI / 16;
-  for (int e = threadIdx.x; e < kPrepTB * g.TPe * 2 * Q; e += blockDim.x) {
-    const int q = e % Q, kp = (e / Q) % (2 * g.TPe), bl = e / (Q * 2 * g.TPe);
-    const int k = kp >> 1, phi = kp & 1;
+  for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
+    const int q = e % Q, bl = e / Q;
     const int64_t b = b0 + bl;
     if (b >= M) continue;
-    uint32_t w0[4];
+    {  // 16 columns of tile padding only: left as allocated (zero)
+      const int col = c0 + q * 16, cc = col % g.C;
+      if (cc >= g.tile_cols || (col / g.C) * g.tile_cols + cc >= g.N) continue;
+    }
+    uint32_t pl[4], ph[4], ml[4], mh[4];  // plus / minus magnitudes: low and high bytes
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t v = 0;
+      uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
         const int sm = cs[bl][q * 16 + q4 * 4 + qq];
-        const uint32_t mag = phi ? uint32_t(sm < 0 ? -sm : 0) : uint32_t(sm > 0 ? sm : 0);
-        v |= ((mag >> k) & 1u) << (8 * qq);
+        const uint32_t p = uint32_t(sm > 0 ? sm : 0), m = uint32_t(sm < 0 ? -sm : 0);
+        a0 |= (p & 0xffu) << (8 * qq);
+        a1 |= (p >> 8) << (8 * qq);
+        a2 |= (m & 0xffu) << (8 * qq);
+        a3 |= (m >> 8) << (8 * qq);
       }
-      w0[q4] = v;
+      pl[q4] = a0;
+      ph[q4] = a1;
+      ml[q4] = a2;
+      mh[q4] = a3;
     }
-    const int64_t row = (b * g.TPe + k) * 2 + phi;
-    uint8_t* p0 = A + row * g.NI + c0 + q * 16;
-    *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    *reinterpret_cast<uint4*>(p0 + rowsB * g.NI) = make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
+    uint8_t* p0 = A + (b * g.TPe * 2) * g.NI + c0 + q * 16;
+    for (int k = 0; k < g.TPe; ++k) {
+#pragma unroll
+      for (int phi = 0; phi < 2; ++phi, p0 += g.NI) {
+        uint32_t w0[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t lo = phi ? ml[q4] : pl[q4], hi = phi ? mh[q4] : ph[q4];
+          w0[q4] = (k < 8 ? lo >> k : hi >> (k - 8)) & 0x01010101u;
+        }
+        *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(p0 + rowsB * g.NI) =
+            make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
+      }
+    }
   }
 }
 
