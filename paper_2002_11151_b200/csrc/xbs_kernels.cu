@@ -523,11 +523,23 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 // of codes is staged in shared memory from coalesced column reads, then the
 // code rows, the u8 dW code plane and both bit-plane copies (bits, 255*bits)
 // are written as contiguous row segments.
-constexpr int kPrepTB = 64, kPrepTI = 64;
+constexpr int kPrepTB = 64, kPrepTI = 64, kPrepThreads = 256;
+
+// min(llround(v / step), levels) for v > 0 (tensor.cpp:8-51), without the
+// fp64 division on the common path: t = v * RN(1/step) is within 3 2^-53 t
+// of RN(v / step), so rint(t) is the answer unless t sits within 2^-40 of a
+// half-integer (then the exact quotient decides).
+__device__ __forceinline__ double quant_mag(double v, double step, double inv, double levels) {
+  const double t = v * inv;
+  if (t >= levels + 1.0) return levels;
+  const double k = rint(t);
+  if (fabs(t - k) < 0.5 - 0x1p-40) return fmin(k, levels);
+  return fmin(double(llround(v / step)), levels);
+}
 
 template <bool CONV>
 __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF,
-                                                double step, double levels, uint16_t* __restrict__ codes,
+                                                double step, double inv, double levels, uint16_t* __restrict__ codes,
                                                 uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8,
                                                 ConvSrc cv) {
   __shared__ uint16_t cs[kPrepTB][kPrepTI + 2];
@@ -556,27 +568,36 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+  // all of this thread's loads are issued before any is used (memory-level
+  // parallelism); blockDim.x == kPrepThreads
+  constexpr int kLd = kPrepTB * kPrepTI / kPrepThreads;
+  double xv[kLd];
+  bool live[kLd];
+#pragma unroll
+  for (int n = 0; n < kLd; ++n) {
+    const int e = threadIdx.x + n * kPrepThreads;
     const int bl = e % kPrepTB, il = e / kPrepTB;  // consecutive threads: consecutive batch rows
     const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
     const int64_t b = b0 + bl;
-    uint32_t code = 0;
-    if (b < M && r < g.tile_rows && i < g.K) {
-      double xv;
+    live[n] = b < M && r < g.tile_rows && i < g.K;
+    xv[n] = 0.0;
+    if (live[n]) {
       if constexpr (CONV) {
         const int iy = oys + cky[il], ix = oxs + ckx[il];
-        xv = (iy >= 0 && iy < cv.h && ix >= 0 && ix < cv.w)
-                 ? x[int64_t(coff[il] + oys * cv.w + oxs) * cv.batch + img]
-                 : 0.0;
+        if (iy >= 0 && iy < cv.h && ix >= 0 && ix < cv.w)
+          xv[n] = __ldg(x + int64_t(coff[il] + oys * cv.w + oxs) * cv.batch + img);
       } else {
-        xv = x[int64_t(i) * M + b];
+        xv[n] = __ldg(x + int64_t(i) * M + b);
       }
-      double v = double(llround(xv / step));
-      if (v < 0) v = 0;
-      if (v > levels) v = levels;
-      code = uint32_t(v);
     }
-    cs[bl][il] = uint16_t(code);
+  }
+#pragma unroll
+  for (int n = 0; n < kLd; ++n) {
+    const int e = threadIdx.x + n * kPrepThreads;
+    uint32_t code = 0;
+    // llround of a non-positive quotient is <= 0: code 0 (clamped)
+    if (live[n] && xv[n] > 0.0) code = uint32_t(quant_mag(xv[n], step, inv, levels));
+    cs[e % kPrepTB][e / kPrepTB] = uint16_t(code);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
@@ -635,15 +656,16 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
   if (M == 0) return;
   const dim3 grid(unsigned((M + kPrepTB - 1) / kPrepTB), unsigned(c->g.KI / kPrepTI));
   const double levels = double((1 << c->opt.act_bits) - 1);
+  const double step = c->opt.act_full_scale / levels;  // tensor.cpp:11
   if (c->d_xc8) {  // u8 code plane for the tcgen05 dW: rows [M, Mpad) must read 0
     const int64_t Mp = ((M + 127) / 128) * 128;
     if (Mp > M) cudaMemsetAsync(c->d_xc8 + M * c->KA, 0, size_t(Mp - M) * c->KA, st);
   }
   if (conv)
-    k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+    k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
                                           c->d_Af, c->d_xc8, c->KA, *conv);
   else
-    k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, c->opt.act_full_scale / levels, levels, c->d_xcodes,
+    k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
                                            c->d_Af, c->d_xc8, c->KA, ConvSrc{});
 }
 
@@ -658,21 +680,31 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
   __shared__ int16_t cs[kPrepTB][kPrepTI + 2];
   const double se = sc->se;
   const double step = se / levels;
+  const double inv = 1.0 / step;
   const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
   const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. NI)
-  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
+  constexpr int kLd = kPrepTB * kPrepTI / kPrepThreads;  // loads issued before use, as in k_prep_x
+  double dv[kLd];
+  bool live[kLd];
+#pragma unroll
+  for (int n = 0; n < kLd; ++n) {
+    const int e = threadIdx.x + n * kPrepThreads;
     const int bl = e % kPrepTB, il = e / kPrepTB;
     const int col = c0 + il, tc = col / g.C, cc = col % g.C, j = tc * g.tile_cols + cc;
     const int64_t b = b0 + bl;
+    live[n] = b < M && cc < g.tile_cols && j < g.N && se > 0;
+    dv[n] = live[n] ? __ldg(dy + int64_t(j) * M + b) : 0.0;
+  }
+#pragma unroll
+  for (int n = 0; n < kLd; ++n) {
+    const int e = threadIdx.x + n * kPrepThreads;
     int sm = 0;
-    if (b < M && cc < g.tile_cols && j < g.N && se > 0) {
-      const double v = dy[int64_t(j) * M + b];
-      double qq = double(llround(fabs(v) / step));
-      if (qq > levels) qq = levels;
-      const int mag = int(qq);
+    if (live[n] && dv[n] != 0.0) {
+      const double v = dv[n];
+      const int mag = int(quant_mag(fabs(v), step, inv, levels));
       sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
     }
-    cs[bl][il] = int16_t(sm);
+    cs[e % kPrepTB][e / kPrepTB] = int16_t(sm);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {

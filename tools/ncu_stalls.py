@@ -9,7 +9,16 @@ n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kern}"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr, data = rows[1], rows[2:]
+# one section per captured kernel instance: "Kernel Name" line, header, rows
+data, hdr = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        continue
+    if r and r[0] == "Address":
+        hdr = r
+        continue
+    if hdr is not None and len(r) == len(hdr):
+        data.append(r)
 ix = {h: i for i, h in enumerate(hdr)}
 S = "Warp Stall Sampling (All Samples)"
 tot = sum(float(r[ix[S]] or 0) for r in data)
