@@ -120,16 +120,38 @@ __device__ __forceinline__ uint32_t load_q(const uint8_t* digits, const Geo& g, 
 }
 
 // -------------------------------------------------------------- map_weights
-__global__ void k_absmax(const double* __restrict__ x, int64_t n, unsigned long long* out) {
+__global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ x, int64_t n,
+                                                unsigned long long* out) {
+  // four 16-byte loads in flight per thread
   double m = 0.0;
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
-    m = fmax(m, fabs(x[k]));
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (reinterpret_cast<uintptr_t>(x) & 15) {  // caller's device pointer not 16-byte aligned
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) m = fmax(m, fabs(x[k]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(out, m);
+    return;
+  }
+  const int64_t n2 = n / 2;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (; k + 3 * stride < n2; k += 4 * stride) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(x2 + k + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m = fmax(m, fmax(fabs(v[u].x), fabs(v[u].y)));
+  }
+  for (; k < n2; k += stride) {
+    const double2 v = __ldg(x2 + k);
+    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) m = fmax(m, fabs(x[n - 1]));
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) atomic_max_pos(out, m);
 }
 
 void launch_absmax(const double* d_x, int64_t n, unsigned long long* out_bits, cudaStream_t st) {
-  int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  int blocks = int(std::min<int64_t>((n / 2 + 255) / 256, 148 * 8));
   if (blocks < 1) blocks = 1;
   k_absmax<<<blocks, 256, 0, st>>>(d_x, n, out_bits);
 }
@@ -537,27 +559,37 @@ __device__ __forceinline__ double quant_mag(double v, double step, double inv, d
   return fmin(double(llround(v / step)), levels);
 }
 
+// The plane copies of a 16-column group are written when the group or its
+// 32-byte sector partner holds logical columns (a partial sector would make
+// L2 read the line back from HBM to merge it); groups whose whole sector is
+// tile padding are left as allocated (zero) and never touched.
+__device__ __forceinline__ bool plane_sector_live(int r16, int nlive) {
+  return (r16 & ~31) < nlive;  // r16: first block column of the group
+}
+
 template <bool CONV>
 __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF,
                                                 double step, double inv, double levels, uint16_t* __restrict__ codes,
                                                 uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8,
-                                                ConvSrc cv) {
+                                                ConvSrc cv, int64_t bt0) {
   __shared__ uint16_t cs[kPrepTB][kPrepTI + 2];
   __shared__ int coff[kPrepTI], cky[kPrepTI], ckx[kPrepTI];  // CONV: image offset and (ky, kx) per column
-  const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
-  const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. KI)
+  const int64_t b0 = (bt0 + blockIdx.y) * kPrepTB;
+  const int c0 = blockIdx.x * kPrepTI;  // column blocks fastest: a plane row's segments are written together  // device column (0 .. KI); a block lies in one row tile (R % 64 == 0)
+  const int tr = c0 / g.R, r0 = c0 % g.R;
+  const int i0 = tr * g.tile_rows + r0;  // logical feature of block column 0
+  const int nlive = min(kPrepTI, min(g.tile_rows - r0, g.K - i0));  // logical columns in this block
+  if (nlive <= 0) return;  // tile padding only: planes stay zero, no codes
   // CONV: this thread's patch row (blockDim.x is a multiple of kPrepTB, so
   // bl = threadIdx.x % kPrepTB for every element it loads)
   int img = 0, oys = 0, oxs = 0;
   if constexpr (CONV) {
-    if (threadIdx.x < kPrepTI) {
-      const int col = c0 + threadIdx.x, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
-      if (r < g.tile_rows && i < g.K) {
-        const int kk = cv.k * cv.k, c = i / kk, ky = (i % kk) / cv.k, kx = i % cv.k;
-        coff[threadIdx.x] = (c * cv.h + ky) * cv.w + kx;
-        cky[threadIdx.x] = ky;
-        ckx[threadIdx.x] = kx;
-      }
+    if (threadIdx.x < nlive) {
+      const int i = i0 + threadIdx.x;
+      const int kk = cv.k * cv.k, c = i / kk, ky = (i % kk) / cv.k, kx = i % cv.k;
+      coff[threadIdx.x] = (c * cv.h + ky) * cv.w + kx;
+      cky[threadIdx.x] = ky;
+      ckx[threadIdx.x] = kx;
     }
     const int64_t b = b0 + threadIdx.x % kPrepTB;
     if (b < M) {
@@ -571,62 +603,70 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
   // all of this thread's loads are issued before any is used (memory-level
   // parallelism); blockDim.x == kPrepThreads
   constexpr int kLd = kPrepTB * kPrepTI / kPrepThreads;
+  const int bl = threadIdx.x % kPrepTB, il0 = threadIdx.x / kPrepTB;  // consecutive threads: consecutive rows
+  const bool brow = b0 + bl < M;
   double xv[kLd];
-  bool live[kLd];
 #pragma unroll
   for (int n = 0; n < kLd; ++n) {
-    const int e = threadIdx.x + n * kPrepThreads;
-    const int bl = e % kPrepTB, il = e / kPrepTB;  // consecutive threads: consecutive batch rows
-    const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
-    const int64_t b = b0 + bl;
-    live[n] = b < M && r < g.tile_rows && i < g.K;
+    const int il = il0 + n * (kPrepThreads / kPrepTB);
     xv[n] = 0.0;
-    if (live[n]) {
+    if (brow && il < nlive) {
       if constexpr (CONV) {
         const int iy = oys + cky[il], ix = oxs + ckx[il];
         if (iy >= 0 && iy < cv.h && ix >= 0 && ix < cv.w)
           xv[n] = __ldg(x + int64_t(coff[il] + oys * cv.w + oxs) * cv.batch + img);
       } else {
-        xv[n] = __ldg(x + int64_t(i) * M + b);
+        xv[n] = __ldg(x + int64_t(i0 + il) * M + b0 + bl);
       }
     }
   }
 #pragma unroll
   for (int n = 0; n < kLd; ++n) {
-    const int e = threadIdx.x + n * kPrepThreads;
-    uint32_t code = 0;
-    // llround of a non-positive quotient is <= 0: code 0 (clamped)
-    if (live[n] && xv[n] > 0.0) code = uint32_t(quant_mag(xv[n], step, inv, levels));
-    cs[e % kPrepTB][e / kPrepTB] = uint16_t(code);
+    // llround of a non-positive quotient is <= 0: code 0 (clamped); columns
+    // beyond nlive load 0 and so hold code 0
+    const uint32_t code = xv[n] > 0.0 ? uint32_t(quant_mag(xv[n], step, inv, levels)) : 0u;
+    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = uint16_t(code);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
-    const int il = e % kPrepTI, bl = e / kPrepTI;  // consecutive threads: consecutive columns
-    const int col = c0 + il, tr = col / g.R, r = col % g.R, i = tr * g.tile_rows + r;
-    const int64_t b = b0 + bl;
-    if (b < M && r < g.tile_rows && i < g.K) {
-      codes[b * g.K + i] = cs[bl][il];
-      if (c8) c8[b * ld8 + i] = uint8_t(cs[bl][il]);
+  // codes [b][K] (u16) and the u8 dW codes [b][ld8]: one thread per (row, 8
+  // columns), vector stores where the row segment is 16-byte aligned
+  const bool vec = (g.K % 8) == 0 && (i0 % 8) == 0;
+  for (int e = threadIdx.x; e < kPrepTB * (kPrepTI / 8); e += blockDim.x) {
+    const int o = e % (kPrepTI / 8) * 8, r = e / (kPrepTI / 8);
+    const int64_t b = b0 + r;
+    if (b >= M || o >= nlive) continue;
+    const uint16_t* src = &cs[r][o];
+    if (vec && o + 8 <= nlive) {
+      uint32_t w[4], w8[2];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) w[h] = uint32_t(src[2 * h]) | (uint32_t(src[2 * h + 1]) << 16);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        w8[h] = (uint32_t(src[4 * h]) & 0xffu) | ((uint32_t(src[4 * h + 1]) & 0xffu) << 8) |
+                ((uint32_t(src[4 * h + 2]) & 0xffu) << 16) | (uint32_t(src[4 * h + 3]) << 24);
+      *reinterpret_cast<uint4*>(codes + b * g.K + i0 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (c8) *reinterpret_cast<uint2*>(c8 + b * ld8 + i0 + o) = make_uint2(w8[0], w8[1]);
+    } else {
+      for (int t = 0; t < 8 && o + t < nlive; ++t) {
+        codes[b * g.K + i0 + o + t] = src[t];
+        if (c8) c8[b * ld8 + i0 + o + t] = uint8_t(src[t]);
+      }
     }
   }
   // bit planes: one thread per (batch row, 16 columns) packs the codes'
   // bytes four to a word once; plane k is then (word >> k) & 0x01010101
   constexpr int Q = kPrepTI / 16;
   for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
-    const int q = e % Q, bl = e / Q;
-    const int64_t b = b0 + bl;
-    if (b >= M) continue;
-    {  // 16 columns of tile padding only: left as allocated (zero)
-      const int col = c0 + q * 16, r = col % g.R;
-      if (r >= g.tile_rows || (col / g.R) * g.tile_rows + r >= g.K) continue;
-    }
+    const int q = e % Q, r = e / Q;
+    const int64_t b = b0 + r;
+    if (b >= M || !plane_sector_live(q * 16, nlive)) continue;
     uint32_t lo8[4], hi8[4];
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       uint32_t l = 0, h = 0;
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t v = cs[bl][q * 16 + q4 * 4 + qq];
+        const uint32_t v = cs[r][q * 16 + q4 * 4 + qq];
         l |= (v & 0xffu) << (8 * qq);
         h |= (v >> 8) << (8 * qq);
       }
@@ -654,19 +694,22 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
     cudaMemsetAsync(c->d_Af + (rowsF + pad0) * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
   }
   if (M == 0) return;
-  const dim3 grid(unsigned((M + kPrepTB - 1) / kPrepTB), unsigned(c->g.KI / kPrepTI));
+  const int64_t nbt = (M + kPrepTB - 1) / kPrepTB;  // batch tiles, launched in chunks of gridDim.y <= 65535
   const double levels = double((1 << c->opt.act_bits) - 1);
   const double step = c->opt.act_full_scale / levels;  // tensor.cpp:11
   if (c->d_xc8) {  // u8 code plane for the tcgen05 dW: rows [M, Mpad) must read 0
     const int64_t Mp = ((M + 127) / 128) * 128;
     if (Mp > M) cudaMemsetAsync(c->d_xc8 + M * c->KA, 0, size_t(Mp - M) * c->KA, st);
   }
-  if (conv)
-    k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
-                                          c->d_Af, c->d_xc8, c->KA, *conv);
-  else
-    k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
-                                           c->d_Af, c->d_xc8, c->KA, ConvSrc{});
+  for (int64_t bt0 = 0; bt0 < nbt; bt0 += 65535) {
+    const dim3 grid(unsigned(c->g.KI / kPrepTI), unsigned(std::min<int64_t>(nbt - bt0, 65535)));
+    if (conv)
+      k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes, c->d_Af,
+                                            c->d_xc8, c->KA, *conv, bt0);
+    else
+      k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes, c->d_Af,
+                                             c->d_xc8, c->KA, ConvSrc{}, bt0);
+  }
 }
 
 // ----------------------------------------------------------------- prep_dy
@@ -676,68 +719,90 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
 __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB,
                                                  double levels, const DevScalars* __restrict__ sc,
                                                  int16_t* __restrict__ ecodes, uint8_t* __restrict__ A,
-                                                 uint8_t* __restrict__ e8, int64_t plane8, int ld8) {
+                                                 uint8_t* __restrict__ e8, int64_t plane8, int ld8, int64_t bt0) {
   __shared__ int16_t cs[kPrepTB][kPrepTI + 2];
   const double se = sc->se;
   const double step = se / levels;
   const double inv = 1.0 / step;
-  const int64_t b0 = int64_t(blockIdx.x) * kPrepTB;
-  const int c0 = blockIdx.y * kPrepTI;  // device column (0 .. NI)
+  const int64_t b0 = (bt0 + blockIdx.y) * kPrepTB;
+  const int c0 = blockIdx.x * kPrepTI;  // column blocks fastest: a plane row's segments are written together  // device column (0 .. NI); a block lies in one column tile
+  const int tc = c0 / g.C, cc0 = c0 % g.C;
+  const int j0 = tc * g.tile_cols + cc0;
+  const int nlive = min(kPrepTI, min(g.tile_cols - cc0, g.N - j0));
+  if (nlive <= 0) return;  // tile padding only
   constexpr int kLd = kPrepTB * kPrepTI / kPrepThreads;  // loads issued before use, as in k_prep_x
+  const int bl = threadIdx.x % kPrepTB, il0 = threadIdx.x / kPrepTB;
+  const bool brow = b0 + bl < M && se > 0;
   double dv[kLd];
-  bool live[kLd];
 #pragma unroll
   for (int n = 0; n < kLd; ++n) {
-    const int e = threadIdx.x + n * kPrepThreads;
-    const int bl = e % kPrepTB, il = e / kPrepTB;
-    const int col = c0 + il, tc = col / g.C, cc = col % g.C, j = tc * g.tile_cols + cc;
-    const int64_t b = b0 + bl;
-    live[n] = b < M && cc < g.tile_cols && j < g.N && se > 0;
-    dv[n] = live[n] ? __ldg(dy + int64_t(j) * M + b) : 0.0;
+    const int il = il0 + n * (kPrepThreads / kPrepTB);
+    dv[n] = brow && il < nlive ? __ldg(dy + int64_t(j0 + il) * M + b0 + bl) : 0.0;
   }
 #pragma unroll
   for (int n = 0; n < kLd; ++n) {
-    const int e = threadIdx.x + n * kPrepThreads;
     int sm = 0;
-    if (live[n] && dv[n] != 0.0) {
+    if (dv[n] != 0.0) {
       const double v = dv[n];
       const int mag = int(quant_mag(fabs(v), step, inv, levels));
       sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
     }
-    cs[e % kPrepTB][e / kPrepTB] = int16_t(sm);
+    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = int16_t(sm);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < kPrepTB * kPrepTI; e += blockDim.x) {
-    const int il = e % kPrepTI, bl = e / kPrepTI;
-    const int col = c0 + il, tc = col / g.C, cc = col % g.C, j = tc * g.tile_cols + cc;
-    const int64_t b = b0 + bl;
-    if (b < M && cc < g.tile_cols && j < g.N) {
-      const int sm = cs[bl][il];
-      ecodes[b * g.N + j] = int16_t(sm);
+  // signed codes [b][N] and the u8 plus / minus dW magnitudes, 8 columns per thread
+  const bool vec = (g.N % 8) == 0 && (j0 % 8) == 0;
+  for (int e = threadIdx.x; e < kPrepTB * (kPrepTI / 8); e += blockDim.x) {
+    const int o = e % (kPrepTI / 8) * 8, r = e / (kPrepTI / 8);
+    const int64_t b = b0 + r;
+    if (b >= M || o >= nlive) continue;
+    const int16_t* src = &cs[r][o];
+    if (vec && o + 8 <= nlive) {
+      uint32_t w[4], wp[2], wm[2];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) w[h] = uint32_t(uint16_t(src[2 * h])) | (uint32_t(uint16_t(src[2 * h + 1])) << 16);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t a = 0, m = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int v = src[4 * h + t];
+          a |= uint32_t(v > 0 ? v : 0) << (8 * t);
+          m |= uint32_t(v < 0 ? -v : 0) << (8 * t);
+        }
+        wp[h] = a;
+        wm[h] = m;
+      }
+      *reinterpret_cast<uint4*>(ecodes + b * g.N + j0 + o) = make_uint4(w[0], w[1], w[2], w[3]);
       if (e8) {
-        e8[b * ld8 + j] = uint8_t(sm > 0 ? sm : 0);
-        e8[plane8 + b * ld8 + j] = uint8_t(sm < 0 ? -sm : 0);
+        *reinterpret_cast<uint2*>(e8 + b * ld8 + j0 + o) = make_uint2(wp[0], wp[1]);
+        *reinterpret_cast<uint2*>(e8 + plane8 + b * ld8 + j0 + o) = make_uint2(wm[0], wm[1]);
+      }
+    } else {
+      for (int t = 0; t < 8 && o + t < nlive; ++t) {
+        const int sm = src[t];
+        ecodes[b * g.N + j0 + o + t] = int16_t(sm);
+        if (e8) {
+          e8[b * ld8 + j0 + o + t] = uint8_t(sm > 0 ? sm : 0);
+          e8[plane8 + b * ld8 + j0 + o + t] = uint8_t(sm < 0 ? -sm : 0);
+        }
       }
     }
   }
   // bit planes of the plus / minus magnitudes, packed four bytes to a word
-  // once per (batch row, 16 columns) as in k_prep_x
+  // once per (batch row, 16 columns) as in k_prep_x (full 32-byte sectors)
   constexpr int Q = kPrepTI / 16;
   for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
-    const int q = e % Q, bl = e / Q;
-    const int64_t b = b0 + bl;
-    if (b >= M) continue;
-    {  // 16 columns of tile padding only: left as allocated (zero)
-      const int col = c0 + q * 16, cc = col % g.C;
-      if (cc >= g.tile_cols || (col / g.C) * g.tile_cols + cc >= g.N) continue;
-    }
+    const int q = e % Q, r = e / Q;
+    const int64_t b = b0 + r;
+    if (b >= M || !plane_sector_live(q * 16, nlive)) continue;
     uint32_t pl[4], ph[4], ml[4], mh[4];  // plus / minus magnitudes: low and high bytes
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
       uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
-        const int sm = cs[bl][q * 16 + q4 * 4 + qq];
+        const int sm = cs[r][q * 16 + q4 * 4 + qq];
         const uint32_t p = uint32_t(sm > 0 ? sm : 0), m = uint32_t(sm < 0 ? -sm : 0);
         a0 |= (p & 0xffu) << (8 * qq);
         a1 |= (p >> 8) << (8 * qq);
@@ -782,7 +847,6 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
     cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
   }
   if (M == 0) return;
-  const dim3 grid(unsigned((M + kPrepTB - 1) / kPrepTB), unsigned(c->g.NI / kPrepTI));
   const int64_t plane8 = c->M_cap8 * c->NA;
   if (c->d_e8) {
     const int64_t Mp = ((M + 127) / 128) * 128;
@@ -791,8 +855,12 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
       cudaMemsetAsync(c->d_e8 + plane8 + M * c->NA, 0, size_t(Mp - M) * c->NA, st);
     }
   }
-  k_prep_dy<<<grid, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
-                                     c->d_ecodes, c->d_Ab, c->d_e8, plane8, c->NA);
+  const int64_t nbt = (M + kPrepTB - 1) / kPrepTB;
+  for (int64_t bt0 = 0; bt0 < nbt; bt0 += 65535) {
+    const dim3 grid(unsigned(c->g.NI / kPrepTI), unsigned(std::min<int64_t>(nbt - bt0, 65535)));
+    k_prep_dy<<<grid, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
+                                       c->d_ecodes, c->d_Ab, c->d_e8, plane8, c->NA, bt0);
+  }
 }
 
 // ---------------------------------------------------------------------- dW
