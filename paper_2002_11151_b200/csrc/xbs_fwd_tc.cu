@@ -196,7 +196,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
                     // apart, 32 K rows per MMA = 2 KB)
                     const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kABox + 32 * ks, 16, 1024, 2);
                     const uint64_t bd = sdesc(b0 + dh * kBBox + 2048 * ks, kBBox, 512, 4);
+#ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
                     umma_i8_pair(tmem + ab * 128, ad, bd, idesc, (kb | dh | ks) != 0);
+#else
+                    (void)ad; (void)bd;
+#endif
                   }
                 umma_commit_pair(&b_empty[bs]);
                 if (kb == KB - 1) umma_commit_pair(&t_full[ab]);
@@ -252,6 +256,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
         if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+#ifdef XBS_STUB_EPI  // perf experiment hook: TMEM loads and barriers only
+        if (lo[0] == 0xdeadbeef && hi[kCPW - 1] == 0x12345) P[0] += w;
+        continue;
+#endif
         adc_conv8<0, kCPW, kCPW, 16>(lo, hi, k, w, P, 0, exact);
         if constexpr (kCPW >= 32) {
           adc_conv8<16, kCPW, kCPW, 16>(lo, hi, k, w, P, 16, exact);

@@ -67,10 +67,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
-// Named CTA barrier over `count` threads (whole warps); id 0 is __syncthreads.
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 // One lane of a converged warp (the others skip the guarded issue).
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

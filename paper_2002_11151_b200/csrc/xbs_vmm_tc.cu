@@ -290,7 +290,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int ks = 0; ks < 4; ++ks) {
                       const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kPlane + 32 * ks, 16, 1024, 2);
                       const uint64_t bd = sdesc(b0 + (p * 2 + dh) * kBHalf + 32 * ks, 16, 1024, 2);
+#ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
                       umma_i8_pair(td, ad, bd, idesc, (kb | dh | ks) != 0);
+#else
+                      (void)ad; (void)bd; (void)td;
+#endif
                     }
                   if (kb == KB - 1) umma_commit_pair(&t_full[p == 0 ? ab : ab1]);
                 }
@@ -363,6 +367,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
           if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           const float wp = p == 0 ? wpos : wneg;
+#ifdef XBS_STUB_EPI  // perf experiment hook: TMEM loads and barriers only
+          if (lo[0] == 0xdeadbeef && hi[kRows - 1] == 0x12345) P[0] += wp;
+          continue;
+#endif
           adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
           adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
           if constexpr (kRows >= 32) {
