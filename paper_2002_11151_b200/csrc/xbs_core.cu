@@ -362,7 +362,35 @@ void maybe_freeze_adc(xbs_core* c) {
 
 bool calibrating(const xbs_core* c) { return c->adc_auto && !c->adc_frozen; }
 
-void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, double* d_y,
+// Output of a VMM call: a device buffer (column stride M), or the device
+// alias of the caller's pinned host buffer (stride ld).  The tcgen05 kernels
+// store straight into a host buffer from their epilogues, so the D2H
+// transfer overlaps the VMM; the other kernels write d_io_out, copied after.
+struct Out {
+  double* p;
+  int64_t ld;  // 0: M
+  bool host;
+};
+
+// Device alias of a pinned, mapped host buffer; nullptr for pageable memory.
+double* mapped_alias(const double* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+  return static_cast<double*>(at.devicePointer);
+}
+
+void finish_out(xbs_core* c, const Out& o, int64_t M, int64_t cols, bool direct) {
+  if (o.host && !direct)
+    ck(cudaMemcpy2DAsync(o.p, size_t(o.ld) * 8, c->d_io_out, size_t(M) * 8, size_t(M) * 8, size_t(cols),
+                         cudaMemcpyDefault, c->stream),
+       "D2H");
+}
+
+void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, Out out,
                     const xbs::ConvSrc* conv = nullptr) {
   if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
   maybe_freeze_adc(c);
@@ -381,14 +409,18 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, do
   if (calibrating(c) && training) xbs::calib_observe_fwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_FWD);
   c->launches += 1;
+  const int64_t ld = out.ld ? out.ld : M;
+  double* stage = out.host ? c->d_io_out : out.p;  // written with stride M
+  bool direct = false;
   if (c->fully_ideal) {
-    xbs::launch_fwd_ideal(c, M, d_y, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_fwd_tc(c, M, d_y, c->stream)) {
-    xbs::launch_fwd_simt(c, M, d_y, c->stream);
+    xbs::launch_fwd_ideal(c, M, stage, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
+    xbs::launch_fwd_simt(c, M, stage, c->stream);
   }
+  finish_out(c, Out{out.p, ld, out.host}, M, c->g.N, direct);
 }
 
-void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
+void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out out) {
   if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
   if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
   maybe_freeze_adc(c);
@@ -414,11 +446,15 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, doub
   if (calibrating(c)) xbs::calib_observe_bwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_BWD);
   c->launches += 1;
+  const int64_t ld = out.ld ? out.ld : M;
+  double* stage = out.host ? c->d_io_out : out.p;
+  bool direct = false;
   if (c->fully_ideal) {
-    xbs::launch_bwd_ideal(c, d_dy, M, d_dx, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !xbs::launch_bwd_tc(c, M, d_dx, c->stream)) {
-    xbs::launch_bwd_simt(c, M, d_dx, c->stream);
+    xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
+    xbs::launch_bwd_simt(c, M, stage, c->stream);
   }
+  finish_out(c, Out{out.p, ld, out.host}, M, c->g.K, direct);
 }
 
 void apply_updates_device(xbs_core* c, uint64_t iteration) {
@@ -460,7 +496,7 @@ namespace xbs {
 void core_forward_conv(xbs_core* c, const double* d_img, const ConvSrc& cs, bool training, double* d_y) {
   const int64_t rows = cs.batch * cs.oh * cs.ow;
   if (rows >= (int64_t(1) << 31)) fail(XBS_UNSUPPORTED, "CrossbarConv2d: more than 2^31 patch rows");
-  forward_device(c, d_img, rows, training, d_y, &cs);
+  forward_device(c, d_img, rows, training, Out{d_y, 0, false}, &cs);
 }
 }  // namespace xbs
 
@@ -726,8 +762,9 @@ int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t K, int64_t
       ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, x, size_t(ldx) * 8, size_t(M) * 8, size_t(c->g.K),
                            cudaMemcpyHostToDevice, c->stream),
          "H2D x");
-    forward_device(c, c->d_io_in, M, training != 0, c->d_io_out);
-    if (M > 0)
+    double* ym = M > 0 ? mapped_alias(y) : nullptr;  // pinned: the kernel stores y into it
+    forward_device(c, c->d_io_in, M, training != 0, ym ? Out{ym, ldy, true} : Out{c->d_io_out, 0, false});
+    if (M > 0 && !ym)
       ck(cudaMemcpy2DAsync(y, size_t(ldy) * 8, c->d_io_out, size_t(M) * 8, size_t(M) * 8, size_t(c->g.N),
                            cudaMemcpyDeviceToHost, c->stream),
          "D2H y");
@@ -747,8 +784,9 @@ int xbs_core_backward(xbs_core* c, const double* dy, int64_t M, int64_t N, int64
       ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, dy, size_t(lddy) * 8, size_t(M) * 8, size_t(c->g.N),
                            cudaMemcpyHostToDevice, c->stream),
          "H2D dy");
-    backward_device(c, c->d_io_in, M, gd, c->d_io_out);
-    if (M > 0)
+    double* dxm = M > 0 ? mapped_alias(dx) : nullptr;
+    backward_device(c, c->d_io_in, M, gd, dxm ? Out{dxm, lddx, true} : Out{c->d_io_out, 0, false});
+    if (M > 0 && !dxm)
       ck(cudaMemcpy2DAsync(dx, size_t(lddx) * 8, c->d_io_out, size_t(M) * 8, size_t(M) * 8, size_t(c->g.K),
                            cudaMemcpyDeviceToHost, c->stream),
          "D2H dx");
@@ -771,13 +809,13 @@ int xbs_core_apply_updates(xbs_core* c, uint64_t iteration) {
 int xbs_core_forward_device(xbs_core* c, const double* d_x, int64_t M, int32_t training, double* d_y) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
-    forward_device(c, d_x, M, training != 0, d_y);
+    forward_device(c, d_x, M, training != 0, Out{d_y, 0, false});
   });
 }
 int xbs_core_backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, double* d_dx) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
-    backward_device(c, d_dy, M, gd, d_dx);
+    backward_device(c, d_dy, M, gd, Out{d_dx, 0, false});
   });
 }
 int xbs_core_apply_updates_device(xbs_core* c, uint64_t iteration) {

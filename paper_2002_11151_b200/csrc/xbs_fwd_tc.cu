@@ -68,6 +68,7 @@ struct FwdArgs {
   double k_out;
   AdcConst adc;
   double* y;
+  int64_t ldy;  // column stride of y (M, or the caller's ld for a mapped host buffer)
   unsigned long long* ctr;
 };
 
@@ -290,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           if (i >= per) break;
           const int cc = hcol * kCW + kCPW * q + 16 * h + kk * per + i;
           const int jg = tc * a.tile_cols + cc;
-          if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.M + b] = double(v[i]) * a.k_out;
+          if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
         }
       }
     }
@@ -303,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
 
 }  // namespace tc
 
-bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
+bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_t st) {
   using namespace tc;
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || g.TPi > 16 || c->adc.passthrough) return false;
@@ -346,6 +347,7 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
   a.adc = make_adc_const(c->adc, c->d_adc_tab);
   if (a.adc.unscale == 0.0f) return false;
   a.y = d_y;
+  a.ldy = ldy;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
   if (!attr) {

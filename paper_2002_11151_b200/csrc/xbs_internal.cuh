@@ -223,8 +223,8 @@ void launch_varm(const xbs_core* c, cudaStream_t st);
 void launch_implied(const xbs_core* c, double* d_out, cudaStream_t st);
 void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double* d_out, cudaStream_t st);
 // tcgen05 kernels (xbs_vmm_tc.cu); return false if the shape is not covered
-bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
-bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
+bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_t st);
+bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream_t st);
 bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
 // ADC auto-calibration (xbs_calib.cu)
 void calib_observe_fwd(xbs_core* c, int64_t M, cudaStream_t st);

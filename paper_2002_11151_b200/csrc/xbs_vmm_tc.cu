@@ -153,6 +153,7 @@ struct BwdArgs {
   const DevScalars* sc;
   AdcConst adc;
   double* dx;
+  int64_t ldx;  // column stride of dx (M, or the caller's ld for a mapped host buffer)
   unsigned long long* ctr;
 };
 
@@ -399,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (i >= per) break;
           const int rloc = rh * 64 + kRows * ch + 16 * h + j0 + i;
           const int ig = tr * a.tile_rows + rloc;
-          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.M + b] = double(v[i]) * k_out;
+          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
         }
       }
     }
@@ -412,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 }  // namespace tc
 
-bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
+bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream_t st) {
   using namespace tc;
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc_b.passthrough) return false;
@@ -459,6 +460,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
   a.adc = make_adc_const(c->adc_b, c->d_adc_tab_b);
   if (a.adc.unscale == 0.0f) return false;
   a.dx = d_dx;
+  a.ldx = ldx;
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
   if (!attr) {
