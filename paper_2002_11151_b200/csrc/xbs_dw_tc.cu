@@ -18,6 +18,7 @@
 // warps); the TMEM accumulator pair is double buffered so the epilogue's
 // stores overlap the next unit's MMAs.
 #include <cuda.h>
+#include <cmath>
 #include <cuda_runtime.h>
 
 #include "xbs_internal.cuh"
@@ -41,9 +42,17 @@ struct DwArgs {
   unsigned long long* S64;  // split mode: int64 partial sums [KA][NA]; nullptr: direct dW
   int64_t Mcap8;
   double sx, lev_e, gd;
+  double rgd;  // 1 / gd when gd is a power of two (then x / gd == x * rgd exactly), else 0
   const DevScalars* sc;
   double* dW;
 };
+
+// ((S * sx) * step_e) / gd; a power-of-two divisor (the
+// usual grad_divisor = 1) is an exact multiply by its reciprocal
+__device__ __forceinline__ double dw_value(long long S, double sx, double step_e, double gd, double rgd) {
+  const double t = (double(S) * sx) * step_e;
+  return rgd != 0.0 ? t * rgd : t / gd;
+}
 
 __global__ void __launch_bounds__(dw::kThreads, 1)
     k_dw_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapE, const DwArgs a) {
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
               if (a.S64) {
                 if (S != 0) atomicAdd(&a.S64[int64_t(i0 + ii) * a.NA + j], (unsigned long long)(long long)S);
               } else {
-                a.dW[int64_t(i0 + ii) * a.N + j] = ((double(S) * a.sx) * step_e) / a.gd;
+                a.dW[int64_t(i0 + ii) * a.N + j] = dw_value(S, a.sx, step_e, a.gd, a.rgd);
               }
             }
           }
@@ -169,8 +178,8 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
 
 // Split mode: dW = ((S * sx) * step_e) / grad_divisor from the int64 sums,
 // then S64 is cleared for the next call.
-__global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, double gd, const DevScalars* sc,
-                              unsigned long long* __restrict__ S64, double* __restrict__ dW) {
+__global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, double gd, double rgd,
+                              const DevScalars* sc, unsigned long long* __restrict__ S64, double* __restrict__ dW) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
   const int64_t n = int64_t(K) * N;
@@ -179,7 +188,7 @@ __global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, dou
     unsigned long long* p = &S64[int64_t(i) * NA + j];
     const long long S = (long long)*p;
     *p = 0ull;
-    dW[t] = ((double(S) * sx) * step_e) / gd;
+    dW[t] = dw_value(S, sx, step_e, gd, rgd);
   }
 }
 
@@ -221,6 +230,12 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
   a.sx = c->sx;
   a.lev_e = c->lev_e;
   a.gd = grad_divisor;
+  {
+    int e;
+    const double m = std::frexp(grad_divisor, &e);  // gd = m 2^e, m = 0.5 for a power of two
+    a.rgd = (std::isfinite(grad_divisor) && std::fabs(m) == 0.5) ? 1.0 / grad_divisor : 0.0;
+    if (a.rgd != 0.0 && (!std::isfinite(a.rgd) || std::fabs(std::frexp(a.rgd, &e)) != 0.5)) a.rgd = 0.0;
+  }
   a.sc = c->d_sc;
   a.dW = c->d_dW;
   static bool attr = false;
@@ -234,8 +249,8 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
     const int64_t n = int64_t(c->g.K) * c->g.N;
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
     c->launches += 1;  // the finalize pass (the caller counts k_dw_tc)
-    k_dw_finalize<<<blocks, 256, 0, st>>>(c->g.K, c->g.N, c->NA, c->sx, c->lev_e, grad_divisor, c->d_sc, c->d_S64,
-                                          c->d_dW);
+    k_dw_finalize<<<blocks, 256, 0, st>>>(c->g.K, c->g.N, c->NA, c->sx, c->lev_e, grad_divisor, a.rgd, c->d_sc,
+                                          c->d_S64, c->d_dW);
   }
   return cudaPeekAtLastError() == cudaSuccess;
 }

@@ -40,6 +40,9 @@ namespace xbs {
 namespace tc {
 
 namespace fw {
+#ifndef XBS_FWD_PIPE
+#define XBS_FWD_PIPE 1
+#endif
 #ifndef XBS_FWD_EPI_WARPS
 #define XBS_FWD_EPI_WARPS 8
 #endif
@@ -236,6 +239,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       const float wstep = float(1 << a.db);
       float wmag = k.unscale;
       int sp = 0;
+#if XBS_FWD_PIPE
+      // software-pipelined TMEM reads: one 16-column half is in flight while
+      // the other is converted (A: columns 0-15, B: 16-31 of this warp)
+      static_assert(kCPW == 32, "pipelined epilogue: 32 columns per warp");
+      uint32_t alo[16], ahi[16], blo[16], bhi[16];
+      mbar_wait_hint(&t_full[ab], abph);
+      tc_fence_after();
+      tmem_ld16(tl + ab * 128, alo);
+      tmem_ld16(tl + ab * 128 + kCW, ahi);
+      tmem_wait_ld();
+      for (int c = 0; c < nchain; ++c) {
+        const float w = (sp & 1) == 0 ? wmag : -wmag;
+        if (++sp == 2 * a.S) {
+          sp = 0;
+          wmag = k.unscale;
+        } else if ((sp & 1) == 0) {
+          wmag = __fmul_rn(wmag, wstep);
+        }
+        tmem_ld16(tl + ab * 128 + 16, blo);
+        tmem_ld16(tl + ab * 128 + kCW + 16, bhi);
+        adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+        if (c + 1 < nchain) {
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+          tmem_ld16(tl + ab * 128, alo);
+          tmem_ld16(tl + ab * 128 + kCW, ahi);
+        }
+        adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, w, P, 16, exact);
+        tmem_wait_ld();
+      }
+#else
       for (int c = 0; c < nchain; ++c) {
         const float w = (sp & 1) == 0 ? wmag : -wmag;
         if (++sp == 2 * a.S) {
@@ -272,6 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           adc_conv8<56>(lo, hi, k, w, P, 56, exact);
         }
       }
+#endif
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
       // (exact in int32: host-checked bound); per 16 columns, lane q ends
       // with the totals of columns q * (16 / TPi) + i

@@ -13,6 +13,9 @@
 namespace xbs {
 namespace tc {
 
+#ifndef XBS_BWD_PIPE
+#define XBS_BWD_PIPE 0
+#endif
 #ifndef XBS_BWD_EPI_WARPS
 #define XBS_BWD_EPI_WARPS 16
 #endif
@@ -340,6 +343,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float wstep = float(1 << a.db);
       float wmag = k.unscale;
       int s = 0;
+#if XBS_BWD_PIPE
+      // software-pipelined TMEM reads: the next polarity's accumulator is
+      // loaded (and released to the MMA) while this one is converted
+      static_assert(kRows == 16, "pipelined epilogue: 16 rows per warp");
+      uint32_t alo[16], ahi[16], blo[16], bhi[16];
+      mbar_wait_hint(&t_full[ab], abph);
+      tc_fence_after();
+      tmem_ld16(tl + ab * 128, alo);
+      tmem_ld16(tl + ab * 128 + 64, ahi);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+      if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+      for (int c = 0; c < nchain; ++c) {
+        const float w = wmag;
+        if (++s == a.S) {
+          s = 0;
+          wmag = k.unscale;
+        } else {
+          wmag = __fmul_rn(wmag, wstep);
+        }
+        const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
+        const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
+        mbar_wait_hint(&t_full[ab], abph);      // polarity 1 of chain c
+        tc_fence_after();
+        tmem_ld16(tl + ab * 128, blo);
+        tmem_ld16(tl + ab * 128 + 64, bhi);
+        adc_conv8<0>(alo, ahi, k, wpos, P, 0, exact);
+        adc_conv8<8>(alo, ahi, k, wpos, P, 8, exact);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+        const bool more = c + 1 < nchain;
+        if (more) {  // polarity 0 of chain c + 1
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+          tmem_ld16(tl + ab * 128, alo);
+          tmem_ld16(tl + ab * 128 + 64, ahi);
+        }
+        adc_conv8<0>(blo, bhi, k, wneg, P, 0, exact);
+        adc_conv8<8>(blo, bhi, k, wneg, P, 8, exact);
+        if (more) {
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+        }
+      }
+#else
       for (int c = 0; c < nchain; ++c) {
         // chains run tc-major, then slice: weight 2^(s db) k.unscale
         const float w = wmag;
@@ -380,6 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+#endif
       // combine the 2*TPe (plane, phase) lanes of each batch row (exact in
       // int32: host-checked bound); lane q ends with the totals of rows
       // q * (16 / grp) + i (grp = 32: lanes q, q ^ 1 share row q >> 1)

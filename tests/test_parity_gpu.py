@@ -170,3 +170,21 @@ def test_zero_input_zero_output_and_empty_batch():
     gpu = xb.CrossbarCore(normal((6, 4), 1, 0.3), opt)
     assert np.all(gpu.forward(np.zeros((3, 6)), False) == 0.0)
     assert gpu.forward(np.zeros((0, 6)), False).shape == (0, 4)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("gd", [4.0, 3.0, 0.125, 1e-310])
+def test_grad_divisor(kernel, gd):
+    """dW = x_values^T dy_q / grad_divisor (layers.cpp:304): power-of-two
+    divisors take an exact reciprocal multiply on the GPU, others divide;
+    both bit-identical to the oracle's division (subnormal divisor included)."""
+    K, N, M = 150, 140, 300
+    opt = aam_options(tile=128, adc_bits=7, i_fs=2e-4)
+    W = normal((K, N), 41, 0.05)
+    gpu, orc = _pair(W, opt, kernel)
+    x = rand((M, K), 42, -0.2, 1.2)
+    dy = rand((M, N), 43)
+    gpu.forward(x, True)
+    orc.forward(x, True)
+    assert np.array_equal(gpu.backward(dy, gd), orc.backward(dy, gd))
+    assert np.array_equal(gpu.gradient(), orc.gradient())
