@@ -182,14 +182,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         for (int tr = 0; tr < a.GR; ++tr) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + as * kAStage);
+          const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
           for (int sp = 0; sp < 2 * a.S; ++sp) {
             mbar_wait(&t_empty[ab], abph ^ 1);
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&b_full[bs], bph);
               tc_fence_after();
-              const uint32_t b0 = smem_u32(sB + bs * kBStage);
+              const uint64_t b0d = sdesc(smem_u32(sB + bs * kBStage), kBBox, 512, 4);
               if (elect_one()) {
 #pragma unroll
                 for (int dh = 0; dh < 2; ++dh)
@@ -198,8 +198,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
                     // A: K-major SW128 (LBO 16, SBO 1024); B: each CTA's
                     // 64-column half, MN-major SW64 (8-row K groups 512 B
                     // apart, 32 K rows per MMA = 2 KB)
-                    const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kABox + 32 * ks, 16, 1024, 2);
-                    const uint64_t bd = sdesc(b0 + dh * kBBox + 2048 * ks, kBBox, 512, 4);
+                    const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kABox + 32 * ks);
+                    const uint64_t bd = sdesc_add(b0d, dh * kBBox + 2048 * ks);
 #ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
                     umma_i8_pair(tmem + ab * 128, ad, bd, idesc, (kb | dh | ks) != 0);
 #else

@@ -101,6 +101,14 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= uint64_t(layout & 7u) << 61;
   return d;
 }
+// Descriptor of the tile `bytes` (a multiple of 16) past the one `d`
+// describes: only the start-address field moves.  Shared-memory addresses
+// are < 2^18, so start >> 4 + bytes >> 4 stays inside the 14-bit field and
+// a 32-bit add on the low word is exact (no per-MMA re-encoding).
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t d, uint32_t bytes) {
+  const uint32_t lo = uint32_t(d) + (bytes >> 4), hi = uint32_t(d >> 32);
+  return (uint64_t(hi) << 32) | lo;
+}
 // Instruction descriptor, kind::i8: D s32, A/B u8, A K-major, B major as given.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool b_mn_major) {
   return (2u << 4)                      /* c_format S32        */

@@ -272,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int tc = 0; tc < a.GC; ++tc) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + as * kAStage);
+          const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
           for (int s = 0; s < a.S; ++s) {
             // both polarities' accumulators, then the k-blocks of one B stage
             mbar_wait(&t_empty[ab], abph ^ 1);
@@ -283,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&b_full[bs], bph);
               tc_fence_after();
-              const uint32_t b0 = smem_u32(sB + bs * kBStage);
+              const uint64_t b0d = sdesc(smem_u32(sB + bs * kBStage), 16, 1024, 2);
               if (elect_one()) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
@@ -292,8 +292,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
-                      const uint64_t ad = sdesc(a0 + (dh * KB + kb) * kPlane + 32 * ks, 16, 1024, 2);
-                      const uint64_t bd = sdesc(b0 + (p * 2 + dh) * kBHalf + 32 * ks, 16, 1024, 2);
+                      const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kPlane + 32 * ks);
+                      const uint64_t bd = sdesc_add(b0d, (p * 2 + dh) * kBHalf + 32 * ks);
 #ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
                       umma_i8_pair(td, ad, bd, idesc, (kb | dh | ks) != 0);
 #else
