@@ -740,6 +740,7 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_xc8);
   cudaFree(c->d_e8);
   cudaFree(c->d_S64);
+  cudaFree(c->d_acc32);
   cudaFree(c->d_io_in);
   cudaFree(c->d_io_out);
   for (auto& p : c->pending) {

@@ -67,7 +67,9 @@ struct FwdArgs {
   int n_nb;              // scheduled column units
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = column units fastest
   int64_t M, rowsF;
-  int num_mbp, num_units;
+  int num_mbp, num_units;  // num_units = base units (M-block pair x column unit) x ksplit
+  int nbase, ksplit, trs;   // split-K (small layers): crossbar row tiles [sp * trs, +trs) per unit
+  int* acc;                 // ksplit > 1: int32 totals [N][M] (atomics), scaled by k_out in k_fwd_finalize
   double k_out;
   AdcConst adc;
   double* y;
@@ -85,6 +87,15 @@ __device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int&
   } else {
     h = nb - tc * a.live;
   }
+}
+
+// Unit index -> (M-block pair, column unit, row-tile range).
+__device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int& nb, int& tr0, int& tr1) {
+  const int ub = u % a.nbase, sp = u / a.nbase;
+  mbp = a.mfast ? ub % a.num_mbp : ub / a.n_nb;
+  nb = a.mfast ? ub / a.num_mbp : ub % a.n_nb;
+  tr0 = sp * a.trs;
+  tr1 = min(a.GR, tr0 + a.trs);
 }
 
 template <int KB>
@@ -137,11 +148,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int mbp = a.mfast ? u % a.num_mbp : u / a.n_nb, nb = a.mfast ? u / a.num_mbp : u % a.n_nb;
+        int mbp, nb, tr0, tr1;
+        fwd_unit(u, a, mbp, nb, tr0, tr1);
         int tc, h;
         col_unit(nb, a, tc, h);
         const int mrow = (2 * mbp + int(rank)) * 128;
-        for (int tr = 0; tr < a.GR; ++tr) {
+        for (int tr = tr0; tr < tr1; ++tr) {
           mbar_wait(&a_empty[as], aph ^ 1);
           if (elect_one()) {
             if (rank == 0) mbar_expect_tx(&a_full[as], 2 * kAStage);
@@ -179,7 +191,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       constexpr uint32_t idesc = idesc_i8(256, 2 * kCW, /*b_mn_major=*/true);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        for (int tr = 0; tr < a.GR; ++tr) {
+        const int ntr = min(a.GR, (u / a.nbase + 1) * a.trs) - (u / a.nbase) * a.trs;
+        for (int tr = 0; tr < ntr; ++tr) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
           const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
@@ -226,11 +239,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     const int ml = 32 * lg + lane;
     const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kCPW * q;
     const uint32_t te0 = mapa(smem_u32(&t_empty[0]), 0);  // leader's barriers, 8 B apart
-    const int nchain = a.GR * a.S * 2;
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     for (int u = cid; u < a.num_units; u += ncl) {
-      const int mbp = a.mfast ? u % a.num_mbp : u / a.n_nb, nb = a.mfast ? u / a.num_mbp : u % a.n_nb;
+      int mbp, nb, tr0, tr1;
+      fwd_unit(u, a, mbp, nb, tr0, tr1);
+      const int nchain = (tr1 - tr0) * a.S * 2;
       float P[kCPW];
 #pragma unroll
       for (int j = 0; j < kCPW; ++j) P[j] = 0.f;
@@ -331,7 +345,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           if (i >= per) break;
           const int cc = hcol * kCW + kCPW * q + 16 * h + kk * per + i;
           const int jg = tc * a.tile_cols + cc;
-          if (b < a.M && cc < a.tile_cols && jg < a.N) a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
+          if (b < a.M && cc < a.tile_cols && jg < a.N) {
+            if (a.acc) atomicAdd(&a.acc[int64_t(jg) * a.M + b], v[i]);  // split-K partial (exact)
+            else a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
+          }
         }
       }
     }
@@ -340,6 +357,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
   tc_fence_before();
   cluster_sync();  // both CTAs done with the pair's TMEM and barriers
   if (warp == 1) tmem_dealloc_pair<512>(tmem);
+}
+
+// Split-K: y = total * k_out (the single fp64 rounding of layers.cpp:283);
+// the partial buffer is left zero for the next call.
+__global__ void k_fwd_finalize(int64_t M, int N, double k_out, int* __restrict__ acc, double* __restrict__ y,
+                               int64_t ldy) {
+  const int64_t n = M * N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = t / M, b = t - j * M;
+    y[j * ldy + b] = double(acc[t]) * k_out;
+    acc[t] = 0;
+  }
+}
+
+// int32 split-K buffer of at least `bytes` (kept zero between calls)
+int* acc32(xbs_core* c, size_t bytes, cudaStream_t st) {
+  if (c->acc32_bytes < bytes) {
+    cudaFree(c->d_acc32);
+    c->d_acc32 = nullptr;
+    c->acc32_bytes = 0;
+    if (cudaMalloc(&c->d_acc32, bytes) != cudaSuccess) return nullptr;
+    cudaMemsetAsync(c->d_acc32, 0, bytes, st);
+    c->acc32_bytes = bytes;
+  }
+  return c->d_acc32;
 }
 
 }  // namespace tc
@@ -374,7 +416,18 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.num_mbp = int(rowsF / 256);
   a.live_last = (g.N - (g.GC - 1) * g.tile_cols + fw::kCW - 1) / fw::kCW;
   a.n_nb = (g.GC - 1) * a.live + a.live_last;
-  a.num_units = a.num_mbp * a.n_nb;
+  a.nbase = a.num_mbp * a.n_nb;
+  // small layers: too few units for the 74 CTA pairs, so the crossbar row
+  // tiles of a unit are split across pairs and the exact integer totals
+  // summed with int32 atomics (the host-checked bound covers any partial)
+  const int pairs = num_sms() / 2;
+  a.ksplit = 1;
+  if (2 * a.nbase <= pairs && g.GR > 1) a.ksplit = std::min(g.GR, pairs / a.nbase);
+  a.trs = (g.GR + a.ksplit - 1) / a.ksplit;
+  a.ksplit = (g.GR + a.trs - 1) / a.trs;
+  a.num_units = a.nbase * a.ksplit;
+  a.acc = nullptr;
+  if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.N * 4, st))) return false;
   {  // sweep the larger operand once: A (input planes) vs the conductance digits
     const double bytesA = 2.0 * double(rowsF) * g.KI, bytesB = double(g.digits_bytes()) * a.n_nb / (g.GC * (g.C / fw::kCW));
     // an operand that fits in L2 (126 MB; use half) is re-read for free
@@ -398,6 +451,12 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   const int grid = 2 * std::min(a.num_units, num_sms() / 2);  // CTA pairs
   if (g.R == 128) k_fwd_tc<1><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
   else k_fwd_tc<2><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
+  if (a.acc) {
+    const int64_t n = M * g.N;
+    k_fwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * num_sms())), 256, 0, st>>>(M, g.N, a.k_out, a.acc,
+                                                                                          d_y, ldy);
+    c->launches += 1;
+  }
   return cudaPeekAtLastError() == cudaSuccess;
 }
 

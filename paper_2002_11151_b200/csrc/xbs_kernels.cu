@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
   double wmax = 0.0, dwmax = 0.0;
   const int j0 = JPT * (blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 < g.N) {
-    // column-only terms, hoisted out of the row loop
+    // column-only terms, hoisted out of the row loop (a block covers
+    // blockDim.y rows: narrow layers keep every thread busy)
     const int tc = j0 / g.tile_cols, c0 = j0 - tc * g.tile_cols;  // JPT | tile_cols (host-checked)
     double rrow[JPT];
 #pragma unroll
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
     const size_t plane = g.plane_bytes();
     const size_t sp_stride = size_t(g.GR) * g.GC * 4 * plane;
     const size_t sstride = size_t(g.Kp) * g.Np;
-    for (int i = blockIdx.y; i < g.K; i += gridDim.y) {
+    for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < g.K; i += gridDim.y * blockDim.y) {
       const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
       const double rcol = double(g.tile_rows - r) * rp.r_col;
       constexpr int PRE = S < 4 ? S : 4;  // slices loaded per group (register budget)
@@ -448,12 +449,16 @@ __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, c
 
 template <int S, int JPT>
 static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
-  const dim3 grid((c->g.N / JPT + 255) / 256, std::min(c->g.K, 65535));
+  // threads per row: the row's JPT-weight groups rounded up to whole warps
+  // (<= 256); the rest of the 256-thread block takes further rows
+  const int tpr = int(std::min<int64_t>(256, ((c->g.N / JPT + 31) / 32) * 32));
+  const dim3 block(tpr, 256 / tpr);
+  const dim3 grid((c->g.N / JPT + tpr - 1) / tpr, unsigned(std::min<int64_t>((c->g.K + block.y - 1) / block.y, 65535)));
   const bool var = c->rp.sigma != 0.0, nl = !up.linear, noise = up.gamma != 0.0;
   // AAM with a zero path resistance everywhere is the identity conversion
   const bool aam = c->rp.aam && (c->rp.r_source + c->rp.r_row + c->rp.r_col + c->rp.r_sense) > 0.0;
   auto go = [&](auto kern) {
-    kern<<<grid, 256, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
+    kern<<<grid, block, 0, st>>>(c->g, c->rp, up, c->d_dW, c->d_master, c->d_digits, c->d_sc, c->d_qmin);
   };
 #define XBS_UPD(V, N, A) go(k_update<S, JPT, V, N, N, A>)
   if (master_only) {

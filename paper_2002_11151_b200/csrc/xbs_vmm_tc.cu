@@ -13,9 +13,6 @@
 namespace xbs {
 namespace tc {
 
-#ifndef XBS_BWD_PIPE
-#define XBS_BWD_PIPE 0
-#endif
 #ifndef XBS_BWD_EPI_WARPS
 #define XBS_BWD_EPI_WARPS 16
 #endif
@@ -150,7 +147,9 @@ struct BwdArgs {
   int n_rb;              // scheduled row blocks
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = row blocks fastest
   int64_t M, rowsB;
-  int num_mbp, num_units;
+  int num_mbp, num_units;  // num_units = base units (M-block pair x row block) x ksplit
+  int nbase, ksplit, tcs;   // split-K (small layers): crossbar column tiles [sp * tcs, +tcs) per unit
+  int* acc;                 // ksplit > 1: int32 totals [K][M] (atomics), scaled in k_bwd_finalize
   double F, vu, ifs_fac, lev_e;
   int adc_scaled;
   const DevScalars* sc;
@@ -170,6 +169,24 @@ __device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int
   } else {
     rh = rb - tr * a.live;
   }
+}
+
+// Unit index -> (M-block pair, row block, column-tile range).
+__device__ __forceinline__ void bwd_unit(int u, const BwdArgs& a, int& mbp, int& rb, int& tc0, int& tc1) {
+  const int ub = u % a.nbase, sp = u / a.nbase;
+  mbp = a.mfast ? ub % a.num_mbp : ub / a.n_rb;
+  rb = a.mfast ? ub / a.num_mbp : ub % a.n_rb;
+  tc0 = sp * a.tcs;
+  tc1 = min(a.GC, tc0 + a.tcs);
+}
+
+// dx scale of layers.cpp:375-377 (same expression on every path)
+__device__ __forceinline__ double bwd_k_out(const BwdArgs& a) {
+  const double se = a.sc->se;
+  const double step_e = se > 0 ? se / a.lev_e : 0.0;
+  double k_out = step_e * a.F / a.vu;
+  if (a.adc_scaled) k_out *= a.ifs_fac;
+  return k_out;
 }
 
 template <int KB>
@@ -222,11 +239,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int mbp = a.mfast ? u % a.num_mbp : u / a.n_rb, rb = a.mfast ? u / a.num_mbp : u % a.n_rb;
+        int mbp, rb, tc0, tc1;
+        bwd_unit(u, a, mbp, rb, tc0, tc1);
         int tr, rh;
         row_block(rb, a, tr, rh);
         const int mrow = (2 * mbp + int(rank)) * 128;
-        for (int tc = 0; tc < a.GC; ++tc) {
+        for (int tc = tc0; tc < tc1; ++tc) {
           mbar_wait(&a_empty[as], aph ^ 1);
           if (elect_one()) {
             if (rank == 0) mbar_expect_tx(&a_full[as], 2 * kAStage);
@@ -269,7 +287,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = idesc_i8(256, 128, /*b_mn_major=*/false);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        for (int tc = 0; tc < a.GC; ++tc) {
+        const int ntc = min(a.GC, (u / a.nbase + 1) * a.tcs) - (u / a.nbase) * a.tcs;
+        for (int tc = 0; tc < ntc; ++tc) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
           const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
@@ -328,13 +347,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t te0 = mapa(smem_u32(&t_empty[0]), 0);  // leader's barriers, 8 B apart
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
-    const double se = a.sc->se;
-    const double step_e = se > 0 ? se / a.lev_e : 0.0;
-    double k_out = step_e * a.F / a.vu;  // layers.cpp:375-377
-    if (a.adc_scaled) k_out *= a.ifs_fac;
-    const int nchain = a.GC * a.S;
+    const double k_out = bwd_k_out(a);  // layers.cpp:375-377
     for (int u = cid; u < a.num_units; u += ncl) {
-      const int mbp = a.mfast ? u % a.num_mbp : u / a.n_rb, rb = a.mfast ? u / a.num_mbp : u % a.n_rb;
+      int mbp, rb, tc0, tc1;
+      bwd_unit(u, a, mbp, rb, tc0, tc1);
+      const int nchain = (tc1 - tc0) * a.S;
       int tr, rh;
       row_block(rb, a, tr, rh);
       float P[kRows];
@@ -343,59 +360,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const float wstep = float(1 << a.db);
       float wmag = k.unscale;
       int s = 0;
-#if XBS_BWD_PIPE
-      // software-pipelined TMEM reads: the next polarity's accumulator is
-      // loaded (and released to the MMA) while this one is converted
-      static_assert(kRows == 16, "pipelined epilogue: 16 rows per warp");
-      uint32_t alo[16], ahi[16], blo[16], bhi[16];
-      mbar_wait_hint(&t_full[ab], abph);
-      tc_fence_after();
-      tmem_ld16(tl + ab * 128, alo);
-      tmem_ld16(tl + ab * 128 + 64, ahi);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-      if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-      for (int c = 0; c < nchain; ++c) {
-        const float w = wmag;
-        if (++s == a.S) {
-          s = 0;
-          wmag = k.unscale;
-        } else {
-          wmag = __fmul_rn(wmag, wstep);
-        }
-        const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
-        const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
-        mbar_wait_hint(&t_full[ab], abph);      // polarity 1 of chain c
-        tc_fence_after();
-        tmem_ld16(tl + ab * 128, blo);
-        tmem_ld16(tl + ab * 128 + 64, bhi);
-        adc_conv8<0>(alo, ahi, k, wpos, P, 0, exact);
-        adc_conv8<8>(alo, ahi, k, wpos, P, 8, exact);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-        const bool more = c + 1 < nchain;
-        if (more) {  // polarity 0 of chain c + 1
-          mbar_wait_hint(&t_full[ab], abph);
-          tc_fence_after();
-          tmem_ld16(tl + ab * 128, alo);
-          tmem_ld16(tl + ab * 128 + 64, ahi);
-        }
-        adc_conv8<0>(blo, bhi, k, wneg, P, 0, exact);
-        adc_conv8<8>(blo, bhi, k, wneg, P, 8, exact);
-        if (more) {
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-        }
-      }
-#else
       for (int c = 0; c < nchain; ++c) {
         // chains run tc-major, then slice: weight 2^(s db) k.unscale
         const float w = wmag;
@@ -436,7 +400,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-#endif
       // combine the 2*TPe (plane, phase) lanes of each batch row (exact in
       // int32: host-checked bound); lane q ends with the totals of rows
       // q * (16 / grp) + i (grp = 32: lanes q, q ^ 1 share row q >> 1)
@@ -457,7 +420,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (i >= per) break;
           const int rloc = rh * 64 + kRows * ch + 16 * h + j0 + i;
           const int ig = tr * a.tile_rows + rloc;
-          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
+          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) {
+            if (a.acc) atomicAdd(&a.acc[int64_t(ig) * a.M + b], v[i]);  // split-K partial (exact)
+            else a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
+          }
         }
       }
     }
@@ -466,6 +432,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();  // both CTAs done with the pair's TMEM and barriers
   if (warp == 1) tmem_dealloc_pair<512>(tmem);
+}
+
+__global__ void k_bwd_finalize(const BwdArgs a, int64_t M, int K) {
+  const double k_out = bwd_k_out(a);
+  const int64_t n = M * K;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / M, b = t - i * M;
+    a.dx[i * a.ldx + b] = double(a.acc[t]) * k_out;
+    a.acc[t] = 0;
+  }
 }
 
 }  // namespace tc
@@ -499,7 +475,17 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.live = (g.tile_rows + 63) / 64;
   a.live_last = (g.K - (g.GR - 1) * g.tile_rows + 63) / 64;
   a.n_rb = (g.GR - 1) * a.live + a.live_last;
-  a.num_units = a.num_mbp * a.n_rb;
+  a.nbase = a.num_mbp * a.n_rb;
+  // small layers: split the crossbar column tiles of a unit across CTA pairs
+  // (exact int32 totals, summed with atomics; see launch_fwd_tc)
+  const int pairs = sm_count() / 2;
+  a.ksplit = 1;
+  if (2 * a.nbase <= pairs && g.GC > 1) a.ksplit = std::min(g.GC, pairs / a.nbase);
+  a.tcs = (g.GC + a.ksplit - 1) / a.ksplit;
+  a.ksplit = (g.GC + a.tcs - 1) / a.tcs;
+  a.num_units = a.nbase * a.ksplit;
+  a.acc = nullptr;
+  if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.K * 4, st))) return false;
   {  // sweep the larger operand once: A' (error planes) vs the conductance digits
     const double bytesA = 2.0 * double(rowsB) * g.NI, bytesB = double(g.digits_bytes()) / g.GR * (double(a.n_rb) / a.live);
     // an operand that fits in L2 (126 MB; use half) is re-read for free
@@ -528,6 +514,11 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   const int grid = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
   if (KB == 1) k_bwd_tc<1><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
   else k_bwd_tc<2><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
+  if (a.acc) {
+    const int64_t n = M * g.K;
+    k_bwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * sm_count())), 256, 0, st>>>(a, M, g.K);
+    c->launches += 1;
+  }
   return cudaPeekAtLastError() == cudaSuccess;
 }
 
