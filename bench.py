@@ -459,8 +459,6 @@ def main():
     clocks.start()
     time.sleep(0.3)
     launches0 = sum(c.launch_count() for c in cores)
-    for c in cores:
-        c.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -471,13 +469,22 @@ def main():
         c.synchronize()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    launches = sum(c.launch_count() for c in cores) - launches0
+    # per-stage kernel times: the same K steps again with CUDA events around
+    # every stage (eager launches; the timed steps above replay the cores'
+    # captured graphs, which per-stage events would split)
+    for c in cores:
+        c.profile(True)
+    for _ in range(args.steps):
+        step()
+    for c in cores:
+        c.synchronize()
     stages = {}
     for c in cores:
         for k, (t, n) in c.stage_times().items():
             t0, n0 = stages.get(k, (0.0, 0))
             stages[k] = (t0 + t, n0 + n)
         c.profile(False)
-    launches = sum(c.launch_count() for c in cores) - launches0
     barrier(world)
     ms = max_over_ranks(ms, world, "cuda")
 

@@ -187,6 +187,11 @@ int xbs_conv2d_apply_updates(xbs_conv2d* conv, uint64_t iteration);
 enum { XBS_STAGE_PREP_X = 0, XBS_STAGE_FWD = 1, XBS_STAGE_PREP_DY = 2, XBS_STAGE_DW = 3, XBS_STAGE_BWD = 4,
        XBS_STAGE_UPDATE = 5, XBS_NUM_STAGES = 6 };
 int xbs_core_profile(xbs_core* core, int32_t enable);
+/* CUDA graphs (default on): a forward / backward call that repeats the
+ * previous call's buffers and shape is replayed from a captured graph (one
+ * launch); results are identical with graphs off.  Stage profiling and ADC
+ * auto-calibration always run eagerly. */
+int xbs_core_use_graphs(xbs_core* core, int32_t enable);
 int xbs_core_stage_times(xbs_core* core, double* ms, int64_t* count, int32_t n);
 /* Number of this library's kernels launched by the core so far. */
 int64_t xbs_core_launch_count(xbs_core* core);

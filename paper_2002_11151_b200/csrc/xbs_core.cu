@@ -158,6 +158,7 @@ int snap_exponent(double g_max) {  // largest e with g_max * 2^e <= Q_MAX
 
 void ensure_batch(xbs_core* c, int64_t M) {
   if (M <= c->M_cap) return;
+  ++c->gen;  // buffers move: captured graphs are stale
   const int64_t cap = std::max<int64_t>(M, 2 * c->M_cap);
   cudaFree(c->d_Af);
   cudaFree(c->d_Ab);
@@ -306,6 +307,7 @@ void collect_stage_times(xbs_core* c) {
 void set_adc(xbs_core* c, int dir, double i_fs) {
   xbs::AdcP& a = dir == 0 ? c->adc : c->adc_b;
   unsigned long long*& tab = dir == 0 ? c->d_adc_tab : c->d_adc_tab_b;
+  ++c->gen;
   a.passthrough = 0;
   a.i_fs = i_fs;
   const double fac = i_fs / (std::pow(2.0, c->opt.adc_bits) - 1.0);
@@ -390,6 +392,83 @@ void finish_out(xbs_core* c, const Out& o, int64_t M, int64_t cols, bool direct)
        "D2H");
 }
 
+void enqueue_fwd_vmm(xbs_core* c, int64_t M, const Out& out) {
+  const int64_t ld = out.ld ? out.ld : M;
+  double* stage = out.host ? c->d_io_out : out.p;  // written with stride M
+  bool direct = false;
+  if (c->fully_ideal) {
+    xbs::launch_fwd_ideal(c, M, stage, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
+    xbs::launch_fwd_simt(c, M, stage, c->stream);
+  }
+  finish_out(c, Out{out.p, ld, out.host}, M, c->g.N, direct);
+}
+
+void enqueue_bwd_vmm(xbs_core* c, const double* d_dy, int64_t M, const Out& out) {
+  const int64_t ld = out.ld ? out.ld : M;
+  double* stage = out.host ? c->d_io_out : out.p;
+  bool direct = false;
+  if (c->fully_ideal) {
+    xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
+  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
+    xbs::launch_bwd_simt(c, M, stage, c->stream);
+  }
+  finish_out(c, Out{out.p, ld, out.host}, M, c->g.K, direct);
+}
+
+// Replays `enqueue` (pure stream work on c->stream) from a CUDA graph when
+// the same call repeats: the first call with a key runs eagerly, the second
+// is captured and instantiated, later ones launch the executable graph (one
+// launch instead of ~5-12 kernels and memsets).  Host-side state is updated
+// by the caller on every call, outside the graph.
+template <class F>
+void run_graphed(xbs_core* c, xbs_core::GraphSlot& g, const uint64_t (&key)[8], F&& enqueue) {
+  uint64_t k[8];
+  std::memcpy(k, key, sizeof k);
+  k[7] = c->gen;
+  const bool same = std::memcmp(k, g.key, sizeof k) == 0;
+  if (same && g.ready) {
+    ck(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
+    c->launches += g.kernels;
+    return;
+  }
+  if (!same || !g.seen) {  // new key: run eagerly, capture on the next identical call
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.ready = false;
+    std::memcpy(g.key, k, sizeof k);
+    g.seen = true;
+    enqueue();
+    return;
+  }
+  const int64_t l0 = c->launches;
+  ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  cudaGraph_t graph = nullptr;
+  try {
+    enqueue();
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    g.seen = false;
+    throw;
+  }
+  ck(cudaStreamEndCapture(c->stream, &graph), "cudaStreamEndCapture");
+  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  ck(e, "cudaGraphInstantiate");
+  g.kernels = c->launches - l0;
+  c->launches = l0;
+  g.ready = true;
+  ck(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
+  c->launches += g.kernels;
+}
+
+bool graphable(const xbs_core* c, int64_t M) { return c->use_graphs && !c->profile && !c->adc_auto && M > 0; }
+
+uint64_t u64(const void* p) { return uint64_t(reinterpret_cast<uintptr_t>(p)); }
+uint64_t u64(double v) { return __builtin_bit_cast(uint64_t, v); }
+
 void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, Out out,
                     const xbs::ConvSrc* conv = nullptr) {
   if (M < 0) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: negative batch");
@@ -397,6 +476,23 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, Ou
   if (c->adc_auto && c->adc_frozen && !(c->adc.i_fs > 0) && M > 0)
     fail(XBS_STATE_ERROR, "adc_quantize: i_fs not set (calibrate first)");  // converters.cpp:83-84
   ensure_batch(c, std::max<int64_t>(M, 1));
+  if (graphable(c, M)) {
+    uint64_t key[8] = {u64(d_x), uint64_t(M), u64(out.p), uint64_t(out.ld), uint64_t(out.host), 0, 0, 0};
+    if (conv) {
+      key[5] = uint64_t(conv->batch) ^ (uint64_t(conv->h) << 32) ^ (uint64_t(conv->w) << 48);
+      key[6] = uint64_t(conv->in_c) ^ (uint64_t(conv->k) << 16) ^ (uint64_t(conv->stride) << 24) ^
+               (uint64_t(conv->pad) << 32) ^ (uint64_t(1) << 63);
+    }
+    run_graphed(c, c->gfwd, key, [&] {
+      xbs::launch_prep_x(c, d_x, M, c->stream, conv);
+      c->launches += 2;
+      enqueue_fwd_vmm(c, M, out);
+    });
+    c->have_forward = true;
+    c->M_fwd = M;
+    if (training) ++c->training_batches;  // layers.cpp:224
+    return;
+  }
   {
     StageScope st(c, XBS_STAGE_PREP_X);
     xbs::launch_prep_x(c, d_x, M, c->stream, conv);
@@ -409,21 +505,25 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, Ou
   if (calibrating(c) && training) xbs::calib_observe_fwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_FWD);
   c->launches += 1;
-  const int64_t ld = out.ld ? out.ld : M;
-  double* stage = out.host ? c->d_io_out : out.p;  // written with stride M
-  bool direct = false;
-  if (c->fully_ideal) {
-    xbs::launch_fwd_ideal(c, M, stage, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
-    xbs::launch_fwd_simt(c, M, stage, c->stream);
-  }
-  finish_out(c, Out{out.p, ld, out.host}, M, c->g.N, direct);
+  enqueue_fwd_vmm(c, M, out);
 }
 
 void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out out) {
   if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
   if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
   maybe_freeze_adc(c);
+  if (graphable(c, M)) {
+    const uint64_t key[8] = {u64(d_dy), uint64_t(M), u64(out.p), uint64_t(out.ld), uint64_t(out.host), u64(gd), 0, 0};
+    run_graphed(c, c->gbwd, key, [&] {
+      xbs::launch_prep_dy(c, d_dy, M, c->stream);
+      c->launches += 3;
+      if (c->kernel == 1 || !xbs::launch_dw_tc(c, M, gd, c->stream)) xbs::launch_dw(c, M, gd, c->stream);
+      c->launches += 2;
+      enqueue_bwd_vmm(c, d_dy, M, out);
+    });
+    c->have_grad = true;
+    return;
+  }
   {
     StageScope st(c, XBS_STAGE_PREP_DY);
     xbs::launch_prep_dy(c, d_dy, M, c->stream);
@@ -446,15 +546,7 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out 
   if (calibrating(c)) xbs::calib_observe_bwd(c, M, c->stream);
   StageScope st(c, XBS_STAGE_BWD);
   c->launches += 1;
-  const int64_t ld = out.ld ? out.ld : M;
-  double* stage = out.host ? c->d_io_out : out.p;
-  bool direct = false;
-  if (c->fully_ideal) {
-    xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
-    xbs::launch_bwd_simt(c, M, stage, c->stream);
-  }
-  finish_out(c, Out{out.p, ld, out.host}, M, c->g.K, direct);
+  enqueue_bwd_vmm(c, d_dy, M, out);
 }
 
 void apply_updates_device(xbs_core* c, uint64_t iteration) {
@@ -741,6 +833,8 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_e8);
   cudaFree(c->d_S64);
   cudaFree(c->d_acc32);
+  if (c->gfwd.exec) cudaGraphExecDestroy(c->gfwd.exec);
+  if (c->gbwd.exec) cudaGraphExecDestroy(c->gbwd.exec);
   cudaFree(c->d_io_in);
   cudaFree(c->d_io_out);
   for (auto& p : c->pending) {
@@ -941,6 +1035,7 @@ int xbs_core_select_kernel(xbs_core* c, int32_t kernel) {
   return guard([&] {
     if (!c || kernel < 0 || kernel > 1) fail(XBS_INVALID_ARGUMENT, "select_kernel: 0 (tcgen05) or 1 (SIMT)");
     c->kernel = kernel;
+    ++c->gen;
   });
 }
 
@@ -953,11 +1048,19 @@ int xbs_core_set_stream(xbs_core* c, void* stream) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
+      ++c->gen;
       c->own_stream = false;
     } else {
       ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
       c->own_stream = true;
     }
+  });
+}
+
+int xbs_core_use_graphs(xbs_core* c, int32_t enable) {
+  return guard([&] {
+    if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    c->use_graphs = enable != 0;
   });
 }
 

@@ -223,6 +223,7 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
       if (cudaMalloc(&c->d_S64, bytes) != cudaSuccess) return false;
       cudaMemsetAsync(c->d_S64, 0, bytes, st);
       c->S64_bytes = bytes;
+      ++c->gen;
     }
     a.S64 = c->d_S64;
   }

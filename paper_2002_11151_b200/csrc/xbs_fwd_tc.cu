@@ -380,6 +380,7 @@ int* acc32(xbs_core* c, size_t bytes, cudaStream_t st) {
     if (cudaMalloc(&c->d_acc32, bytes) != cudaSuccess) return nullptr;
     cudaMemsetAsync(c->d_acc32, 0, bytes, st);
     c->acc32_bytes = bytes;
+    ++c->gen;
   }
   return c->d_acc32;
 }

@@ -181,6 +181,18 @@ struct xbs_core {
   std::vector<double> h_tmp;
   // profiling: pending (stage, start, stop) event pairs, accumulated totals
   bool profile = false;
+  // CUDA graphs of the forward / backward launch sequences (xbs_core.cu):
+  // a call whose key repeats is captured once and replayed as one launch.
+  // gen changes whenever a kernel argument the key does not cover changes
+  // (buffers reallocated, ADC re-armed, kernel / stream switched).
+  bool use_graphs = true;
+  uint64_t gen = 0;
+  struct GraphSlot {
+    uint64_t key[8] = {};
+    bool seen = false, ready = false;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  } gfwd, gbwd;
   std::vector<cudaEvent_t> ev_pool;
   struct Pending { int stage; cudaEvent_t a, b; };
   std::vector<Pending> pending;

@@ -263,6 +263,7 @@ SYMBOLS = {
     "xbs_conv2d_backward_device": (ctypes.c_int, [_P, _P, _I64, _P]),
     "xbs_conv2d_apply_updates": (ctypes.c_int, [_P, ctypes.c_uint64]),
     "xbs_core_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
+    "xbs_core_use_graphs": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(_I64), ctypes.c_int32]),
     "xbs_core_launch_count": (_I64, [_P]),
 }
@@ -449,6 +450,10 @@ class CrossbarCore:
 
     def profile(self, enable: bool) -> None:
         _check(load_library().xbs_core_profile(self._h, int(bool(enable))))
+
+    def use_graphs(self, enable: bool) -> None:
+        """CUDA-graph replay of repeated forward / backward calls (default on)."""
+        _check(load_library().xbs_core_use_graphs(self._h, int(bool(enable))))
 
     def stage_times(self):
         """{stage: (total_ms, count)} accumulated while profiling."""
