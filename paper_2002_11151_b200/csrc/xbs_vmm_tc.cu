@@ -142,7 +142,7 @@ constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages<KB> * kBStage + 1024
 }  // namespace bw
 
 struct BwdArgs {
-  int GR, GC, S, db, TPe, tile_rows, R, C, K;
+  int GR, GC, S, db, TPe, tile_rows, tile_cols, R, C, K, N;
   int live, live_last;  // 64-row blocks holding logical rows per row tile / in the last row tile
   int n_rb;              // scheduled row blocks
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = row blocks fastest
@@ -189,7 +189,11 @@ __device__ __forceinline__ double bwd_k_out(const BwdArgs& a) {
   return k_out;
 }
 
-template <int KB>
+// TRIM: the layer has padded crossbar columns (N not a multiple of the tile
+// width, or tiles narrower than the 128-column device tile), so the MMA
+// issuer skips K = 32 steps made only of padding; without padding the
+// issue loop is the plain unrolled one.
+template <int KB, bool TRIM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const BwdArgs a) {
   using namespace bw;
@@ -287,8 +291,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = idesc_i8(256, 128, /*b_mn_major=*/false);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int ntc = min(a.GC, (u / a.nbase + 1) * a.tcs) - (u / a.nbase) * a.tcs;
+        const int tc0 = (u / a.nbase) * a.tcs, ntc = min(a.GC, tc0 + a.tcs) - tc0;
         for (int tc = 0; tc < ntc; ++tc) {
+          // crossbar columns holding logical outputs: padded columns carry a
+          // zero error, so K = 32 steps made only of padding are not issued
+          const int lcol = min(a.tile_cols, a.N - (tc0 + tc) * a.tile_cols);
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
           const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
@@ -303,6 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mbar_wait(&b_full[bs], bph);
               tc_fence_after();
               const uint64_t b0d = sdesc(smem_u32(sB + bs * kBStage), 16, 1024, 2);
+              const int nks = TRIM ? min(4, (lcol - kb * 128 + 31) >> 5) : 4;  // >= 1 for kb 0
               if (elect_one()) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
@@ -311,6 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
+                      if (TRIM && ks >= nks) break;
                       const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kPlane + 32 * ks);
                       const uint64_t bd = sdesc_add(b0d, (p * 2 + dh) * kBHalf + 32 * ks);
 #ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
@@ -466,9 +475,11 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.db = g.db;
   a.TPe = g.TPe;
   a.tile_rows = g.tile_rows;
+  a.tile_cols = g.tile_cols;
   a.R = g.R;
   a.C = g.C;
   a.K = g.K;
+  a.N = g.N;
   a.M = M;
   a.rowsB = rowsB;
   a.num_mbp = int(rowsB / 256);
@@ -507,13 +518,21 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_bwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<1>);
-    cudaFuncSetAttribute(k_bwd_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<2>);
+    cudaFuncSetAttribute(k_bwd_tc<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<1>);
+    cudaFuncSetAttribute(k_bwd_tc<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<2>);
+    cudaFuncSetAttribute(k_bwd_tc<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<1>);
+    cudaFuncSetAttribute(k_bwd_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<2>);
     attr = true;
   }
   const int grid = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
-  if (KB == 1) k_bwd_tc<1><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
-  else k_bwd_tc<2><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
+  const bool trim = (g.N % g.tile_cols) != 0 || g.tile_cols <= g.C - 32;
+  if (KB == 1) {
+    if (trim) k_bwd_tc<1, true><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
+    else k_bwd_tc<1, false><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
+  } else {
+    if (trim) k_bwd_tc<2, true><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
+    else k_bwd_tc<2, false><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
+  }
   if (a.acc) {
     const int64_t n = M * g.K;
     k_bwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * sm_count())), 256, 0, st>>>(a, M, g.K);
