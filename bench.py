@@ -554,6 +554,10 @@ def main():
         "prep_x": ("hbm", sum(L.M * L.K * (8 + 2 + 1 + 2 * 8) for L in layers) / 1e9, "GB/s"),
         "prep_dy": ("hbm", sum(L.M * L.N * (8 + 2 + 2 + 4 * 8) for L in layers) / 1e9, "GB/s"),
     }
+    conv = {}
+    for L in layers:
+        for k, v in cfg.adc_conversions(L).items():
+            conv[k] = conv.get(k, 0) + v
     roof_all = {}
     for st, (bound, amount, unit) in work.items():
         if per.get(st):
@@ -561,6 +565,12 @@ def main():
             pk = peak_tops if bound == "tensor" else hbm
             roof_all[st] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk,
                             "ms": per[st]}
+            if st in ("fwd_vmm", "bwd_vmm"):
+                # the ADC epilogue's work: conversions/s and MACs per conversion
+                # (the tensor fraction of a narrow layer is capped by the latter)
+                n = conv[st[:3]]
+                roof_all[st].update({"adc_conversions": n, "adc_conv_per_s": n / (per[st] * 1e-3),
+                                     "macs_per_conversion": macs[st[:3]] / n})
     dominant = max(("fwd_vmm", "bwd_vmm", "update", "dw", "prep_x", "prep_dy"), key=lambda s: per.get(s, 0.0))
     traffic = None
     tpath = args.traffic or os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")

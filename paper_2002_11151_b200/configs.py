@@ -108,6 +108,18 @@ class Config:
         u = layer.M * layer.K * layer.N
         return {"fwd": f, "bwd": b, "upd": u, "total": f + b + u}
 
+    def adc_conversions(self, layer: Layer, T_in: int = 8, T_err: int = 8) -> dict:
+        """Logical ADC conversions per step (on logical rather
+        than padded extents): forward one per (row, input plane, column,
+        crossbar row tile, slice, polarity); backward one per (row, error
+        plane, phase, device row, crossbar column tile, slice, polarity).
+        Each forward conversion sums min(K, tile) MACs and each backward one
+        min(N, tile): narrow layers do few MACs per conversion."""
+        S = self.weight_bits // self.device_bits
+        gr = -(-layer.K // self.tile)
+        gc = -(-layer.N // self.tile)
+        return {"fwd": layer.M * T_in * layer.N * gr * S * 2, "bwd": layer.M * T_err * 2 * layer.K * gc * S * 2}
+
 
 def _conv(name: str, cv: Conv) -> Layer:
     oh = (cv.h + 2 * cv.pad - cv.k) // cv.stride + 1

@@ -69,6 +69,8 @@ struct FwdArgs {
   int64_t M, rowsF;
   int num_mbp, num_units;  // num_units = base units (M-block pair x column unit) x ksplit
   int nbase, ksplit, trs;   // split-K (small layers): crossbar row tiles [sp * trs, +trs) per unit
+  FDiv f_nbase, f_mbp, f_nnb, f_live;  // divisions of the unit decode
+  int lg_tpi;                          // log2(TPi) (a power of two)
   int* acc;                 // ksplit > 1: int32 totals [N][M] (atomics), scaled by k_out in k_fwd_finalize
   double k_out;
   AdcConst adc;
@@ -79,8 +81,9 @@ struct FwdArgs {
 
 // Column unit index -> (tile column, 64-column unit); units made only of
 // padding are not scheduled.
+template <bool FAST>
 __device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int& h) {
-  tc = nb / a.live;
+  tc = udiv<FAST>(nb, a.live, a.f_live);
   if (tc >= a.GC - 1) {
     tc = a.GC - 1;
     h = nb - (a.GC - 1) * a.live;
@@ -90,15 +93,24 @@ __device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int&
 }
 
 // Unit index -> (M-block pair, column unit, row-tile range).
+template <bool FAST>
 __device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int& nb, int& tr0, int& tr1) {
-  const int ub = u % a.nbase, sp = u / a.nbase;
-  mbp = a.mfast ? ub % a.num_mbp : ub / a.n_nb;
-  nb = a.mfast ? ub / a.num_mbp : ub % a.n_nb;
+  const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
+  if (a.mfast) {
+    nb = udiv<FAST>(ub, a.num_mbp, a.f_mbp);
+    mbp = ub - nb * a.num_mbp;
+  } else {
+    mbp = udiv<FAST>(ub, a.n_nb, a.f_nnb);
+    nb = ub - mbp * a.n_nb;
+  }
   tr0 = sp * a.trs;
   tr1 = min(a.GR, tr0 + a.trs);
 }
 
-template <int KB>
+// NARROW: some 64-column units hold fewer than 64 logical columns (N or the
+// tile width not a multiple of 64), so epilogue warps skip the conversions
+// of padded columns; full-width layers keep the plain pipelined loop.
+template <int KB, bool NARROW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
   using namespace fw;
@@ -149,9 +161,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
         int mbp, nb, tr0, tr1;
-        fwd_unit(u, a, mbp, nb, tr0, tr1);
+        fwd_unit<NARROW>(u, a, mbp, nb, tr0, tr1);
         int tc, h;
-        col_unit(nb, a, tc, h);
+        col_unit<NARROW>(nb, a, tc, h);
         const int mrow = (2 * mbp + int(rank)) * 128;
         for (int tr = tr0; tr < tr1; ++tr) {
           mbar_wait(&a_empty[as], aph ^ 1);
@@ -191,7 +203,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       constexpr uint32_t idesc = idesc_i8(256, 2 * kCW, /*b_mn_major=*/true);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int ntr = min(a.GR, (u / a.nbase + 1) * a.trs) - (u / a.nbase) * a.trs;
+        const int usp = udiv<NARROW>(u, a.nbase, a.f_nbase);
+        const int ntr = min(a.GR, (usp + 1) * a.trs) - usp * a.trs;
         for (int tr = 0; tr < ntr; ++tr) {
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
@@ -243,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     const AdcConst k = a.adc;
     for (int u = cid; u < a.num_units; u += ncl) {
       int mbp, nb, tr0, tr1;
-      fwd_unit(u, a, mbp, nb, tr0, tr1);
+      fwd_unit<NARROW>(u, a, mbp, nb, tr0, tr1);
       const int nchain = (tr1 - tr0) * a.S * 2;
       float P[kCPW];
 #pragma unroll
@@ -258,6 +271,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       // the other is converted (A: columns 0-15, B: 16-31 of this warp)
       static_assert(kCPW == 32, "pipelined epilogue: 32 columns per warp");
       uint32_t alo[16], ahi[16], blo[16], bhi[16];
+      // logical columns in this warp's 32 (narrow layers: N or the tile
+      // width below the unit's 64 device columns); padded columns are
+      // discarded (layers.cpp:283), so their conversions are skipped
+      int nv = kCPW;
+      if constexpr (NARROW) {
+        int tcu, hu;
+        col_unit<NARROW>(nb, a, tcu, hu);
+        nv = min(a.tile_cols, a.N - tcu * a.tile_cols) - hu * kCW - kCPW * q;
+      }
+      if (NARROW && nv <= 16) {
+        // at most the first 16 columns: one TMEM read and conversion per chain
+        // (none when the warp holds only padding); barrier protocol unchanged
+        for (int c = 0; c < nchain; ++c) {
+          const float w = (sp & 1) == 0 ? wmag : -wmag;
+          if (++sp == 2 * a.S) {
+            sp = 0;
+            wmag = k.unscale;
+          } else if ((sp & 1) == 0) {
+            wmag = __fmul_rn(wmag, wstep);
+          }
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+          if (nv > 0) {
+            tmem_ld16(tl + ab * 128, alo);
+            tmem_ld16(tl + ab * 128 + kCW, ahi);
+            tmem_wait_ld();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          if (nv > 0) adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
+        }
+        if (nv <= 0) continue;  // no logical output columns: nothing to combine
+      } else {
       mbar_wait_hint(&t_full[ab], abph);
       tc_fence_after();
       tmem_ld16(tl + ab * 128, alo);
@@ -287,6 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         }
         adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, w, P, 16, exact);
         tmem_wait_ld();
+      }
       }
 #else
       for (int c = 0; c < nchain; ++c) {
@@ -329,11 +378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
       // (exact in int32: host-checked bound); per 16 columns, lane q ends
       // with the totals of columns q * (16 / TPi) + i
-      const int kk = ml % a.TPi;
-      const int64_t b = (int64_t(2 * mbp + int(rank)) * 128 + ml) / a.TPi;
+      const int kk = NARROW ? ml & (a.TPi - 1) : ml % a.TPi;
+      const int64_t b = NARROW ? (int64_t(2 * mbp + int(rank)) * 128 + ml) >> a.lg_tpi
+                               : (int64_t(2 * mbp + int(rank)) * 128 + ml) / a.TPi;
       int tc, hcol;
-      col_unit(nb, a, tc, hcol);
-      const int per = 16 / a.TPi;
+      col_unit<NARROW>(nb, a, tc, hcol);
+      const int per = NARROW ? 16 >> a.lg_tpi : 16 / a.TPi;
 #pragma unroll
       for (int h = 0; h < kCPW / 16; ++h) {
         int v[16];
@@ -407,6 +457,8 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.S = g.S;
   a.db = g.db;
   a.TPi = g.TPi;
+  a.lg_tpi = 0;
+  while ((1 << a.lg_tpi) < g.TPi) ++a.lg_tpi;
   a.tile_cols = g.tile_cols;
   a.C = g.C;
   a.R = g.R;
@@ -427,6 +479,10 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.trs = (g.GR + a.ksplit - 1) / a.ksplit;
   a.ksplit = (g.GR + a.trs - 1) / a.trs;
   a.num_units = a.nbase * a.ksplit;
+  a.f_nbase = make_fdiv(uint32_t(a.nbase));
+  a.f_mbp = make_fdiv(uint32_t(a.num_mbp));
+  a.f_nnb = make_fdiv(uint32_t(a.n_nb));
+  a.f_live = make_fdiv(uint32_t(a.live));
   a.acc = nullptr;
   if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.N * 4, st))) return false;
   {  // sweep the larger operand once: A (input planes) vs the conductance digits
@@ -445,13 +501,21 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.ctr = &c->d_sc->exact_path;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fwd_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
-    cudaFuncSetAttribute(k_fwd_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
+    cudaFuncSetAttribute(k_fwd_tc<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
+    cudaFuncSetAttribute(k_fwd_tc<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
+    cudaFuncSetAttribute(k_fwd_tc<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
+    cudaFuncSetAttribute(k_fwd_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
     attr = true;
   }
   const int grid = 2 * std::min(a.num_units, num_sms() / 2);  // CTA pairs
-  if (g.R == 128) k_fwd_tc<1><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
-  else k_fwd_tc<2><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
+  const bool narrow = (g.tile_cols % fw::kCW) != 0 || ((g.N - (g.GC - 1) * g.tile_cols) % fw::kCW) != 0;
+  if (g.R == 128) {
+    if (narrow) k_fwd_tc<1, true><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
+    else k_fwd_tc<1, false><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
+  } else {
+    if (narrow) k_fwd_tc<2, true><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
+    else k_fwd_tc<2, false><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
+  }
   if (a.acc) {
     const int64_t n = M * g.N;
     k_fwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * num_sms())), 256, 0, st>>>(M, g.N, a.k_out, a.acc,

@@ -239,6 +239,32 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 // on the host so that no constant overflows and no x' is subnormal).  The
 // rounding magic, clamp and threshold are scaled alike, and the shift-add
 // weights by 2^s, so P still sums true codes.
+// Unsigned division by a runtime divisor fixed per launch (unit decode in
+// the persistent VMM loops): q = (umulhi(n, m) + n) >> s with
+// s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1, exact for n < 2^31.
+// Three instructions instead of the ~25 of a signed runtime division.
+struct FDiv {
+  uint32_t d, m, s;
+};
+inline FDiv make_fdiv(uint32_t d) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  const uint32_t m = uint32_t(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  return FDiv{d, m, s};
+}
+__device__ __forceinline__ int fdiv(int n, const FDiv& f) {
+  return int((__umulhi(uint32_t(n), f.m) + uint32_t(n)) >> f.s);
+}
+
+// n / d through the FDiv (FAST) or the plain runtime division: the narrow-
+// layer instantiations (many short units) take the former; full-width
+// layers keep the division, whose code layout their hot loops were tuned on.
+template <bool FAST>
+__device__ __forceinline__ int udiv(int n, int d, const FDiv& f) {
+  if constexpr (FAST) return fdiv(n, f);
+  else return n / d;
+}
+
 struct AdcConst {
   float c_hi, c_lo, maxc;  // scaled: c * 2^(149 - s), maxc * 2^-s
   float thr;               // (0.5 - delta) * 2^-s

@@ -149,6 +149,8 @@ struct BwdArgs {
   int64_t M, rowsB;
   int num_mbp, num_units;  // num_units = base units (M-block pair x row block) x ksplit
   int nbase, ksplit, tcs;   // split-K (small layers): crossbar column tiles [sp * tcs, +tcs) per unit
+  FDiv f_nbase, f_mbp, f_nrb, f_live;  // divisions of the unit decode
+  int lg_grp;                          // log2(2 TPe) (TPe a power of two)
   int* acc;                 // ksplit > 1: int32 totals [K][M] (atomics), scaled in k_bwd_finalize
   double F, vu, ifs_fac, lev_e;
   int adc_scaled;
@@ -161,8 +163,9 @@ struct BwdArgs {
 
 // Row block index -> (row tile, 64-row half); blocks made only of padding
 // (beyond K in the last row tile) are not scheduled.
+template <bool FAST>
 __device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int& rh) {
-  tr = rb / a.live;
+  tr = udiv<FAST>(rb, a.live, a.f_live);
   if (tr >= a.GR - 1) {
     tr = a.GR - 1;
     rh = rb - (a.GR - 1) * a.live;
@@ -172,10 +175,16 @@ __device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int
 }
 
 // Unit index -> (M-block pair, row block, column-tile range).
+template <bool FAST>
 __device__ __forceinline__ void bwd_unit(int u, const BwdArgs& a, int& mbp, int& rb, int& tc0, int& tc1) {
-  const int ub = u % a.nbase, sp = u / a.nbase;
-  mbp = a.mfast ? ub % a.num_mbp : ub / a.n_rb;
-  rb = a.mfast ? ub / a.num_mbp : ub % a.n_rb;
+  const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
+  if (a.mfast) {
+    rb = udiv<FAST>(ub, a.num_mbp, a.f_mbp);
+    mbp = ub - rb * a.num_mbp;
+  } else {
+    mbp = udiv<FAST>(ub, a.n_rb, a.f_nrb);
+    rb = ub - mbp * a.n_rb;
+  }
   tc0 = sp * a.tcs;
   tc1 = min(a.GC, tc0 + a.tcs);
 }
@@ -191,8 +200,9 @@ __device__ __forceinline__ double bwd_k_out(const BwdArgs& a) {
 
 // TRIM: the layer has padded crossbar columns (N not a multiple of the tile
 // width, or tiles narrower than the 128-column device tile), so the MMA
-// issuer skips K = 32 steps made only of padding; without padding the
-// issue loop is the plain unrolled one.
+// issuer skips K = 32 steps made only of padding, or padded crossbar rows
+// inside a scheduled 64-row block, whose conversions the epilogue warps
+// skip; without padding the issue and epilogue loops are the plain ones.
 template <int KB, bool TRIM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const BwdArgs a) {
@@ -244,9 +254,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
         int mbp, rb, tc0, tc1;
-        bwd_unit(u, a, mbp, rb, tc0, tc1);
+        bwd_unit<TRIM>(u, a, mbp, rb, tc0, tc1);
         int tr, rh;
-        row_block(rb, a, tr, rh);
+        row_block<TRIM>(rb, a, tr, rh);
         const int mrow = (2 * mbp + int(rank)) * 128;
         for (int tc = tc0; tc < tc1; ++tc) {
           mbar_wait(&a_empty[as], aph ^ 1);
@@ -291,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = idesc_i8(256, 128, /*b_mn_major=*/false);
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
-        const int tc0 = (u / a.nbase) * a.tcs, ntc = min(a.GC, tc0 + a.tcs) - tc0;
+        const int tc0 = udiv<TRIM>(u, a.nbase, a.f_nbase) * a.tcs, ntc = min(a.GC, tc0 + a.tcs) - tc0;
         for (int tc = 0; tc < ntc; ++tc) {
           // crossbar columns holding logical outputs: padded columns carry a
           // zero error, so K = 32 steps made only of padding are not issued
@@ -359,10 +369,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const double k_out = bwd_k_out(a);  // layers.cpp:375-377
     for (int u = cid; u < a.num_units; u += ncl) {
       int mbp, rb, tc0, tc1;
-      bwd_unit(u, a, mbp, rb, tc0, tc1);
+      bwd_unit<TRIM>(u, a, mbp, rb, tc0, tc1);
       const int nchain = (tc1 - tc0) * a.S;
       int tr, rh;
-      row_block(rb, a, tr, rh);
+      row_block<TRIM>(rb, a, tr, rh);
+      // logical device rows among this warp's kRows: rows beyond K (or the
+      // tile height) are discarded (layers.cpp:378), so a warp holding only
+      // padding skips its TMEM reads and conversions (barrier protocol kept)
+      const int nvr = TRIM ? min(a.tile_rows, a.K - tr * a.tile_rows) - rh * 64 - kRows * ch : kRows;
       float P[kRows];
 #pragma unroll
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
@@ -386,36 +400,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait_hint(&t_full[ab], abph);
           tc_fence_after();
           const uint32_t ta = tl + ab * 128;
+          if (!TRIM || nvr > 0) {
 #pragma unroll
-          for (int h = 0; h < kRows / 16; ++h) {
-            tmem_ld16(ta + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
-            tmem_ld16(ta + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+            for (int h = 0; h < kRows / 16; ++h) {
+              tmem_ld16(ta + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
+              tmem_ld16(ta + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+            }
+            tmem_wait_ld();
           }
-          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
           if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          if (TRIM && nvr <= 0) continue;
           const float wp = p == 0 ? wpos : wneg;
 #ifdef XBS_STUB_EPI  // perf experiment hook: TMEM loads and barriers only
           if (lo[0] == 0xdeadbeef && hi[kRows - 1] == 0x12345) P[0] += wp;
           continue;
 #endif
           adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
-          adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
+          if (!TRIM || nvr > 8) adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
           if constexpr (kRows >= 32) {
-            adc_conv8<16>(lo, hi, k, wp, P, 16, exact);
-            adc_conv8<24>(lo, hi, k, wp, P, 24, exact);
+            if (!TRIM || nvr > 16) adc_conv8<16>(lo, hi, k, wp, P, 16, exact);
+            if (!TRIM || nvr > 24) adc_conv8<24>(lo, hi, k, wp, P, 24, exact);
           }
         }
       }
+      if (TRIM && nvr <= 0) continue;  // no logical output rows: nothing to combine
       // combine the 2*TPe (plane, phase) lanes of each batch row (exact in
       // int32: host-checked bound); lane q ends with the totals of rows
       // q * (16 / grp) + i (grp = 32: lanes q, q ^ 1 share row q >> 1)
       const int grp = 2 * a.TPe;
-      const int q = ml % grp, kk = q >> 1;
-      const int64_t b = int64_t(2 * mbp + int(rank)) * (128 / grp) + ml / grp;
-      const int per = grp <= 16 ? 16 / grp : 1;
+      const int q = TRIM ? ml & (grp - 1) : ml % grp, kk = q >> 1;
+      const int64_t b = TRIM ? int64_t(2 * mbp + int(rank)) * (128 >> a.lg_grp) + (ml >> a.lg_grp)
+                             : int64_t(2 * mbp + int(rank)) * (128 / grp) + ml / grp;
+      const int per = grp <= 16 ? (TRIM ? 16 >> a.lg_grp : 16 / grp) : 1;
       const int j0 = grp <= 16 ? q * per : (q >> 1);
       const bool writer = grp <= 16 || (q & 1) == 0;
 #pragma unroll
@@ -474,6 +493,8 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.S = g.S;
   a.db = g.db;
   a.TPe = g.TPe;
+  a.lg_grp = 1;
+  while ((1 << a.lg_grp) < 2 * g.TPe) ++a.lg_grp;
   a.tile_rows = g.tile_rows;
   a.tile_cols = g.tile_cols;
   a.R = g.R;
@@ -495,6 +516,10 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.tcs = (g.GC + a.ksplit - 1) / a.ksplit;
   a.ksplit = (g.GC + a.tcs - 1) / a.tcs;
   a.num_units = a.nbase * a.ksplit;
+  a.f_nbase = make_fdiv(uint32_t(a.nbase));
+  a.f_mbp = make_fdiv(uint32_t(a.num_mbp));
+  a.f_nrb = make_fdiv(uint32_t(a.n_rb));
+  a.f_live = make_fdiv(uint32_t(a.live));
   a.acc = nullptr;
   if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.K * 4, st))) return false;
   {  // sweep the larger operand once: A' (error planes) vs the conductance digits
@@ -525,7 +550,8 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
     attr = true;
   }
   const int grid = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
-  const bool trim = (g.N % g.tile_cols) != 0 || g.tile_cols <= g.C - 32;
+  const bool trim = (g.N % g.tile_cols) != 0 || g.tile_cols <= g.C - 32 || (g.tile_rows % 64) != 0 ||
+                    ((g.K - (g.GR - 1) * g.tile_rows) % 64) != 0;
   if (KB == 1) {
     if (trim) k_bwd_tc<1, true><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
     else k_bwd_tc<1, false><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
