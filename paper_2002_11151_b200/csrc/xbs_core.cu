@@ -203,9 +203,26 @@ void ensure_io(xbs_core* c, int64_t elems) {
   c->io_cap = elems;
 }
 
+void finish_update_stats(xbs_core* c);
+
+// Completes a deferred apply_updates: its regeneration time (CUDA events,
+// the reference times regenerate() on the host, layers.cpp:176-177) and the
+// |W| / |dW| statistics.  Every entry point that observes core state calls
+// this (directly or through sync) before reading.
+void settle(xbs_core* c) {
+  if (!c->upd_pending) return;
+  c->upd_pending = false;
+  ck(cudaEventSynchronize(c->upd_ev1), "kernel execution");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, c->upd_ev0, c->upd_ev1), "update timing");
+  c->conversion_seconds += 1e-3 * ms;
+  finish_update_stats(c);
+}
+
 void sync(xbs_core* c) {
   ck(cudaStreamSynchronize(c->stream), "kernel execution");
   ck(cudaGetLastError(), "kernel launch");
+  settle(c);
 }
 
 void regenerate_bookkeeping(xbs_core* c) {
@@ -575,6 +592,7 @@ void apply_updates_device(xbs_core* c, uint64_t iteration) {
 }
 
 void finish_update_stats(xbs_core* c) {
+  c->upd_pending = false;
   ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
   if (c->h_sc->err_flag) fail(XBS_INVALID_ARGUMENT, "nonlinear_update: g outside device range");
   check_fcm(c);
@@ -809,6 +827,13 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
 void xbs_core_destroy(xbs_core* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->copy_ev) cudaEventDestroy(c->copy_ev);
+  if (c->upd_ev0) cudaEventDestroy(c->upd_ev0);
+  if (c->upd_ev1) cudaEventDestroy(c->upd_ev1);
   cudaFree(c->d_digits);
   cudaFree(c->d_adc_tab);
   cudaFree(c->d_adc_tab_b);
@@ -853,10 +878,23 @@ int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t K, int64_t
     if (K != c->g.K) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: feature count mismatch");  // layers.cpp:216-217
     if (M < 0 || (M > 0 && (ldx < M || ldy < M || !x || !y))) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: bad buffers");
     ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
-    if (M > 0)
+    if (M > 0 && c->upd_pending) {
+      // the pending update does not touch the staging buffer: copy x on the
+      // side stream while it runs, and order the forward after both
+      if (!c->copy_stream) {
+        ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&c->copy_ev, cudaEventDisableTiming), "cudaEventCreate");
+      }
+      ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, x, size_t(ldx) * 8, size_t(M) * 8, size_t(c->g.K),
+                           cudaMemcpyHostToDevice, c->copy_stream),
+         "H2D x");
+      ck(cudaEventRecord(c->copy_ev, c->copy_stream), "event record");
+      ck(cudaStreamWaitEvent(c->stream, c->copy_ev, 0), "stream wait");
+    } else if (M > 0) {
       ck(cudaMemcpy2DAsync(c->d_io_in, size_t(M) * 8, x, size_t(ldx) * 8, size_t(M) * 8, size_t(c->g.K),
                            cudaMemcpyHostToDevice, c->stream),
          "H2D x");
+    }
     double* ym = M > 0 ? mapped_alias(y) : nullptr;  // pinned: the kernel stores y into it
     forward_device(c, c->d_io_in, M, training != 0, ym ? Out{ym, ldy, true} : Out{c->d_io_out, 0, false});
     if (M > 0 && !ym)
@@ -893,6 +931,26 @@ int xbs_core_apply_updates(xbs_core* c, uint64_t iteration) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
     if (!c->have_grad) return;
+    settle(c);
+    // Engines whose update cannot raise (AAM / ideal regeneration, linear
+    // update: no range check, update.cpp:28-29, no FCM convergence) return
+    // before the kernels finish; the next call settles timing and statistics
+    // and a forward overlaps its input copy with them.  Others stay
+    // synchronous so their exceptions surface here, as in the reference.
+    const bool defer = (c->opt.engine == XBS_ENGINE_AAM || c->opt.engine == XBS_ENGINE_IDEAL) &&
+                       c->opt.upd_v == 0.0 && !c->profile;
+    if (defer) {
+      if (!c->upd_ev0) {
+        ck(cudaEventCreate(&c->upd_ev0), "cudaEventCreate");
+        ck(cudaEventCreate(&c->upd_ev1), "cudaEventCreate");
+      }
+      ck(cudaEventRecord(c->upd_ev0, c->stream), "event record");
+      apply_updates_device(c, iteration);
+      ck(cudaEventRecord(c->upd_ev1, c->stream), "event record");
+      ck(cudaGetLastError(), "kernel launch");
+      c->upd_pending = true;
+      return;
+    }
     const auto t0 = std::chrono::steady_clock::now();
     apply_updates_device(c, iteration);
     sync(c);
@@ -916,6 +974,7 @@ int xbs_core_backward_device(xbs_core* c, const double* d_dy, int64_t M, double 
 int xbs_core_apply_updates_device(xbs_core* c, uint64_t iteration) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    settle(c);  // its statistics are read before this update resets them
     apply_updates_device(c, iteration);
   });
 }
@@ -930,6 +989,7 @@ int xbs_core_synchronize(xbs_core* c) {
 int xbs_core_get_info(xbs_core* c, xbs_core_info* info) {
   return guard([&] {
     if (!c || !info) fail(XBS_INVALID_ARGUMENT, "null argument");
+    settle(c);
     std::memset(info, 0, sizeof(*info));
     info->in_features = c->g.K;
     info->out_features = c->g.N;
@@ -1034,6 +1094,7 @@ int xbs_core_adc_counters(xbs_core* c, int64_t* exact_path, int64_t* conversions
 int xbs_core_select_kernel(xbs_core* c, int32_t kernel) {
   return guard([&] {
     if (!c || kernel < 0 || kernel > 1) fail(XBS_INVALID_ARGUMENT, "select_kernel: 0 (tcgen05) or 1 (SIMT)");
+    settle(c);
     c->kernel = kernel;
     ++c->gen;
   });
@@ -1060,6 +1121,7 @@ int xbs_core_set_stream(xbs_core* c, void* stream) {
 int xbs_core_use_graphs(xbs_core* c, int32_t enable) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    settle(c);
     c->use_graphs = enable != 0;
   });
 }
@@ -1067,6 +1129,7 @@ int xbs_core_use_graphs(xbs_core* c, int32_t enable) {
 int xbs_core_profile(xbs_core* c, int32_t enable) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
+    settle(c);
     collect_stage_times(c);
     c->profile = enable != 0;
     for (int i = 0; i < XBS_NUM_STAGES; ++i) {
@@ -1079,6 +1142,7 @@ int xbs_core_profile(xbs_core* c, int32_t enable) {
 int xbs_core_stage_times(xbs_core* c, double* ms, int64_t* count, int32_t n) {
   return guard([&] {
     if (!c || n < 0 || n > XBS_NUM_STAGES) fail(XBS_INVALID_ARGUMENT, "stage_times: bad arguments");
+    settle(c);
     collect_stage_times(c);
     for (int i = 0; i < n; ++i) {
       if (ms) ms[i] = c->stage_ms[i];

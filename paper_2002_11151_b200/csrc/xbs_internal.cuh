@@ -117,6 +117,12 @@ struct xbs_core {
   bool tile_engine = false;     // fcm / interp_fcm with parasitics: per-tile regeneration kernels
   uint64_t update_count = 0;    // layers.cpp:389 (interp refresh schedule)
   cudaStream_t stream = nullptr;
+  // deferred apply_updates (host API, engines that cannot raise from the
+  // update): completion and statistics are settled by the next call
+  bool upd_pending = false;
+  cudaEvent_t upd_ev0 = nullptr, upd_ev1 = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host->device input copies overlapping a pending update
+  cudaEvent_t copy_ev = nullptr;
   bool own_stream = true;  // false after xbs_core_set_stream(caller's stream)
   int kernel = 0;  // 0 tcgen05, 1 SIMT
   bool fully_ideal = false;
