@@ -60,3 +60,37 @@ def test_pinned_outputs_bit_identical(kernel, pad):
     orc = oracle_py.OracleCore(W, opt, snapped=True)
     assert np.array_equal(y[:M], orc.forward(x, True))
     assert np.array_equal(dx[:M], orc.backward(dy, 1.0))
+
+
+def test_deferred_update_matches_synchronous():
+    """Host apply_updates on an AAM / linear-update core returns before the
+    update finishes; every later call settles it first.  The
+    trajectory, the statistics and the next forward (whose input copy
+    overlaps the pending update) equal those of the synchronous path
+    (profiling on keeps apply_updates synchronous)."""
+    from helpers import aam_options, normal, rand, xb
+
+    W = normal((300, 200), 71, 0.05)
+    x = rand((48, 300), 72, 0.0, 1.0)
+    dy = rand((48, 200), 73)
+    opt = aam_options(tile=128, adc_bits=7, i_fs=1.8e-4, r_col=4.6)
+    runs = []
+    for sync_path in (False, True):
+        c = xb.CrossbarCore(W, opt)
+        if sync_path:
+            c.profile(True)
+        ys, stats = [], []
+        for it in range(3):
+            ys.append(c.forward(x, True).copy())
+            c.backward(dy, 1.0)
+            c.apply_updates(it)
+            stats.append((c.weight_abs_max_seen(), c.grad_abs_max_seen(), c.refresh_count()))
+        ys.append(c.forward(x, False).copy())
+        assert c.conversion_seconds() > 0.0
+        runs.append((ys, stats, [c.master_diff(s).copy() for s in range(opt.map.num_slices())]))
+    (ya, sa, ma), (yb, sb, mb) = runs
+    for a, b in zip(ya, yb):
+        assert np.array_equal(a, b)
+    assert sa == sb
+    for a, b in zip(ma, mb):
+        assert np.array_equal(a, b)
