@@ -126,7 +126,12 @@ int xbs_core_forward(xbs_core* core, const double* x, int64_t M, int64_t K, int6
  * forward batch -> XBS_INVALID_ARGUMENT (layers.cpp:287-290). */
 int xbs_core_backward(xbs_core* core, const double* dy, int64_t M, int64_t N, int64_t lddy, double grad_divisor,
                       double* dx, int64_t lddx);
-/* CrossbarCore::apply_updates(iteration) — layers.cpp:382-391. */
+/* CrossbarCore::apply_updates(iteration) — layers.cpp:382-391.  When the
+ * update cannot raise (engine AAM or ideal, update.v == 0, profiling off) the
+ * call returns once the update is queued on the core's stream; every later
+ * call on the core settles it (statistics, conversion_seconds) before it
+ * reads state, so results are those of the synchronous call.  Other engines
+ * return after completion, so ConvergenceError / range errors surface here. */
 int xbs_core_apply_updates(xbs_core* core, uint64_t iteration);
 
 /* Device-resident variants (HBM pointers, column-major, ld = M): enqueue on
