@@ -1,0 +1,76 @@
+"""BASELINE configs[0] end to end: the MLP 784-256-10
+train step at full size (batch 64, 64x64 crossbars, 4 two-bit slices, 6-bit
+ADC, 1 kOhm source / sense, variation sigma = 0.1) through the reference's
+layer stack -- CrossbarLinear -> ReLU -> CrossbarLinear -> softmax CE
+(train.cpp:11-33) -> backward x2 -> apply_updates (train.cpp:93-144) -- on
+the GPU (C ABI) against the same stack on the snapped CPU oracle, for three
+iterations.  Bar: logits, loss, dW and dx bit-exact; the non-ideal
+conductances regenerated after each update equal the oracle's up to libm
+ulp flips in the variation Gaussian (CUDA vs glibc), which are counted and
+fed back so the trajectories stay comparable (as in test_parity_gpu)."""
+import numpy as np
+import pytest
+
+from helpers import xb
+
+pytestmark = pytest.mark.gpu
+oracle_py = pytest.importorskip("oracle_py")
+
+from paper_2002_11151_b200.configs import CONFIGS  # noqa: E402
+from test_parity_gpu import _sync_conductances  # noqa: E402
+
+
+class _OracleLinear(xb.Layer):
+    def __init__(self, W, opt):
+        self.c = oracle_py.OracleCore(W, opt, snapped=True)
+
+    def forward(self, x, training):
+        return xb.Tensor(self.c.forward(x.values, training), [self.c.N])
+
+    def backward(self, dy):
+        return xb.Tensor(self.c.backward(dy.values, 1.0), [self.c.K])
+
+    def apply_updates(self, it):
+        self.c.apply_updates(it)
+
+
+def _step(net, x, labels, it):
+    h = xb.Tensor(x, [x.shape[1]])
+    for layer in net:
+        h = layer.forward(h, True)
+    loss, d = xb.softmax_cross_entropy(h.values, labels)
+    g = xb.Tensor(d, [d.shape[1]])
+    grads = []
+    for layer in reversed(net):
+        g = layer.backward(g)
+        grads.append(g.values.copy())
+    for layer in net:
+        layer.apply_updates(it)
+    return h.values.copy(), loss, grads
+
+
+def test_c1_mlp_train_step_matches_oracle():
+    cfg = CONFIGS["c1"]
+    opt = cfg.options()
+    L1, L2 = cfg.layers
+    W1, W2 = cfg.weights(L1, 0), cfg.weights(L2, 1)
+    x = cfg.inputs(L1)
+    labels = np.random.default_rng(6000 + cfg.cid).integers(0, 10, size=L1.M)
+    gpu = [xb.CrossbarLinear(W1, opt), xb.ReLU(), xb.CrossbarLinear(W2, opt)]
+    orc = [_OracleLinear(W1, opt), xb.ReLU(), _OracleLinear(W2, opt)]
+    flips = 0
+    for g, o in ((gpu[0], orc[0]), (gpu[2], orc[2])):
+        flips += _sync_conductances(g.core(), o.c, opt)
+    for it in range(3):
+        lg, loss_g, grads_g = _step(gpu, x, labels, it)
+        lo, loss_o, grads_o = _step(orc, x, labels, it)
+        assert np.array_equal(lg, lo), it
+        assert loss_g == loss_o, it
+        for a, b in zip(grads_g, grads_o):
+            assert np.array_equal(a, b), it
+        for g, o in ((gpu[0], orc[0]), (gpu[2], orc[2])):
+            assert np.array_equal(g.core().gradient(), o.c.gradient()), it
+            flips += _sync_conductances(g.core(), o.c, opt)
+    # libm flips are rare (a snapped value one grid step off at a tie)
+    n_dev = 2 * opt.map.num_slices() * (832 * 256 + 256 * 64)
+    assert flips <= 1e-4 * n_dev * 4
