@@ -470,6 +470,11 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     launches = sum(c.launch_count() for c in cores) - launches0
+    fallbacks = sum(int(c.info().tc_fallbacks) for c in cores)
+    if fallbacks:  # a VMM left the tcgen05 kernels (exact SIMT ran): not a valid tensor-core measurement
+        print(json.dumps({"error": f"{fallbacks} tcgen05->SIMT VMM fallbacks during the bench", "config": cfg.name}),
+              file=sys.stderr)
+        sys.exit(3)
     # per-stage kernel times: the same K steps again with CUDA events around
     # every stage (eager launches; the timed steps above replay the cores'
     # captured graphs, which per-stage events would split)
@@ -597,6 +602,7 @@ def main():
         "int8_peak_tops": peak_tops,
         "macs_per_step": macs,
         "gpu_launches": launches,
+        "tc_fallbacks": fallbacks,
         "clocks": clk,
     }
     if e2e:

@@ -118,23 +118,21 @@ class CrossbarCore {
   MatrixXd backward(const MatrixXd& dy, double grad_divisor) {
     MatrixXd dx(dy.rows(), in_features());
     detail::check(xbs_core_backward(h_.get(), dy.data(), dy.rows(), dy.cols(), ld(dy), grad_divisor, dx.data(), ld(dx)));
-    grad_valid_ = false;
     return dx;
   }
   void apply_updates(std::uint64_t iteration) {
     detail::check(xbs_core_apply_updates(h_.get(), iteration));
-    grad_valid_ = false;
   }
 
   int in_features() const { return info().in_features; }
   int out_features() const { return info().out_features; }
   mapping::TiledLayerWeights weights() const { return mapping::TiledLayerWeights(h_.get()); }
+  /// Fetched on every call: a conv layer, set_gradient or a raw handle()
+  /// caller can replace dW behind this wrapper's back.  The reference stays
+  /// valid until the next mutating call; this copy until the next gradient().
   const MatrixXd& gradient() const {
-    if (!grad_valid_) {
-      dW_.resize(in_features(), out_features());
-      detail::check(xbs_core_gradient(h_.get(), dW_.data(), ld(dW_)));
-      grad_valid_ = true;
-    }
+    dW_.resize(in_features(), out_features());
+    detail::check(xbs_core_gradient(h_.get(), dW_.data(), ld(dW_)));
     return dW_;
   }
   long refresh_count() const { return static_cast<long>(info().refresh_count); }
@@ -157,11 +155,9 @@ class CrossbarCore {
   }
   void backward_device(const double* d_dy, std::int64_t M, double grad_divisor, double* d_dx) {
     detail::check(xbs_core_backward_device(h_.get(), d_dy, M, grad_divisor, d_dx));
-    grad_valid_ = false;
   }
   void apply_updates_device(std::uint64_t iteration) {
     detail::check(xbs_core_apply_updates_device(h_.get(), iteration));
-    grad_valid_ = false;
   }
   void synchronize() { detail::check(xbs_core_synchronize(h_.get())); }
   /// Enqueue on the caller's cudaStream_t (nullptr: a private stream).
@@ -178,7 +174,6 @@ class CrossbarCore {
   }
   std::unique_ptr<xbs_core, core_detail::CoreDeleter> h_;
   mutable MatrixXd dW_, tile_;
-  mutable bool grad_valid_ = false;
 };
 
 /// reference layers.hpp:113-121

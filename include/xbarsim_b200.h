@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define XBS_ABI_VERSION 2
+#define XBS_ABI_VERSION 3
 
 /* Status codes: one per reference exception class (errors.hpp:10-47). */
 typedef enum xbs_status {
@@ -101,6 +101,10 @@ typedef struct xbs_core_info {
   double forward_adc_full_scale;              /* forward_adc_full_scale()    */
   int32_t fully_ideal;                        /* fully_ideal() fast path     */
   int32_t kernel;                             /* 0 = tcgen05, 1 = SIMT check */
+  int64_t tc_fallbacks;                       /* forward / backward VMM calls whose
+                                                 shape left the tcgen05 kernels'
+                                                 exact int32 / fp32 bounds, so the
+                                                 exact SIMT kernel ran instead  */
 } xbs_core_info;
 
 typedef struct xbs_core xbs_core;

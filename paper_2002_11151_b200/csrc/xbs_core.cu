@@ -203,20 +203,42 @@ void ensure_io(xbs_core* c, int64_t elems) {
   c->io_cap = elems;
 }
 
-void finish_update_stats(xbs_core* c);
+void check_fcm(xbs_core* c);
+cudaEvent_t take_event(xbs_core* c);
 
-// Completes a deferred apply_updates: its regeneration time (CUDA events,
-// the reference times regenerate() on the host, layers.cpp:176-177) and the
-// |W| / |dW| statistics.  Every entry point that observes core state calls
-// this (directly or through sync) before reading.
+// Folds the statistics of the updates enqueued since the last fold, once
+// their kernels are complete: update time from CUDA events into
+// conversion_seconds (the reference times regenerate(), layers.cpp:176-177),
+// the running |dW| / |W| maxima the device keeps across updates
+// (layers.cpp:384-386), and the sticky error bits, which are cleared once
+// read so an error surfaces exactly once.  Every entry point that observes
+// core state calls this (directly or through sync) before reading; the
+// *_device calls never do, so device-path steps queue back to back.
 void settle(xbs_core* c) {
-  if (!c->upd_pending) return;
-  c->upd_pending = false;
-  ck(cudaEventSynchronize(c->upd_ev1), "kernel execution");
-  float ms = 0.f;
-  ck(cudaEventElapsedTime(&ms, c->upd_ev0, c->upd_ev1), "update timing");
-  c->conversion_seconds += 1e-3 * ms;
-  finish_update_stats(c);
+  if (!c->stats_pending) return;
+  c->stats_pending = false;
+  c->upd_async = false;
+  ck(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+  ck(cudaStreamSynchronize(c->stream), "kernel execution");
+  for (auto& e : c->upd_timing) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, e.first, e.second), "update timing");
+    c->conversion_seconds += 1e-3 * ms;
+    c->ev_pool.push_back(e.first);
+    c->ev_pool.push_back(e.second);
+  }
+  c->upd_timing.clear();
+  c->dwmax_seen = std::max(c->dwmax_seen, __builtin_bit_cast(double, c->h_sc->dwmax));
+  c->wmax_seen = std::max(c->wmax_seen, __builtin_bit_cast(double, c->h_sc->wmax));
+  const int err = c->h_sc->err_flag;
+  if (err || (c->tile_engine && c->h_sc->fcm_fail)) {
+    ck(cudaMemsetAsync(&c->d_sc->err_flag, 0, sizeof(int), c->stream), "memset");
+    ck(cudaMemsetAsync(&c->d_sc->fcm_fail, 0, sizeof(unsigned), c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "kernel execution");
+  }
+  if (err & 2) fail(XBS_INVALID_ARGUMENT, "scale_gradient: gradient must be finite");
+  if (err & 1) fail(XBS_INVALID_ARGUMENT, "nonlinear_update: g outside device range");
+  check_fcm(c);
 }
 
 void sync(xbs_core* c) {
@@ -264,30 +286,36 @@ void h2d_colmajor_to_rowmajor(xbs_core* c, const double* h, int64_t rows, int64_
   c->h_tmp.assign(size_t(rows * cols), 0.0);
   for (int64_t j = 0; j < cols; ++j)
     for (int64_t i = 0; i < rows; ++i) c->h_tmp[size_t(i * cols + j)] = h[j * ld + i];
-  ck(cudaMemcpy(d, c->h_tmp.data(), size_t(rows * cols) * 8, cudaMemcpyHostToDevice), "H2D");
+  // stream-ordered with the kernels that consume it (the core's stream is
+  // non-blocking, so a legacy-stream copy would not order against it)
+  ck(cudaMemcpyAsync(d, c->h_tmp.data(), size_t(rows * cols) * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaStreamSynchronize(c->stream), "H2D");  // h_tmp is reused by the next call
 }
 void d2h_rowmajor_to_colmajor(xbs_core* c, const double* d, int64_t rows, int64_t cols, double* h, int64_t ld) {
   c->h_tmp.resize(size_t(rows * cols));
-  ck(cudaMemcpy(c->h_tmp.data(), d, size_t(rows * cols) * 8, cudaMemcpyDeviceToHost), "D2H");
+  ck(cudaMemcpyAsync(c->h_tmp.data(), d, size_t(rows * cols) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "D2H");
   for (int64_t j = 0; j < cols; ++j)
     for (int64_t i = 0; i < rows; ++i) h[j * ld + i] = c->h_tmp[size_t(i * cols + j)];
 }
 
 // CUDA-event bracket around one stage (only while profiling is enabled).
+cudaEvent_t take_event(xbs_core* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
 struct StageScope {
   xbs_core* c;
   int stage;
   cudaEvent_t a = nullptr;
-  static cudaEvent_t take(xbs_core* c) {
-    if (!c->ev_pool.empty()) {
-      cudaEvent_t e = c->ev_pool.back();
-      c->ev_pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e;
-    ck(cudaEventCreate(&e), "cudaEventCreate");
-    return e;
-  }
+  static cudaEvent_t take(xbs_core* c) { return take_event(c); }
   StageScope(xbs_core* cc, int s) : c(cc), stage(s) {
     if (c->profile) {
       a = take(c);
@@ -355,7 +383,8 @@ void set_adc(xbs_core* c, int dir, double i_fs) {
     T[size_t(k)] = lo;
   }
   ck(cudaMalloc(&tab, T.size() * 8), "cudaMalloc adc table");
-  ck(cudaMemcpy(tab, T.data(), T.size() * 8, cudaMemcpyHostToDevice), "H2D adc table");
+  ck(cudaMemcpyAsync(tab, T.data(), T.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D adc table");
+  ck(cudaStreamSynchronize(c->stream), "H2D adc table");  // T is local
 }
 
 // layers.cpp:189-197: after adc_cal_batches training forwards, each
@@ -416,6 +445,7 @@ void enqueue_fwd_vmm(xbs_core* c, int64_t M, const Out& out) {
   if (c->fully_ideal) {
     xbs::launch_fwd_ideal(c, M, stage, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
+    if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;  // shape outside the tcgen05 kernel's exact bounds
     xbs::launch_fwd_simt(c, M, stage, c->stream);
   }
   finish_out(c, Out{out.p, ld, out.host}, M, c->g.N, direct);
@@ -428,6 +458,7 @@ void enqueue_bwd_vmm(xbs_core* c, const double* d_dy, int64_t M, const Out& out)
   if (c->fully_ideal) {
     xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
+    if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;
     xbs::launch_bwd_simt(c, M, stage, c->stream);
   }
   finish_out(c, Out{out.p, ld, out.host}, M, c->g.K, direct);
@@ -447,6 +478,7 @@ void run_graphed(xbs_core* c, xbs_core::GraphSlot& g, const uint64_t (&key)[8], 
   if (same && g.ready) {
     ck(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
     c->launches += g.kernels;
+    c->tc_fallbacks += g.fallbacks;
     return;
   }
   if (!same || !g.seen) {  // new key: run eagerly, capture on the next identical call
@@ -458,7 +490,7 @@ void run_graphed(xbs_core* c, xbs_core::GraphSlot& g, const uint64_t (&key)[8], 
     enqueue();
     return;
   }
-  const int64_t l0 = c->launches;
+  const int64_t l0 = c->launches, f0 = c->tc_fallbacks;
   ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
   cudaGraph_t graph = nullptr;
   try {
@@ -475,10 +507,13 @@ void run_graphed(xbs_core* c, xbs_core::GraphSlot& g, const uint64_t (&key)[8], 
   cudaGraphDestroy(graph);
   ck(e, "cudaGraphInstantiate");
   g.kernels = c->launches - l0;
+  g.fallbacks = c->tc_fallbacks - f0;
   c->launches = l0;
+  c->tc_fallbacks = f0;
   g.ready = true;
   ck(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
   c->launches += g.kernels;
+  c->tc_fallbacks += g.fallbacks;
 }
 
 bool graphable(const xbs_core* c, int64_t M) { return c->use_graphs && !c->profile && !c->adc_auto && M > 0; }
@@ -525,6 +560,16 @@ void forward_device(xbs_core* c, const double* d_x, int64_t M, bool training, Ou
   enqueue_fwd_vmm(c, M, out);
 }
 
+// dW (layers.cpp:304) with its finiteness flag: cleared, raised by the dW
+// kernels, and copied to the pinned host mirror so a host apply_updates can
+// refuse a non-finite gradient synchronously (update.cpp:18-19).
+void enqueue_dw(xbs_core* c, int64_t M, double gd) {
+  ck(cudaMemsetAsync(&c->d_sc->dw_nonfinite, 0, sizeof(int), c->stream), "memset");
+  if (c->kernel == 1 || !xbs::launch_dw_tc(c, M, gd, c->stream)) xbs::launch_dw(c, M, gd, c->stream);
+  ck(cudaMemcpyAsync(&c->h_sc->dw_nonfinite, &c->d_sc->dw_nonfinite, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+     "D2H flag");
+}
+
 void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out out) {
   if (!c->have_forward) fail(XBS_STATE_ERROR, "CrossbarCore::backward: no cached forward activations");
   if (M != c->M_fwd) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::backward: gradient shape mismatch");
@@ -534,7 +579,7 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out 
     run_graphed(c, c->gbwd, key, [&] {
       xbs::launch_prep_dy(c, d_dy, M, c->stream);
       c->launches += 3;
-      if (c->kernel == 1 || !xbs::launch_dw_tc(c, M, gd, c->stream)) xbs::launch_dw(c, M, gd, c->stream);
+      enqueue_dw(c, M, gd);
       c->launches += 2;
       enqueue_bwd_vmm(c, d_dy, M, out);
     });
@@ -548,7 +593,7 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out 
   }
   {
     StageScope st(c, XBS_STAGE_DW);
-    if (c->kernel == 1 || !xbs::launch_dw_tc(c, M, gd, c->stream)) xbs::launch_dw(c, M, gd, c->stream);
+    enqueue_dw(c, M, gd);
     c->launches += 1;
   }
   c->have_grad = true;
@@ -568,6 +613,8 @@ void backward_device(xbs_core* c, const double* d_dy, int64_t M, double gd, Out 
 
 void apply_updates_device(xbs_core* c, uint64_t iteration) {
   if (!c->have_grad) return;  // layers.cpp:383
+  // dwmax / wmax are running maxima on the device and err_flag is sticky:
+  // nothing is reset here, so device-path steps lose no statistic
   xbs::UpdP up{};
   up.v = c->opt.upd_v;
   up.gamma = c->opt.upd_gamma;
@@ -579,26 +626,23 @@ void apply_updates_device(xbs_core* c, uint64_t iteration) {
   up.seed = c->opt.upd_seed;
   up.iteration = iteration;
   up.linear = c->opt.upd_v == 0.0;
-  ck(cudaMemsetAsync(&c->d_sc->dwmax, 0, 2 * sizeof(unsigned long long), c->stream), "memset");
-  ck(cudaMemsetAsync(&c->d_sc->err_flag, 0, sizeof(int), c->stream), "memset");
-  StageScope st(c, XBS_STAGE_UPDATE);
-  xbs::launch_update(c, up, c->stream, c->tile_engine);  // tile engines: master only, then per-tile regeneration
-  ++c->update_count;                                     // layers.cpp:389
-  if (c->tile_engine) regenerate_tiles(c);
-  regenerate_bookkeeping(c);
+  cudaEvent_t e0 = take_event(c), e1 = take_event(c);
+  ck(cudaEventRecord(e0, c->stream), "event record");
+  {
+    StageScope st(c, XBS_STAGE_UPDATE);
+    xbs::launch_update(c, up, c->stream, c->tile_engine);  // tile engines: master only, then per-tile regeneration
+    ++c->update_count;                                     // layers.cpp:389
+    if (c->tile_engine) regenerate_tiles(c);
+    regenerate_bookkeeping(c);
+  }
+  ck(cudaEventRecord(e1, c->stream), "event record");
+  c->upd_timing.emplace_back(e0, e1);
+  c->stats_pending = true;
   c->launches += c->opt.engine == XBS_ENGINE_IDEAL ? 2 : 1;
   c->have_grad = false;
   c->have_forward = false;
 }
 
-void finish_update_stats(xbs_core* c) {
-  c->upd_pending = false;
-  ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
-  if (c->h_sc->err_flag) fail(XBS_INVALID_ARGUMENT, "nonlinear_update: g outside device range");
-  check_fcm(c);
-  c->dwmax_seen = std::max(c->dwmax_seen, __builtin_bit_cast(double, c->h_sc->dwmax));
-  c->wmax_seen = std::max(c->wmax_seen, __builtin_bit_cast(double, c->h_sc->wmax));
-}
 
 }  // namespace
 
@@ -816,7 +860,8 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     regenerate_all(c.get());
     regenerate_bookkeeping(c.get());
     sync(c.get());
-    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    ck(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "D2H scalars");
     check_fcm(c.get());
     c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     cudaFree(d_W);
@@ -832,8 +877,10 @@ void xbs_core_destroy(xbs_core* c) {
     cudaStreamDestroy(c->copy_stream);
   }
   if (c->copy_ev) cudaEventDestroy(c->copy_ev);
-  if (c->upd_ev0) cudaEventDestroy(c->upd_ev0);
-  if (c->upd_ev1) cudaEventDestroy(c->upd_ev1);
+  for (auto& e : c->upd_timing) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   cudaFree(c->d_digits);
   cudaFree(c->d_adc_tab);
   cudaFree(c->d_adc_tab_b);
@@ -878,7 +925,7 @@ int xbs_core_forward(xbs_core* c, const double* x, int64_t M, int64_t K, int64_t
     if (K != c->g.K) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: feature count mismatch");  // layers.cpp:216-217
     if (M < 0 || (M > 0 && (ldx < M || ldy < M || !x || !y))) fail(XBS_INVALID_ARGUMENT, "CrossbarCore::forward: bad buffers");
     ensure_io(c, std::max<int64_t>(1, M * std::max(c->g.K, c->g.N)));
-    if (M > 0 && c->upd_pending) {
+    if (M > 0 && c->upd_async) {
       // the pending update does not touch the staging buffer: copy x on the
       // side stream while it runs, and order the forward after both
       if (!c->copy_stream) {
@@ -931,31 +978,25 @@ int xbs_core_apply_updates(xbs_core* c, uint64_t iteration) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
     if (!c->have_grad) return;
-    settle(c);
+    sync(c);  // the dW producer is complete and the previous update folded
+    // scale_gradient (update.cpp:18-19): a non-finite gradient throws before
+    // anything changes (the dW kernels raised the flag, or set_gradient did)
+    if (c->h_sc->dw_nonfinite) fail(XBS_INVALID_ARGUMENT, "scale_gradient: gradient must be finite");
     // Engines whose update cannot raise (AAM / ideal regeneration, linear
-    // update: no range check, update.cpp:28-29, no FCM convergence) return
-    // before the kernels finish; the next call settles timing and statistics
-    // and a forward overlaps its input copy with them.  Others stay
-    // synchronous so their exceptions surface here, as in the reference.
+    // update: no range check, update.cpp:28-29, no FCM convergence; the
+    // gradient was checked above) return before the kernels finish; the next
+    // call settles timing and statistics and a forward overlaps its input
+    // copy with them.  Others stay synchronous so their exceptions surface
+    // here, as in the reference.
     const bool defer = (c->opt.engine == XBS_ENGINE_AAM || c->opt.engine == XBS_ENGINE_IDEAL) &&
                        c->opt.upd_v == 0.0 && !c->profile;
+    apply_updates_device(c, iteration);
+    ck(cudaGetLastError(), "kernel launch");
     if (defer) {
-      if (!c->upd_ev0) {
-        ck(cudaEventCreate(&c->upd_ev0), "cudaEventCreate");
-        ck(cudaEventCreate(&c->upd_ev1), "cudaEventCreate");
-      }
-      ck(cudaEventRecord(c->upd_ev0, c->stream), "event record");
-      apply_updates_device(c, iteration);
-      ck(cudaEventRecord(c->upd_ev1, c->stream), "event record");
-      ck(cudaGetLastError(), "kernel launch");
-      c->upd_pending = true;
+      c->upd_async = true;
       return;
     }
-    const auto t0 = std::chrono::steady_clock::now();
-    apply_updates_device(c, iteration);
     sync(c);
-    c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    finish_update_stats(c);
   });
 }
 
@@ -974,7 +1015,6 @@ int xbs_core_backward_device(xbs_core* c, const double* d_dy, int64_t M, double 
 int xbs_core_apply_updates_device(xbs_core* c, uint64_t iteration) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
-    settle(c);  // its statistics are read before this update resets them
     apply_updates_device(c, iteration);
   });
 }
@@ -982,7 +1022,6 @@ int xbs_core_synchronize(xbs_core* c) {
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
     sync(c);
-    finish_update_stats(c);
   });
 }
 
@@ -1008,6 +1047,7 @@ int xbs_core_get_info(xbs_core* c, xbs_core_info* info) {
     info->forward_adc_full_scale = c->adc_auto && c->adc_frozen ? c->adc.i_fs : c->opt.adc_i_fs;
     info->fully_ideal = c->fully_ideal ? 1 : 0;
     info->kernel = c->kernel;
+    info->tc_fallbacks = c->tc_fallbacks;
   });
 }
 
@@ -1024,6 +1064,12 @@ int xbs_core_set_gradient(xbs_core* c, const double* dW, int64_t ld) {
     if (!c || !dW || ld < c->g.K) fail(XBS_INVALID_ARGUMENT, "bad gradient buffer");
     sync(c);
     h2d_colmajor_to_rowmajor(c, dW, c->g.K, c->g.N, ld, c->d_dW);
+    bool finite = true;  // checked when the update runs (update.cpp:18-19), like a backward's dW
+    for (double v : c->h_tmp) finite = finite && std::isfinite(v);
+    c->h_sc->dw_nonfinite = finite ? 0 : 1;
+    ck(cudaMemcpyAsync(&c->d_sc->dw_nonfinite, &c->h_sc->dw_nonfinite, sizeof(int), cudaMemcpyHostToDevice, c->stream),
+       "H2D flag");
+    ck(cudaStreamSynchronize(c->stream), "H2D flag");
     c->have_grad = true;
   });
 }
@@ -1041,7 +1087,8 @@ int xbs_core_nonideal(xbs_core* c, int32_t s, int32_t p, int32_t t, double* out,
     xbs::launch_digits_to_g(c, s, p, t / c->g.GC, t % c->g.GC, d, c->stream);
     sync(c);
     std::vector<double> h(static_cast<size_t>(n));
-    ck(cudaMemcpy(h.data(), d, size_t(n) * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpyAsync(h.data(), d, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "D2H");
     cudaFree(d);
     for (int j = 0; j < c->g.tile_cols; ++j)
       for (int i = 0; i < c->g.tile_rows; ++i) out[int64_t(j) * ld + i] = h[size_t(j) * c->g.tile_rows + i];
@@ -1064,7 +1111,8 @@ int xbs_core_set_master(xbs_core* c, int32_t s, const double* u, int64_t ld) {
     regenerate_all(c);
     if (c->opt.engine == XBS_ENGINE_IDEAL) xbs::launch_implied(c, c->d_wimp, c->stream);
     sync(c);
-    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    ck(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "D2H scalars");
     check_fcm(c);
   });
 }
@@ -1085,7 +1133,8 @@ int xbs_core_adc_counters(xbs_core* c, int64_t* exact_path, int64_t* conversions
   return guard([&] {
     if (!c) fail(XBS_INVALID_ARGUMENT, "null core");
     sync(c);
-    ck(cudaMemcpy(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost), "D2H scalars");
+    ck(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(xbs::DevScalars), cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "D2H scalars");
     if (exact_path) *exact_path = int64_t(c->h_sc->exact_path);
     if (conversions) *conversions = int64_t(c->h_sc->conversions);
   });

@@ -43,7 +43,7 @@ struct DwArgs {
   int64_t Mcap8;
   double sx, lev_e, gd;
   double rgd;  // 1 / gd when gd is a power of two (then x / gd == x * rgd exactly), else 0
-  const DevScalars* sc;
+  DevScalars* sc;
   double* dW;
 };
 
@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const double se = a.sc->se;
     const double step_e = se > 0 ? se / a.lev_e : 0.0;
+    bool nonfinite = false;  // scale_gradient's finiteness check (update.cpp:18-19), raised at apply time
     uint32_t ab = 0, abph = 0;
     for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
       const int t = u % a.ntiles;
@@ -162,7 +163,9 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
               if (a.S64) {
                 if (S != 0) atomicAdd(&a.S64[int64_t(i0 + ii) * a.NA + j], (unsigned long long)(long long)S);
               } else {
-                a.dW[int64_t(i0 + ii) * a.N + j] = dw_value(S, a.sx, step_e, a.gd, a.rgd);
+                const double v = dw_value(S, a.sx, step_e, a.gd, a.rgd);
+                nonfinite |= !isfinite(v);
+                a.dW[int64_t(i0 + ii) * a.N + j] = v;
               }
             }
           }
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
       }
       if (++ab == 2) { ab = 0; abph ^= 1; }
     }
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&a.sc->dw_nonfinite, 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(dw::kThreads, 1)
 // Split mode: dW = ((S * sx) * step_e) / grad_divisor from the int64 sums,
 // then S64 is cleared for the next call.
 __global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, double gd, double rgd,
-                              const DevScalars* sc, unsigned long long* __restrict__ S64, double* __restrict__ dW) {
+                              DevScalars* sc, unsigned long long* __restrict__ S64, double* __restrict__ dW) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
   const int64_t n = int64_t(K) * N;
@@ -188,7 +192,9 @@ __global__ void k_dw_finalize(int K, int N, int NA, double sx, double lev_e, dou
     unsigned long long* p = &S64[int64_t(i) * NA + j];
     const long long S = (long long)*p;
     *p = 0ull;
-    dW[t] = dw_value(S, sx, step_e, gd, rgd);
+    const double v = dw_value(S, sx, step_e, gd, rgd);
+    if (!isfinite(v)) sc->dw_nonfinite = 1;
+    dW[t] = v;
   }
 }
 
@@ -220,7 +226,13 @@ bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) 
     const size_t bytes = size_t(c->KA) * c->NA * 8;
     if (c->S64_bytes < bytes) {
       cudaFree(c->d_S64);
-      if (cudaMalloc(&c->d_S64, bytes) != cudaSuccess) return false;
+      c->d_S64 = nullptr;
+      c->S64_bytes = 0;
+      if (cudaMalloc(&c->d_S64, bytes) != cudaSuccess) {
+        c->d_S64 = nullptr;
+        (void)cudaGetLastError();  // the SIMT dW runs instead; do not leave the error pending
+        return false;
+      }
       cudaMemsetAsync(c->d_S64, 0, bytes, st);
       c->S64_bytes = bytes;
       ++c->gen;

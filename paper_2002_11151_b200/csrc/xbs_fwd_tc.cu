@@ -427,7 +427,11 @@ int* acc32(xbs_core* c, size_t bytes, cudaStream_t st) {
     cudaFree(c->d_acc32);
     c->d_acc32 = nullptr;
     c->acc32_bytes = 0;
-    if (cudaMalloc(&c->d_acc32, bytes) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&c->d_acc32, bytes) != cudaSuccess) {
+      c->d_acc32 = nullptr;
+      (void)cudaGetLastError();
+      return nullptr;
+    }
     cudaMemsetAsync(c->d_acc32, 0, bytes, st);
     c->acc32_bytes = bytes;
     ++c->gen;

@@ -88,8 +88,9 @@ struct DevScalars {
   unsigned long long dwmax;  // bits of max|dW| (non-negative doubles order as u64)
   unsigned long long wmax;   // bits of max|implied W|
   unsigned long long wmax_in;// bits of max|W0| (layer scale)
-  int err_flag;              // 1: nonlinear_update range violation
-  int pad;
+  int err_flag;              // bit 0: nonlinear_update range violation, bit 1: update skipped on a
+                             // non-finite gradient; sticky until the host reads it
+  int dw_nonfinite;          // the last dW holds a non-finite value (update.cpp:18-19)
   unsigned long long exact_path, conversions;
   unsigned int fcm_fail;                 // FCM tiles without a fixed point in the last regeneration
   unsigned int pad2;
@@ -117,10 +118,15 @@ struct xbs_core {
   bool tile_engine = false;     // fcm / interp_fcm with parasitics: per-tile regeneration kernels
   uint64_t update_count = 0;    // layers.cpp:389 (interp refresh schedule)
   cudaStream_t stream = nullptr;
-  // deferred apply_updates (host API, engines that cannot raise from the
-  // update): completion and statistics are settled by the next call
-  bool upd_pending = false;
-  cudaEvent_t upd_ev0 = nullptr, upd_ev1 = nullptr;
+  // Update statistics are folded lazily: every apply_updates records an event
+  // pair around its kernels and marks the device scalars pending; the next
+  // observing call (synchronize, getters, a host call's final sync) reads
+  // them once: running |dW| / |W| maxima, sticky error bits (read and
+  // cleared), update time into conversion_seconds (layers.cpp:176-177).
+  bool stats_pending = false;
+  bool upd_async = false;  // host apply_updates returned before its kernels finished
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> upd_timing;
+  int64_t tc_fallbacks = 0;  // VMM calls whose tcgen05 kernel refused the shape (SIMT ran)
   cudaStream_t copy_stream = nullptr;  // host->device input copies overlapping a pending update
   cudaEvent_t copy_ev = nullptr;
   bool own_stream = true;  // false after xbs_core_set_stream(caller's stream)
@@ -198,6 +204,7 @@ struct xbs_core {
     bool seen = false, ready = false;
     cudaGraphExec_t exec = nullptr;
     int64_t kernels = 0;
+    int64_t fallbacks = 0;
   } gfwd, gbwd;
   std::vector<cudaEvent_t> ev_pool;
   struct Pending { int stage; cudaEvent_t a, b; };

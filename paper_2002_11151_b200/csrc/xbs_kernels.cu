@@ -269,6 +269,10 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
                                                 double* __restrict__ master, uint8_t* __restrict__ digits,
                                                 DevScalars* sc, const uint32_t* __restrict__ qmin) {
   constexpr int S = S_T;
+  if (sc->dw_nonfinite) {  // scale_gradient throws before touching the master (update.cpp:18-19)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) atomicOr(&sc->err_flag, 2);
+    return;
+  }
   const double range = rp.range;
   double wmax = 0.0, dwmax = 0.0;
   const int j0 = JPT * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
               const bool pos_active = ui > 0.0 || (ui == 0.0 && dg[jj] < 0.0);
               const double dev_arg = pos_active ? -dg[jj] : dg[jj];
               const double gg = rp.g_min + fabs(ui);
-              if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);  // update.cpp:28-29
+              if (gg < rp.g_min || gg > rp.g_max) atomicOr(&sc->err_flag, 1);  // update.cpp:28-29
               const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
               const double nl = dev_arg * exp(-up.v * x);
               du = pos_active ? -nl : nl;
@@ -396,6 +400,10 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
 __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, const double* __restrict__ dW,
                                                     double* __restrict__ master, uint8_t* __restrict__ digits,
                                                     DevScalars* sc) {
+  if (sc->dw_nonfinite) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicOr(&sc->err_flag, 2);
+    return;
+  }
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double wmax = 0.0, dwmax = 0.0;
   if (j < g.N) {
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, c
           const bool pos_active = ui > 0.0 || (ui == 0.0 && dg < 0.0);
           const double dev_arg = pos_active ? -dg : dg;
           const double gg = rp.g_min + fabs(ui);
-          if (gg < rp.g_min || gg > rp.g_max) atomicExch(&sc->err_flag, 1);
+          if (gg < rp.g_min || gg > rp.g_max) atomicOr(&sc->err_flag, 1);
           const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
           const double nl = dev_arg * exp(-up.v * x);
           du = pos_active ? -nl : nl;
@@ -871,7 +879,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
 // ---------------------------------------------------------------------- dW
 // Exact integer outer product: dW = ((S * sx) * step_e) / gd.
 __global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const uint16_t* __restrict__ xc,
-                     const int16_t* __restrict__ ec, const DevScalars* __restrict__ sc, double* __restrict__ dW) {
+                     const int16_t* __restrict__ ec, DevScalars* __restrict__ sc, double* __restrict__ dW) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
   const int64_t n = int64_t(g.K) * g.N;
@@ -879,7 +887,9 @@ __global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const
     const int i = int(t / g.N), j = int(t % g.N);
     int64_t S = 0;
     for (int64_t b = 0; b < M; ++b) S += int64_t(xc[b * g.K + i]) * int64_t(ec[b * g.N + j]);
-    dW[t] = ((double(S) * sx) * step_e) / gd;
+    const double v = ((double(S) * sx) * step_e) / gd;
+    if (!isfinite(v)) sc->dw_nonfinite = 1;
+    dW[t] = v;
   }
 }
 

@@ -217,6 +217,7 @@ class CoreInfo(ctypes.Structure):
         ("refresh_count", ctypes.c_int64), ("conversion_seconds", ctypes.c_double),
         ("weight_abs_max_seen", ctypes.c_double), ("grad_abs_max_seen", ctypes.c_double),
         ("forward_adc_full_scale", ctypes.c_double), ("fully_ideal", ctypes.c_int32), ("kernel", ctypes.c_int32),
+        ("tc_fallbacks", ctypes.c_int64),
     ]
 
 

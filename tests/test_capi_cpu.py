@@ -30,7 +30,7 @@ def test_header_and_library_agree(lib):
 
 
 def test_abi_version(lib):
-    assert lib.xbs_abi_version() == 2
+    assert lib.xbs_abi_version() == 3
 
 
 def test_options_init_matches_reference_defaults(lib):
