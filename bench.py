@@ -40,7 +40,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2-4096")
+    p.add_argument("--config", default="c5", help="headline workload (default C5, the largest single-GPU config)")
+    p.add_argument("--no-others", action="store_true", help="skip the per-config summaries of C1-C4")
+    p.add_argument("--stage-probe", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-peak", action="store_true", help="skip the live int8 peak GEMM (ncu launch lists)")
@@ -167,7 +169,7 @@ def measure_int8_peak():
 
 
 # ----------------------------------------------------------- CPU baseline
-def cpu_sample(cfg, n_feat=256, steps=1, idx=0):
+def cpu_sample(cfg, n_feat=256, steps=1, idx=0, rows=None):
     """The oracle (restated reference CPU path, 1 thread: the reference's
     forward/backward/update are serial, layers.hpp:34) on a bounded sample of
     the same workload: a K=N=n_feat slice of the layer (same tile geometry,
@@ -178,7 +180,8 @@ def cpu_sample(cfg, n_feat=256, steps=1, idx=0):
 
     layer = cfg.layers[0]
     n_feat = min(n_feat, layer.K, layer.N)
-    sl = Layer("sample", layer.M, n_feat, n_feat)
+    M = min(layer.M, rows or layer.M)
+    sl = Layer("sample", M, n_feat, n_feat)
     opt = cfg.options()
     W, x, dy = cfg.weights(sl, idx), cfg.inputs(sl, idx), cfg.errors(sl, idx)
     orc = oracle_py.OracleCore(W, opt, snapped=True)
@@ -189,7 +192,7 @@ def cpu_sample(cfg, n_feat=256, steps=1, idx=0):
         orc.apply_updates(it)
     dt = (time.perf_counter() - t0) / steps
     macs = cfg.macs(sl)["total"]
-    desc = (f"oracle fwd+bwd+update of a K=N={n_feat} slice of {cfg.name} (M={layer.M}, "
+    desc = (f"oracle fwd+bwd+update of a K=N={n_feat} slice of {cfg.name} ({M} of {layer.M} batch rows, "
             f"{(n_feat // cfg.tile) ** 2} of {((layer.K + cfg.tile - 1) // cfg.tile) * ((layer.N + cfg.tile - 1) // cfg.tile)}"
             f" crossbar tiles), {dt:.2f} s/step, MACs/s scale linearly in tile count")
     return macs / dt, dt, desc
@@ -199,16 +202,19 @@ def _ref_worker(a):
     from paper_2002_11151_b200.configs import CONFIGS
 
     name, idx = a
-    v, dt, desc = cpu_sample(CONFIGS[name], 256, 1, idx)
+    cfg = CONFIGS[name]
+    # bounded step: one crossbar tile's worth of the layer, at most 128 batch rows
+    v, dt, desc = cpu_sample(cfg, cfg.tile, 1, idx, rows=128)
     return v * dt, desc  # MACs done, description
 
 
 def run_reference(args, cfg):
     """The reference algorithm's CPU implementation on all host cores.  The
     reference's VMM loop is serial per core (threads only split regeneration,
-    layers.hpp:34), so the whole-host rate is one independent K=N=256 tile
-    slice of the workload per core, run concurrently: value = sum of MACs /
-    wall time of the step.  Under torchrun only rank 0 runs."""
+    layers.hpp:34), so the whole-host rate is one independent one-tile slice
+    of the workload (K = N = tile, <= 128 batch rows) per core, run
+    concurrently: value = sum of MACs / wall time of the step.  Under
+    torchrun only rank 0 runs."""
     import multiprocessing as mp
 
     rank, _, world = dist_env()
@@ -397,6 +403,204 @@ def run_calibrate(args, cfg):
             "timing": "host wall clock around synchronised steps"}))
 
 
+MMA_SPEC_TOPS = 4500.0  # NVIDIA dense int8 spec (B200)
+OTHER_CONFIGS = ("c1", "c2-4096", "c3", "c4")
+
+
+def stage_work(cfg, layers, S):
+    """Algorithmic work per step of each stage."""
+    macs = {}
+    for L in layers:
+        for k, v in cfg.macs(L).items():
+            macs[k] = macs.get(k, 0) + v
+    return macs, {
+        "fwd_vmm": ("tensor", 2 * L_LIMBS * macs["fwd"] / 1e12, "TFLOP/s"),
+        "bwd_vmm": ("tensor", 2 * L_LIMBS * macs["bwd"] / 1e12, "TFLOP/s"),
+        # dW: an M-deep outer product whose cost is writing K x N fp64 and
+        # reading the u8 codes -- HBM-bound
+        "dw": ("hbm", sum(8 * L.K * L.N + L.M * (L.K + 2 * L.N) for L in layers) / 1e9, "GB/s"),
+        "update": ("hbm", sum(L.K * L.N * (24 * S + 8) for L in layers) / 1e9, "GB/s"),
+        # input / error quantisation + bit-plane emission: read fp64, write
+        # codes and the two u8 plane copies (x: T_in planes; dy: 2 T_err)
+        "prep_x": ("hbm", sum(L.M * L.K * (8 + 2 + 1 + 2 * 8) for L in layers) / 1e9, "GB/s"),
+        "prep_dy": ("hbm", sum(L.M * L.N * (8 + 2 + 2 + 4 * 8) for L in layers) / 1e9, "GB/s"),
+    }
+
+
+def measure(args, cfg, layers, world, local_rank, steps, warmup, e2e=True, profile=True, engine=None):
+    """One core per layer on one stream; W warm-up steps, K device-resident
+    steps timed with CUDA events on the cores' stream (graph replays), then
+    K profiled steps for per-stage times, then (e2e) K steps through the
+    host-pointer C ABI with pinned buffers.  Returns a dict of raw numbers."""
+    import torch
+    from paper_2002_11151_b200 import xbarsim as xb
+
+    opt = cfg.options()
+    if engine:
+        opt.engine = getattr(xb.EngineKind, engine)
+    cores, host, dev = [], [], []
+    for li, layer in enumerate(layers):
+        W, x, dy = cfg.weights(layer, li), cfg.inputs(layer, li), cfg.errors(layer, li)
+        cores.append(xb.CrossbarCore(W, opt))
+        host.append((x, dy) if e2e else None)
+        # device-resident operands, column-major (Eigen layout): (K, M) C-order == M x K col-major
+        dev.append((torch.from_numpy(np.ascontiguousarray(x.T)).cuda(),
+                    torch.from_numpy(np.ascontiguousarray(dy.T)).cuda(),
+                    torch.empty((layer.N, layer.M), dtype=torch.float64, device="cuda"),
+                    torch.empty((layer.K, layer.M), dtype=torch.float64, device="cuda")))
+        del W, x, dy
+    for c in cores[1:]:
+        c.set_stream(cores[0].stream())  # one stream for the whole network
+    stream = torch.cuda.ExternalStream(cores[0].stream())
+    torch.cuda.synchronize()
+    it = [0]
+
+    def step():
+        for c, layer, (d_x, d_dy, d_y, d_dx) in zip(cores, layers, dev):
+            c.forward_device(d_x.data_ptr(), layer.M, True, d_y.data_ptr())
+        for c, layer, (d_x, d_dy, d_y, d_dx) in reversed(list(zip(cores, layers, dev))):
+            c.backward_device(d_dy.data_ptr(), layer.M, 1.0, d_dx.data_ptr())
+        for c in cores:
+            c.apply_updates_device(it[0])
+        it[0] += 1
+
+    for _ in range(warmup):
+        step()
+    for c in cores:
+        c.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    out = {}
+    launches0 = sum(c.launch_count() for c in cores)
+    fb0 = sum(int(c.info().tc_fallbacks) for c in cores)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    for c in cores:
+        c.synchronize()
+    torch.cuda.synchronize()
+    out["ms"] = max_over_ranks(e0.elapsed_time(e1) / steps, world, "cuda")
+    out["launches"] = sum(c.launch_count() for c in cores) - launches0
+    out["fallbacks"] = sum(int(c.info().tc_fallbacks) for c in cores) - fb0
+    # per-stage kernel times: the same K steps again with CUDA events around
+    # every stage (eager launches; the timed steps above replay the cores'
+    # captured graphs, which per-stage events would split)
+    stages = {}
+    if profile:
+        for c in cores:
+            c.profile(True)
+        for _ in range(steps):
+            step()
+        for c in cores:
+            c.synchronize()
+        for c in cores:
+            for k, (t, n) in c.stage_times().items():
+                t0, n0 = stages.get(k, (0.0, 0))
+                stages[k] = (t0 + t, n0 + n)
+            c.profile(False)
+    out["stages_ms"] = {k: (v[0] / v[1] * len(layers) if v[1] else 0.0) for k, v in stages.items()}
+    barrier(world)
+    if e2e:
+        def pinned(rows, cols):  # F-ordered (rows x cols) numpy view of pinned memory
+            return torch.empty((cols, rows), dtype=torch.float64, pin_memory=True).numpy().T
+
+        hbuf = []
+        for layer, (x, dy) in zip(layers, host):
+            hx, hdy, hy, hdx = pinned(layer.M, layer.K), pinned(layer.M, layer.N), pinned(layer.M, layer.N), pinned(
+                layer.M, layer.K)
+            hx[:] = x
+            hdy[:] = dy
+            hbuf.append((hx, hdy, hy, hdx))
+        host.clear()
+
+        def host_step():
+            for c, (hx, hdy, hy, hdx) in zip(cores, hbuf):
+                c.forward(hx, True, out=hy)
+            for c, (hx, hdy, hy, hdx) in reversed(list(zip(cores, hbuf))):
+                c.backward(hdy, 1.0, out=hdx)
+            for c in cores:
+                c.apply_updates(it[0])
+            it[0] += 1
+
+        for _ in range(max(3, warmup)):
+            host_step()
+        for c in cores:
+            c.synchronize()
+        barrier(world)
+        # the host calls are synchronous; events on the (shared) stream
+        # bracket every H2D copy, kernel and D2H copy of the K steps
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        f0.record(stream)
+        for _ in range(steps):
+            host_step()
+        f1.record(stream)
+        f1.synchronize()
+        wall_s = (time.perf_counter() - t0) / steps
+        bi = sum(8 * L.M * (L.K + L.N) for L in layers)
+        out["e2e"] = {"h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi,
+                      "s": max_over_ranks(f0.elapsed_time(f1) * 1e-3 / steps, world, "cuda"),
+                      "wall_s": max_over_ranks(wall_s, world, "cuda")}
+        out["fallbacks"] += sum(int(c.info().tc_fallbacks) for c in cores) - fb0 - out["fallbacks"]
+    for c in cores[1:]:  # the first core owns the shared stream: detach before teardown
+        c.set_stream(None)
+    torch.cuda.synchronize()
+    del cores, dev
+    torch.cuda.empty_cache()
+    return out
+
+
+def rooflines(cfg, layers, stages_ms, peak_tops, hbm, mma_only=None):
+    S = cfg.weight_bits // cfg.device_bits
+    macs, work = stage_work(cfg, layers, S)
+    conv = {}
+    for L in layers:
+        for k, v in cfg.adc_conversions(L).items():
+            conv[k] = conv.get(k, 0) + v
+    roof = {}
+    for st, (bound, amount, unit) in work.items():
+        ms = stages_ms.get(st)
+        if not ms:
+            continue
+        ach = amount / (ms * 1e-3)
+        pk = peak_tops if bound == "tensor" else hbm
+        roof[st] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk, "ms": ms}
+        if st in ("fwd_vmm", "bwd_vmm"):
+            # the ADC epilogue's work: conversions/s and MACs per conversion
+            # (the tensor fraction of a narrow layer is capped by the latter)
+            n = conv[st[:3]]
+            roof[st].update({"adc_conversions": n, "adc_conv_per_s": n / (ms * 1e-3),
+                             "macs_per_conversion": macs[st[:3]] / n,
+                             "frac_vs_spec": ach / MMA_SPEC_TOPS})
+            if mma_only and mma_only.get(st):
+                mo = amount / (mma_only[st] * 1e-3)
+                roof[st].update({"mma_only_rate": mo, "frac_vs_mma_only": ach / mo})
+    return macs, roof
+
+
+def mma_only_probe(args, cfg_name):
+    """Per-stage VMM times of this workload with the ADC epilogue stubbed out
+    (the XBS_STUB_EPI build, _lib_stubepi/: MMAs, TMA operand loads, TMEM
+    loads and barriers, no conversions) -- the rate this kernel design reaches
+    without the epilogue.  Runs in a child process (the library is loaded per
+    process); None when the stub build is absent."""
+    lib = os.path.join(ROOT, "paper_2002_11151_b200", "_lib_stubepi", "libxbarsim_b200.so")
+    if not os.path.exists(lib):
+        return None
+    env = dict(os.environ, XBS_LIB_PATH=lib)
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--config", cfg_name, "--stage-probe",
+                        "--steps", "3", "--warmup", "2"], env=env, capture_output=True, text=True, timeout=900)
+    try:
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 def main():
     args = parse()
     from paper_2002_11151_b200.configs import CONFIGS
@@ -416,166 +620,33 @@ def main():
 
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
+    if args.stage_probe:  # child of mma_only_probe: stage times only
+        layers = list(cfg.layers)
+        r = measure(args, cfg, layers, 1, local_rank, args.steps, args.warmup, e2e=False)
+        print(json.dumps(r["stages_ms"]))
+        return
     init_dist(world, local_rank, "nccl")
-    from paper_2002_11151_b200 import xbarsim as xb
 
-    layers = list(cfg.layers) if args.all_layers else [cfg.layers[args.layer]]
-    opt = cfg.options()
-    if args.engine:
-        opt.engine = getattr(xb.EngineKind, args.engine)
-    cores, host, dev = [], [], []
-    for li, layer in enumerate(layers):
-        W, x, dy = cfg.weights(layer, li), cfg.inputs(layer, li), cfg.errors(layer, li)
-        cores.append(xb.CrossbarCore(W, opt))
-        host.append((x, dy))
-        # device-resident operands, column-major (Eigen layout): (K, M) C-order == M x K col-major
-        dev.append((torch.from_numpy(np.ascontiguousarray(x.T)).cuda(),
-                    torch.from_numpy(np.ascontiguousarray(dy.T)).cuda(),
-                    torch.empty((layer.N, layer.M), dtype=torch.float64, device="cuda"),
-                    torch.empty((layer.K, layer.M), dtype=torch.float64, device="cuda")))
-    for c in cores[1:]:
-        c.set_stream(cores[0].stream())  # one stream for the whole network
-    stream = torch.cuda.ExternalStream(cores[0].stream())
-    torch.cuda.synchronize()
-
-    it = [0]
-
-    def step():
-        for c, layer, (d_x, d_dy, d_y, d_dx) in zip(cores, layers, dev):
-            c.forward_device(d_x.data_ptr(), layer.M, True, d_y.data_ptr())
-        for c, layer, (d_x, d_dy, d_y, d_dx) in reversed(list(zip(cores, layers, dev))):
-            c.backward_device(d_dy.data_ptr(), layer.M, 1.0, d_dx.data_ptr())
-        for c in cores:
-            c.apply_updates_device(it[0])
-        it[0] += 1
-
-    for _ in range(args.warmup):
-        step()
-    for c in cores:
-        c.synchronize()
-    torch.cuda.synchronize()
-    barrier(world)
+    layers = list(cfg.layers) if (args.all_layers or len(cfg.layers) == 1) else [cfg.layers[args.layer]]
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    launches0 = sum(c.launch_count() for c in cores)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    e1.synchronize()
-    for c in cores:
-        c.synchronize()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    launches = sum(c.launch_count() for c in cores) - launches0
-    fallbacks = sum(int(c.info().tc_fallbacks) for c in cores)
-    if fallbacks:  # a VMM left the tcgen05 kernels (exact SIMT ran): not a valid tensor-core measurement
-        print(json.dumps({"error": f"{fallbacks} tcgen05->SIMT VMM fallbacks during the bench", "config": cfg.name}),
-              file=sys.stderr)
-        sys.exit(3)
-    # per-stage kernel times: the same K steps again with CUDA events around
-    # every stage (eager launches; the timed steps above replay the cores'
-    # captured graphs, which per-stage events would split)
-    for c in cores:
-        c.profile(True)
-    for _ in range(args.steps):
-        step()
-    for c in cores:
-        c.synchronize()
-    stages = {}
-    for c in cores:
-        for k, (t, n) in c.stage_times().items():
-            t0, n0 = stages.get(k, (0.0, 0))
-            stages[k] = (t0 + t, n0 + n)
-        c.profile(False)
-    barrier(world)
-    ms = max_over_ranks(ms, world, "cuda")
-
-    # e2e through the host-pointer C ABI with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        def pinned(rows, cols):  # F-ordered (rows x cols) numpy view of pinned memory
-            return torch.empty((cols, rows), dtype=torch.float64, pin_memory=True).numpy().T
-
-        hbuf = []
-        for layer, (x, dy) in zip(layers, host):
-            hx, hdy, hy, hdx = pinned(layer.M, layer.K), pinned(layer.M, layer.N), pinned(layer.M, layer.N), pinned(
-                layer.M, layer.K)
-            hx[:] = x
-            hdy[:] = dy
-            hbuf.append((hx, hdy, hy, hdx))
-
-        def host_step():
-            for c, (hx, hdy, hy, hdx) in zip(cores, hbuf):
-                c.forward(hx, True, out=hy)
-            for c, (hx, hdy, hy, hdx) in reversed(list(zip(cores, hbuf))):
-                c.backward(hdy, 1.0, out=hdx)
-            for c in cores:
-                c.apply_updates(it[0])
-            it[0] += 1
-
-        for _ in range(max(3, args.warmup)):
-            host_step()
-        for c in cores:
-            c.synchronize()
-        barrier(world)
-        # the host calls are synchronous; events on the (shared) stream
-        # bracket every H2D copy, kernel and D2H copy of the K steps
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        f0.record(stream)
-        for _ in range(args.steps):
-            host_step()
-        f1.record(stream)
-        f1.synchronize()
-        wall_s = (time.perf_counter() - t0) / args.steps
-        e2e_s = max_over_ranks(f0.elapsed_time(f1) * 1e-3 / args.steps, world, "cuda")
-        bi = sum(8 * L.M * (L.K + L.N) for L in layers)
-        e2e = {"h2d_bytes_per_step": bi, "d2h_bytes_per_step": bi, "s": e2e_s,
-               "wall_s": max_over_ranks(wall_s, world, "cuda")}
+    r = measure(args, cfg, layers, world, local_rank, args.steps, args.warmup, e2e=not args.no_e2e,
+                engine=args.engine)
     clk = clocks.stop()
+    if r["fallbacks"]:  # a VMM left the tcgen05 kernels (exact SIMT ran): not a tensor-core measurement
+        print(json.dumps({"error": f"{r['fallbacks']} tcgen05->SIMT VMM fallbacks during the bench",
+                          "config": cfg.name}), file=sys.stderr)
+        sys.exit(3)
 
-    macs = {}
-    for L in layers:
-        for k, v in cfg.macs(L).items():
-            macs[k] = macs.get(k, 0) + v
     S = cfg.weight_bits // cfg.device_bits
-    peak_tops, peak_src = (4500.0, "NVIDIA dense int8 spec (--no-peak)") if args.no_peak else measure_int8_peak()
+    peak_tops, peak_src = (MMA_SPEC_TOPS, "NVIDIA dense int8 spec (--no-peak)") if args.no_peak else measure_int8_peak()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    per = {k: (v[0] / v[1] * len(layers) if v[1] else 0.0) for k, v in stages.items()}  # ms per step
-    work = {  # algorithmic work per step of each stage
-        "fwd_vmm": ("tensor", 2 * L_LIMBS * macs["fwd"] / 1e12, "TFLOP/s"),
-        "bwd_vmm": ("tensor", 2 * L_LIMBS * macs["bwd"] / 1e12, "TFLOP/s"),
-        # dW: an M-deep outer product whose cost is writing K x N fp64 and
-        # reading the u8 codes -- HBM-bound
-        "dw": ("hbm", sum(8 * L.K * L.N + L.M * (L.K + 2 * L.N) for L in layers) / 1e9, "GB/s"),
-        "update": ("hbm", sum(L.K * L.N * (24 * S + 8) for L in layers) / 1e9, "GB/s"),
-        # input / error quantisation + bit-plane emission: read fp64, write
-        # codes and the two u8 plane copies (x: T_in planes; dy: 2 T_err)
-        "prep_x": ("hbm", sum(L.M * L.K * (8 + 2 + 1 + 2 * 8) for L in layers) / 1e9, "GB/s"),
-        "prep_dy": ("hbm", sum(L.M * L.N * (8 + 2 + 2 + 4 * 8) for L in layers) / 1e9, "GB/s"),
-    }
-    conv = {}
-    for L in layers:
-        for k, v in cfg.adc_conversions(L).items():
-            conv[k] = conv.get(k, 0) + v
-    roof_all = {}
-    for st, (bound, amount, unit) in work.items():
-        if per.get(st):
-            ach = amount / (per[st] * 1e-3)
-            pk = peak_tops if bound == "tensor" else hbm
-            roof_all[st] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk,
-                            "ms": per[st]}
-            if st in ("fwd_vmm", "bwd_vmm"):
-                # the ADC epilogue's work: conversions/s and MACs per conversion
-                # (the tensor fraction of a narrow layer is capped by the latter)
-                n = conv[st[:3]]
-                roof_all[st].update({"adc_conversions": n, "adc_conv_per_s": n / (per[st] * 1e-3),
-                                     "macs_per_conversion": macs[st[:3]] / n})
+    mma_only = None if (args.no_peak or world > 1) else mma_only_probe(args, args.config)
+    macs, roof_all = rooflines(cfg, layers, r["stages_ms"], peak_tops, hbm, mma_only)
+    per = r["stages_ms"]
     dominant = max(("fwd_vmm", "bwd_vmm", "update", "dw", "prep_x", "prep_dy"), key=lambda s: per.get(s, 0.0))
     traffic = None
     tpath = args.traffic or os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
@@ -585,6 +656,7 @@ def main():
     roof.update({"kernel": dominant, "traffic": traffic,
                  "peak_source": peak_src if roof.get("bound") == "tensor" else "MEASURED_PEAKS.json hbm_gbs"})
 
+    ms = r["ms"]
     value = world * macs["total"] / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": world, "steps": args.steps,
@@ -600,25 +672,46 @@ def main():
         "roofline": roof,
         "roofline_stages": roof_all,
         "int8_peak_tops": peak_tops,
+        "int8_peak_denominators": {"live_int_mm": peak_tops, "spec": MMA_SPEC_TOPS,
+                                   "mma_only_stub_ms": mma_only},
         "macs_per_step": macs,
-        "gpu_launches": launches,
-        "tc_fallbacks": fallbacks,
+        "gpu_launches": r["launches"],
+        "tc_fallbacks": r["fallbacks"],
         "clocks": clk,
     }
-    if e2e:
-        line["e2e"] = {"value": world * macs["total"] / e2e["s"], "unit": "MAC/s",
-                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
-                       "ms_per_step": e2e["s"] * 1e3, "wall_ms_per_step": e2e["wall_s"] * 1e3,
+    if "e2e" in r:
+        e = r["e2e"]
+        line["e2e"] = {"value": world * macs["total"] / e["s"], "unit": "MAC/s",
+                       "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
+                       "ms_per_step": e["s"] * 1e3, "wall_ms_per_step": e["wall_s"] * 1e3,
                        "path": "xbs_core_forward/backward/apply_updates (host pointers, pinned)"}
+    fl = os.path.join(ROOT, "profiles", "r02", "adc_flips.json")
+    if os.path.exists(fl):
+        f = json.load(open(fl))
+        line["parity"] = {"gpu_vs_snapped_oracle": "bit-exact y, dx, dW (tests/test_parity*_gpu.py, "
+                                                   "tests/test_adc_flips_gpu.py)",
+                          "adc_flips_vs_literal": {"total": f["total"], "max_abs_code_delta": f["max_abs_code_delta"],
+                                                   "source": "profiles/r02/adc_flips.json (tools/flip_report.py)"}}
+    if not args.no_others:
+        others = {}
+        for name in OTHER_CONFIGS:
+            if name == args.config:
+                continue
+            oc = CONFIGS[name]
+            ol = list(oc.layers)
+            o = measure(args, oc, ol, world, local_rank, min(args.steps, 10), max(3, min(args.warmup, 5)), e2e=False)
+            om, orf = rooflines(oc, ol, o["stages_ms"], peak_tops, hbm)
+            others[oc.name] = {"value": world * om["total"] / (o["ms"] * 1e-3), "unit": "MAC/s", "ms_per_step": o["ms"],
+                               "layers": len(ol), "tc_fallbacks": o["fallbacks"],
+                               "frac": {k: round(v["frac"], 4) for k, v in orf.items()},
+                               "stage_ms": {k: round(v, 4) for k, v in o["stages_ms"].items()}}
+        line["other_configs"] = others
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = cpu_sample(cfg, 512, 3)
+        v, dt, desc = cpu_sample(cfg, 256, 2, rows=512)
         line["cpu_baseline"] = {"value": v, "unit": "MAC/s", "cores": 1, "kind": "port",
-                                "sample": desc + f"; 3 steps, {3 * dt:.1f} s of CPU work"}
+                                "sample": desc + f"; 2 steps, {2 * dt:.1f} s of CPU work"}
     if rank == 0:
-        print(json.dumps(line))
-    for c in cores[1:]:  # the first core owns the shared stream: detach before teardown
-        c.set_stream(None)
-    torch.cuda.synchronize()
+        print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 

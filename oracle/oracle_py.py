@@ -34,6 +34,8 @@ def lib():
         L.orc_last_error.restype = ctypes.c_char_p
         L.orc_core_create.argtypes = [ctypes.c_void_p, ctypes.c_int, _D, ctypes.c_long, ctypes.c_long,
                                       ctypes.POINTER(ctypes.c_void_p)]
+        L.orc_core_create_tiles.argtypes = [ctypes.c_void_p, ctypes.c_int, _D, ctypes.c_long, ctypes.c_long,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
         L.orc_core_destroy.argtypes = [ctypes.c_void_p]
         L.orc_core_forward.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_long, ctypes.c_int, _D]
         L.orc_core_forward_tiles.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_long, ctypes.c_int,
@@ -94,12 +96,20 @@ def _p(a):
 class OracleCore:
     """CPU restatement of CrossbarCore; snapped=True is the GPU's exactness contract."""
 
-    def __init__(self, W0, opt, snapped: bool = True):
+    def __init__(self, W0, opt, snapped: bool = True, tiles=None):
+        """tiles: convert only these tiles (tr * grid_cols + tc) -- sampled
+        parity on layers too large to convert whole; forward_tiles /
+        backward_tiles must then stay inside them."""
         W = _f(W0)
         self._copt = opt.to_c()
         h = ctypes.c_void_p()
-        _check(lib().orc_core_create(ctypes.byref(self._copt), int(snapped), _p(W), W.shape[0], W.shape[1],
-                                     ctypes.byref(h)))
+        if tiles is None:
+            _check(lib().orc_core_create(ctypes.byref(self._copt), int(snapped), _p(W), W.shape[0], W.shape[1],
+                                         ctypes.byref(h)))
+        else:
+            arr = (ctypes.c_int * max(1, len(tiles)))(*tiles)
+            _check(lib().orc_core_create_tiles(ctypes.byref(self._copt), int(snapped), _p(W), W.shape[0], W.shape[1],
+                                               arr, len(tiles), ctypes.byref(h)))
         self._h = h
         self.K, self.N = W.shape
         self.opt = opt

@@ -444,8 +444,9 @@ static Matrix plane_volts(const IMatrix& codes, int k, int sb, const std::vector
 }
 
 // layers.cpp:68-83
-CrossbarCore::CrossbarCore(const Matrix& W0, const CrossbarLayerOptions& opt)
+CrossbarCore::CrossbarCore(const Matrix& W0, const CrossbarLayerOptions& opt, const std::vector<int>* tiles)
     : opt_(opt), weights_(map_weights(W0, opt.map, opt.crossbar)) {
+  if (tiles) regen_tiles = *tiles;  // sampled parity runs convert only these tiles
   opt_.validate();
   adc_fwd_ = opt_.adc;
   adc_bwd_ = opt_.adc;

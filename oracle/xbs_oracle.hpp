@@ -289,7 +289,9 @@ struct CrossbarLayerOptions {  // layers.hpp:19-37
 
 class CrossbarCore {  // layers.hpp:49-111
  public:
-  CrossbarCore(const Matrix& W0, const CrossbarLayerOptions& opt);
+  // tiles: convert only these tiles (tr * grid_cols + tc) at construction and
+  // at every regeneration (sampled parity runs on layers too large to convert)
+  CrossbarCore(const Matrix& W0, const CrossbarLayerOptions& opt, const std::vector<int>* tiles = nullptr);
   Matrix forward(const Matrix& x, bool training);
   Matrix backward(const Matrix& dy, double grad_divisor);
   void apply_updates(uint64_t iteration);

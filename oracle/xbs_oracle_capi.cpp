@@ -127,6 +127,15 @@ const char* orc_last_error() { return g_err.c_str(); }
 int orc_core_create(const orc_options* o, int snapped, const double* W, long K, long N, void** out) {
   return guard([&] { *out = new orc::CrossbarCore(wrap(W, K, N), to_opts(o, snapped)); });
 }
+// Sampled construction: only `tiles` are converted (now and at every
+// regeneration); forward_tiles / backward_tiles must stay inside them.
+int orc_core_create_tiles(const orc_options* o, int snapped, const double* W, long K, long N, const int* tiles, int n,
+                          void** out) {
+  return guard([&] {
+    const std::vector<int> t(tiles, tiles + n);
+    *out = new orc::CrossbarCore(wrap(W, K, N), to_opts(o, snapped), &t);
+  });
+}
 void orc_core_destroy(void* h) { delete static_cast<orc::CrossbarCore*>(h); }
 
 // CrossbarConv2d (layers.cpp:415-505); x: batch x (c*h*w) column-major
