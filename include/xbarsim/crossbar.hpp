@@ -19,3 +19,15 @@ struct CrossbarConfig {
 };
 
 }  // namespace xbarsim::circuit
+
+#include "xbarsim/matrix.hpp"
+
+namespace xbarsim::circuit {
+
+/// reference crossbar.hpp:46-61: a tile's geometry and conductances (g(i, j)).
+struct ConductanceTile {
+  CrossbarConfig config;
+  MatrixXd g;
+};
+
+}  // namespace xbarsim::circuit

@@ -17,6 +17,7 @@
 #include "xbarsim/crossbar.hpp"
 #include "xbarsim/engine.hpp"
 #include "xbarsim/mapping.hpp"
+#include "xbarsim/rng.hpp"
 #include "xbarsim/status.hpp"
 #include "xbarsim/tensor.hpp"
 #include "xbarsim/update.hpp"
@@ -39,6 +40,12 @@ struct CrossbarLayerOptions {
   int error_bits = 8;
   int adc_cal_batches = 20;
   int threads = 1;
+
+  /// layers.cpp:17-47 (the reference's checks and exception classes)
+  void validate() const {
+    const xbs_layer_options o = to_c();
+    detail::check(xbs_options_validate(&o));
+  }
 
   /// Flat POD for the C ABI; pointers borrow this object's vectors.
   xbs_layer_options to_c() const {

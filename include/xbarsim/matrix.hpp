@@ -51,4 +51,29 @@ class MatrixXd {
   std::vector<double> v_;
 };
 
+/// Minimal stand-in for Eigen::VectorXd (reconstruct_output's codes).
+class VectorXd {
+ public:
+  using Index = std::int64_t;
+  VectorXd() = default;
+  explicit VectorXd(Index n, double fill = 0.0) : v_(static_cast<size_t>(n < 0 ? 0 : n), fill) {
+    if (n < 0) throw std::invalid_argument("VectorXd: negative dimension");
+  }
+  static VectorXd Zero(Index n) { return VectorXd(n, 0.0); }
+  static VectorXd Constant(Index n, double v) { return VectorXd(n, v); }
+  Index size() const { return static_cast<Index>(v_.size()); }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+  double& operator()(Index i) { return v_[static_cast<size_t>(i)]; }
+  double operator()(Index i) const { return v_[static_cast<size_t>(i)]; }
+  double& operator[](Index i) { return v_[static_cast<size_t>(i)]; }
+  double operator[](Index i) const { return v_[static_cast<size_t>(i)]; }
+  void resize(Index n) { v_.assign(static_cast<size_t>(n), 0.0); }
+  bool operator==(const VectorXd& o) const { return v_ == o.v_; }
+  bool operator!=(const VectorXd& o) const { return !(*this == o); }
+
+ private:
+  std::vector<double> v_;
+};
+
 }  // namespace xbarsim

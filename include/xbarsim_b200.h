@@ -188,6 +188,92 @@ int xbs_conv2d_forward_device(xbs_conv2d* conv, const double* d_x, int64_t batch
 int xbs_conv2d_backward_device(xbs_conv2d* conv, const double* d_dy, int64_t batch, double* d_dx);
 int xbs_conv2d_apply_updates(xbs_conv2d* conv, uint64_t iteration);
 
+/* ---- Free functions of the operator API (mapping.hpp:92-109, update.hpp:25-52)
+ *
+ * mapping::TiledLayerWeights (mapping.hpp:39-90) as a device-resident
+ * object: the per-slice signed master in HBM, mutated only by
+ * xbs_apply_update / xbs_weights_set_master.  A view of a core's weights
+ * (xbs_core_weights) reads the live core; setting its master regenerates
+ * the core's conductances like xbs_core_set_master. */
+typedef struct xbs_weights xbs_weights;
+typedef struct xbs_weights_info {
+  int32_t rows, cols;                 /* K, N                                 */
+  int32_t padded_rows, padded_cols;   /* grid * tile dims                     */
+  int32_t grid_rows, grid_cols;
+  int32_t num_slices;
+  int32_t tile_rows, tile_cols;
+  int32_t weight_bits, device_bits;
+  double layer_scale, level_step;
+  double variation_sigma;
+  uint64_t variation_seed;
+  double g_min, g_max;                /* tile_config() conductance range      */
+} xbs_weights_info;
+
+/* mapping::map_weights(W, spec, cfg) (mapping.cpp:83-131): reads the
+ * MappingSpec (weight_bits, device_bits, tile_rows/cols, variation_sigma /
+ * seed, w_max) and CrossbarConfig fields of opt; the others are ignored.
+ * Errors as the reference: CrossbarConfig / MappingSpec validation, then
+ * non-finite and empty W -> XBS_INVALID_ARGUMENT. */
+int xbs_map_weights(const xbs_layer_options* opt, const double* W, int64_t K, int64_t N, int64_t ldw,
+                    xbs_weights** out);
+/* mapping::apply_variation(t, sigma, seed) (mapping.cpp:133-140): a copy
+ * carrying new variation parameters; the master is copied unchanged. */
+int xbs_weights_apply_variation(const xbs_weights* w, double sigma, uint64_t seed, xbs_weights** out);
+/* View of a core's weights (CrossbarCore::weights(), layers.hpp:59); owned by
+ * the core, valid until xbs_core_destroy; destroy the view with
+ * xbs_weights_destroy (the core is untouched). */
+int xbs_core_weights(xbs_core* core, xbs_weights** out);
+void xbs_weights_destroy(xbs_weights* w);
+int xbs_weights_get_info(const xbs_weights* w, xbs_weights_info* info);
+/* master_diff(slice) / mutable_master_diff(slice) write-back (padded dims). */
+int xbs_weights_master(const xbs_weights* w, int32_t slice, double* u, int64_t ld);
+int xbs_weights_set_master(xbs_weights* w, int32_t slice, const double* u, int64_t ld);
+/* master_polarity(slice, p) (mapping.cpp:39-45) and ideal_working(slice, p)
+ * (mapping.cpp:47-58, variation from the counter RNG): padded dims. */
+int xbs_weights_master_polarity(const xbs_weights* w, int32_t slice, int32_t polarity, double* g, int64_t ld);
+int xbs_weights_ideal_working(const xbs_weights* w, int32_t slice, int32_t polarity, double* g, int64_t ld);
+/* implied_weights() (mapping.cpp:70-81): K x N. */
+int xbs_weights_implied(const xbs_weights* w, double* W, int64_t ld);
+
+/* UpdateSpec (update.hpp:13-23) */
+typedef struct xbs_update_spec {
+  double v, gamma, lr;
+  uint64_t seed;
+  double layer_scale; /* 0: the weights' mapping scale */
+} xbs_update_spec;
+/* update::apply_update(t, dW, spec, iteration) (update.cpp:43-88): the
+ * master only, on the device; the caller regenerates (a core view refuses:
+ * CrossbarCore::apply_updates does update + regeneration).  UpdateSpec
+ * validation, shape mismatch and a non-finite dW -> XBS_INVALID_ARGUMENT
+ * before anything changes; a device state outside [g_min, g_max] ->
+ * XBS_INVALID_ARGUMENT (nonlinear_update, update.cpp:28-29). */
+int xbs_apply_update(xbs_weights* w, const double* dW, int64_t K, int64_t N, int64_t ld, const xbs_update_spec* spec,
+                     uint64_t iteration);
+/* update::scale_gradient (update.cpp:16-24): out = dW * ((g_max - g_min) /
+ * layer_scale), K x N column-major; layer_scale == 0 -> XBS_CONFIG_ERROR,
+ * non-finite dW -> XBS_INVALID_ARGUMENT. */
+int xbs_scale_gradient(const double* dW, int64_t K, int64_t N, int64_t ld, double layer_scale, double g_min,
+                       double g_max, double* out, int64_t ldo);
+/* update::nonlinear_update (update.cpp:26-33), elementwise over n devices;
+ * any g outside [g_min, g_max] -> XBS_INVALID_ARGUMENT. */
+int xbs_nonlinear_update(const double* g, const double* dg, int64_t n, double v, double g_min, double g_max,
+                         double* out);
+/* update::write_noise (update.cpp:35-41), elementwise: element i draws one
+ * Gaussian from the counter RNG (rng.hpp) with key keys[i] at counters
+ * counters[i] + 1 and + 2, unless its deviation is 0 (then out[i] = 0 and
+ * nothing is drawn, as in the reference); drew[i] (nullable) = 1 if it drew.
+ * The caller advances its CounterRng by 2 per drawing element. */
+int xbs_write_noise(const double* dg, int64_t n, double gamma, double g_min, double g_max, const uint64_t* keys,
+                    const uint64_t* counters, double* out, int32_t* drew);
+/* mapping::reconstruct_output (mapping.cpp:142-160): codes_pos / codes_neg
+ * are slices x n (slice-major, contiguous); out = scale * sum_s
+ * 2^(s*device_bits) (pos_s - neg_s) in the reference's order. */
+int xbs_reconstruct_output(const double* codes_pos, const double* codes_neg, int32_t slices, int64_t n,
+                           int32_t device_bits, double scale, double* out);
+/* CrossbarLayerOptions::validate (layers.cpp:17-47): the reference's checks
+ * and exception classes, no device work. */
+int xbs_options_validate(const xbs_layer_options* opt);
+
 /* Per-stage device timing (CUDA events recorded on the core's stream around
  * each stage while enabled).  Stages: 0 prep_x (K0a), 1 forward VMM (K1),
  * 2 prep_dy (K0b), 3 dW (K3a), 4 backward VMM (K2), 5 update+regeneration

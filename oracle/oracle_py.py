@@ -44,7 +44,7 @@ def lib():
         L.orc_core_backward_tiles.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_long, ctypes.c_double,
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, _D]
         L.orc_core_apply_updates.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
-        for n in ("orc_core_gradient", "orc_core_implied_weights"):
+        for n in ("orc_core_gradient", "orc_core_implied_weights", "orc_core_set_gradient"):
             getattr(L, n).argtypes = [ctypes.c_void_p, _D]
         L.orc_core_nonideal.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
         L.orc_core_set_nonideal.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
@@ -158,6 +158,10 @@ class OracleCore:
         g = np.zeros((self.K, self.N), order="F")
         _check(lib().orc_core_gradient(self._h, _p(g)))
         return g
+
+    def set_gradient(self, dW):
+        dW = _f(dW)
+        _check(lib().orc_core_set_gradient(self._h, _p(dW)))
 
     def implied_weights(self):
         g = np.zeros((self.K, self.N), order="F")

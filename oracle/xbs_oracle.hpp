@@ -309,6 +309,12 @@ class CrossbarCore {  // layers.hpp:49-111
   const TiledLayerWeights& weights() const { return weights_; }
   TiledLayerWeights& mutable_weights() { return weights_; }
   const Matrix& gradient() const { return dW_; }
+  // parity harness: feed a gradient for the next apply_updates (the GPU's
+  // xbs_core_set_gradient)
+  void set_gradient(const Matrix& dW) {
+    dW_ = dW;
+    have_grad_ = true;
+  }
   long refresh_count() const { return refreshes_; }
   double weight_abs_max_seen() const { return wmax_seen_; }
   double grad_abs_max_seen() const { return dwmax_seen_; }

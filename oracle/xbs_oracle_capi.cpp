@@ -196,6 +196,12 @@ int orc_core_apply_updates(void* h, uint64_t it) {
 int orc_core_gradient(void* h, double* out) {
   return guard([&] { unwrap(C(h)->gradient(), out); });
 }
+int orc_core_set_gradient(void* h, const double* dW) {
+  return guard([&] {
+    const auto& w = C(h)->weights();
+    C(h)->set_gradient(wrap(dW, w.rows(), w.cols()));
+  });
+}
 int orc_core_nonideal(void* h, int s, int p, int t, double* out) {
   return guard([&] { unwrap(C(h)->nonideal(s, p ? orc::Polarity::neg : orc::Polarity::pos, t), out); });
 }

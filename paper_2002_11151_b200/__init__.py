@@ -13,6 +13,7 @@ from .xbarsim import (  # noqa: F401
     CrossbarConv2d,
     CrossbarCore,
     CrossbarLayerOptions,
+    CounterRng,
     CrossbarLinear,
     DacSpec,
     EngineKind,
@@ -22,7 +23,15 @@ from .xbarsim import (  # noqa: F401
     Polarity,
     ReLU,
     StateError,
+    TiledLayerWeights,
     Tensor,
     UpdateSpec,
+    apply_update,
+    apply_variation,
+    map_weights,
+    nonlinear_update,
+    reconstruct_output,
+    scale_gradient,
     softmax_cross_entropy,
+    write_noise,
 )

@@ -712,12 +712,17 @@ void xbs_options_init(xbs_layer_options* o) {
   o->threads = 1;
 }
 
-int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, int64_t N, int64_t ldw,
-                    xbs_core** out) {
-  return guard([&] {
-    if (!opt || !out) fail(XBS_INVALID_ARGUMENT, "xbs_core_create: null argument");
-    *out = nullptr;
+}  // extern "C"
+
+namespace {
+// CrossbarCore::CrossbarCore (layers.cpp:68-83).  weights_only: just
+// mapping::map_weights (mapping.cpp:83-131) -- geometry, layer scale and the
+// device master, for the free-function TiledLayerWeights (xbs_weights.cu).
+xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K, int64_t N, int64_t ldw,
+                      bool weights_only) {
+    if (!opt) fail(XBS_INVALID_ARGUMENT, "xbs_core_create: null argument");
     auto c = std::make_unique<xbs_core>();
+    c->weights_only = weights_only;
     c->opt = *opt;
     if (opt->dac_transfer && opt->dac_transfer_len > 0)
       c->dac_tr.assign(opt->dac_transfer, opt->dac_transfer + opt->dac_transfer_len);
@@ -738,8 +743,10 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
         if (!std::isfinite(w)) fail(XBS_INVALID_ARGUMENT, "map_weights: weights must be finite");
         wabs = std::max(wabs, std::abs(w));
       }
-    validate_options(o, c->dac_tr, c->adc_tr);  // layers.cpp:70
-    check_scope(o, c->dac_tr, c->adc_tr);
+    if (!weights_only) {
+      validate_options(o, c->dac_tr, c->adc_tr);  // layers.cpp:70
+      check_scope(o, c->dac_tr, c->adc_tr);
+    }
 
     xbs::Geo& g = c->g;
     g.K = int(K);
@@ -816,6 +823,22 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     c->adc_b = a;
 
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (weights_only) {
+      ck(cudaMalloc(&c->d_master, size_t(g.S) * g.Kp * g.Np * 8), "cudaMalloc master");
+      ck(cudaMalloc(&c->d_dW, size_t(g.K) * g.N * 8), "cudaMalloc dW");
+      ck(cudaMalloc(&c->d_sc, sizeof(xbs::DevScalars)), "cudaMalloc scalars");
+      ck(cudaMemsetAsync(c->d_sc, 0, sizeof(xbs::DevScalars), c->stream), "memset scalars");
+      ck(cudaMallocHost(&c->h_sc, sizeof(xbs::DevScalars)), "cudaMallocHost");
+      double* d_W = nullptr;
+      ck(cudaMalloc(&d_W, size_t(K) * N * 8), "cudaMalloc W");
+      ck(cudaMemcpy2DAsync(d_W, size_t(K) * 8, W0, size_t(ldw) * 8, size_t(K) * 8, size_t(N), cudaMemcpyHostToDevice,
+                           c->stream),
+         "H2D W");
+      xbs::launch_map_weights(c.get(), d_W, c->stream);
+      ck(cudaStreamSynchronize(c->stream), "map_weights");
+      cudaFree(d_W);
+      return c.release();
+    }
     if (!a.passthrough) {
       set_adc(c.get(), 0, o.adc_i_fs);
       set_adc(c.get(), 1, o.adc_i_fs);
@@ -865,7 +888,43 @@ int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, i
     check_fcm(c.get());
     c->conversion_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     cudaFree(d_W);
-    *out = c.release();
+    return c.release();
+}
+}  // namespace
+
+namespace xbs {
+xbs_core* create_weights_core(const xbs_layer_options* opt, const double* W, int64_t K, int64_t N, int64_t ldw) {
+  return create_core(opt, W, K, N, ldw, true);
+}
+void core_settle(xbs_core* c) { sync(c); }
+void core_h2d_rowmajor(xbs_core* c, const double* h, int64_t rows, int64_t cols, int64_t ld, double* d) {
+  h2d_colmajor_to_rowmajor(c, h, rows, cols, ld, d);
+}
+void core_d2h_rowmajor(xbs_core* c, const double* d, int64_t rows, int64_t cols, double* h, int64_t ld) {
+  d2h_rowmajor_to_colmajor(c, d, rows, cols, h, ld);
+}
+}  // namespace xbs
+
+extern "C" {
+
+int xbs_options_validate(const xbs_layer_options* opt) {
+  return guard([&] {
+    if (!opt) fail(XBS_INVALID_ARGUMENT, "xbs_options_validate: null argument");
+    std::vector<double> dac_tr, adc_tr;
+    if (opt->dac_transfer && opt->dac_transfer_len > 0)
+      dac_tr.assign(opt->dac_transfer, opt->dac_transfer + opt->dac_transfer_len);
+    if (opt->adc_transfer && opt->adc_transfer_len > 0)
+      adc_tr.assign(opt->adc_transfer, opt->adc_transfer + opt->adc_transfer_len);
+    validate_options(*opt, dac_tr, adc_tr);  // layers.cpp:17-47
+  });
+}
+
+int xbs_core_create(const xbs_layer_options* opt, const double* W0, int64_t K, int64_t N, int64_t ldw,
+                    xbs_core** out) {
+  return guard([&] {
+    if (!out) fail(XBS_INVALID_ARGUMENT, "xbs_core_create: null argument");
+    *out = nullptr;
+    *out = create_core(opt, W0, K, N, ldw, false);
   });
 }
 

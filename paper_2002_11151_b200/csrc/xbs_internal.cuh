@@ -131,6 +131,7 @@ struct xbs_core {
   cudaEvent_t copy_ev = nullptr;
   bool own_stream = true;  // false after xbs_core_set_stream(caller's stream)
   int kernel = 0;  // 0 tcgen05, 1 SIMT
+  bool weights_only = false;  // a mapping::TiledLayerWeights (xbs_weights.cu): master only, no conductances
   bool fully_ideal = false;
   bool adc_scaled = false;  // k_out includes i_fs/(2^bits-1)
   double layer_scale = 1.0, level_step = 0.0;
@@ -253,6 +254,12 @@ void launch_digits_to_g(const xbs_core* c, int s, int p, int tr, int tc, double*
 bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_t st);
 bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream_t st);
 bool launch_dw_tc(xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st);
+// TiledLayerWeights objects (xbs_weights.cu) share the core's geometry,
+// master layout and kernels
+xbs_core* create_weights_core(const xbs_layer_options* opt, const double* W, int64_t K, int64_t N, int64_t ldw);
+void core_settle(xbs_core* c);
+void core_h2d_rowmajor(xbs_core* c, const double* h, int64_t rows, int64_t cols, int64_t ld, double* d);
+void core_d2h_rowmajor(xbs_core* c, const double* d, int64_t rows, int64_t cols, double* h, int64_t ld);
 // ADC auto-calibration (xbs_calib.cu)
 void calib_observe_fwd(xbs_core* c, int64_t M, cudaStream_t st);
 void calib_observe_bwd(xbs_core* c, int64_t M, cudaStream_t st);

@@ -15,26 +15,9 @@
 #include <math.h>
 
 #include "xbs_internal.cuh"
+#include "xbs_rng.cuh"
 
 namespace xbs {
-
-// ------------------------------------------------------------------ rng.hpp
-__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t v) {
-  h += 0x9e3779b97f4a7c15ull + v;
-  h = (h ^ (h >> 30)) * 0xbf58476d1ce4e5b9ull;
-  h = (h ^ (h >> 27)) * 0x94d049bb133111ebull;
-  return h ^ (h >> 31);
-}
-__device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
-  return mix64(mix64(mix64(mix64(0x9e3779b97f4a7c15ull ^ seed, a), b), c), 0);
-}
-__device__ __forceinline__ double to_unit(uint64_t x) { return double(x >> 11) * 0x1.0p-53; }
-// rng.hpp:31-36 (draws 1 and 2 of the keyed stream)
-__device__ __forceinline__ double rng_gaussian(uint64_t key) {
-  double u1 = 1.0 - to_unit(mix64(key, 1));
-  double u2 = to_unit(mix64(key, 2));
-  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925287 * u2);
-}
 
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
   atomicMax(p, (unsigned long long)__double_as_longlong(v));

@@ -156,6 +156,11 @@ class CrossbarLayerOptions:
     adc_cal_batches: int = 20
     threads: int = 1
 
+    def validate(self) -> None:
+        """layers.cpp:17-47 (through the C ABI: same checks and exception classes)."""
+        o = self.to_c()
+        _check(load_library().xbs_options_validate(ctypes.byref(o)))
+
     def to_c(self) -> "CLayerOptions":
         """Flat POD (include/xbarsim_b200.h xbs_layer_options)."""
         o = CLayerOptions()
@@ -221,6 +226,24 @@ class CoreInfo(ctypes.Structure):
     ]
 
 
+class WeightsInfo(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+        ("padded_rows", ctypes.c_int32), ("padded_cols", ctypes.c_int32),
+        ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
+        ("num_slices", ctypes.c_int32), ("tile_rows", ctypes.c_int32), ("tile_cols", ctypes.c_int32),
+        ("weight_bits", ctypes.c_int32), ("device_bits", ctypes.c_int32),
+        ("layer_scale", ctypes.c_double), ("level_step", ctypes.c_double),
+        ("variation_sigma", ctypes.c_double), ("variation_seed", ctypes.c_uint64),
+        ("g_min", ctypes.c_double), ("g_max", ctypes.c_double),
+    ]
+
+
+class CUpdateSpec(ctypes.Structure):
+    _fields_ = [("v", ctypes.c_double), ("gamma", ctypes.c_double), ("lr", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("layer_scale", ctypes.c_double)]
+
+
 # Exported symbols (name -> (restype, argtypes)); tests check every one of
 # them against include/xbarsim_b200.h.
 _P = ctypes.c_void_p
@@ -267,6 +290,25 @@ SYMBOLS = {
     "xbs_core_use_graphs": (ctypes.c_int, [_P, ctypes.c_int32]),
     "xbs_core_stage_times": (ctypes.c_int, [_P, _D, ctypes.POINTER(_I64), ctypes.c_int32]),
     "xbs_core_launch_count": (_I64, [_P]),
+    "xbs_map_weights": (ctypes.c_int, [ctypes.POINTER(CLayerOptions), _D, _I64, _I64, _I64, ctypes.POINTER(_P)]),
+    "xbs_weights_apply_variation": (ctypes.c_int, [_P, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "xbs_core_weights": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "xbs_weights_destroy": (None, [_P]),
+    "xbs_weights_get_info": (ctypes.c_int, [_P, ctypes.POINTER(WeightsInfo)]),
+    "xbs_weights_master": (ctypes.c_int, [_P, ctypes.c_int32, _D, _I64]),
+    "xbs_weights_set_master": (ctypes.c_int, [_P, ctypes.c_int32, _D, _I64]),
+    "xbs_weights_master_polarity": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _D, _I64]),
+    "xbs_weights_ideal_working": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _D, _I64]),
+    "xbs_weights_implied": (ctypes.c_int, [_P, _D, _I64]),
+    "xbs_apply_update": (ctypes.c_int, [_P, _D, _I64, _I64, _I64, ctypes.POINTER(CUpdateSpec), ctypes.c_uint64]),
+    "xbs_scale_gradient": (ctypes.c_int, [_D, _I64, _I64, _I64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                          _D, _I64]),
+    "xbs_nonlinear_update": (ctypes.c_int, [_D, _D, _I64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _D]),
+    "xbs_write_noise": (ctypes.c_int, [_D, _I64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                       ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64), _D,
+                                       ctypes.POINTER(ctypes.c_int32)]),
+    "xbs_reconstruct_output": (ctypes.c_int, [_D, _D, ctypes.c_int32, _I64, ctypes.c_int32, ctypes.c_double, _D]),
+    "xbs_options_validate": (ctypes.c_int, [ctypes.POINTER(CLayerOptions)]),
 }
 
 STAGES = ("prep_x", "fwd_vmm", "prep_dy", "dw", "bwd_vmm", "update")
@@ -385,6 +427,12 @@ class CrossbarCore:
         dW = _fortran(dW)
         _check(load_library().xbs_core_set_gradient(self._h, _ptr(dW), self._K))
 
+    def weights(self) -> "TiledLayerWeights":
+        """CrossbarCore::weights() (layers.hpp:59): a view of the core's state."""
+        h = ctypes.c_void_p()
+        _check(load_library().xbs_core_weights(self._h, ctypes.byref(h)))
+        return TiledLayerWeights(h, owner=self)
+
     def refresh_count(self) -> int:
         return int(self.info().refresh_count)
 
@@ -468,6 +516,211 @@ class CrossbarCore:
 
 
 @dataclasses.dataclass
+# ------------------------------------------- free functions (mapping / update)
+class TiledLayerWeights:
+    """mapping::TiledLayerWeights (mapping.hpp:39-90): device-resident master.
+    From map_weights / apply_variation (owned) or CrossbarCore.weights()
+    (a view of the core's live state)."""
+
+    def __init__(self, handle, owner=None):
+        self._h = handle
+        self._owner = owner  # the core of a view (kept alive)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.xbs_weights_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> WeightsInfo:
+        i = WeightsInfo()
+        _check(load_library().xbs_weights_get_info(self._h, ctypes.byref(i)))
+        return i
+
+    def rows(self):
+        return self.info().rows
+
+    def cols(self):
+        return self.info().cols
+
+    def padded_rows(self):
+        return self.info().padded_rows
+
+    def padded_cols(self):
+        return self.info().padded_cols
+
+    def grid_rows(self):
+        return self.info().grid_rows
+
+    def grid_cols(self):
+        return self.info().grid_cols
+
+    def num_slices(self):
+        return self.info().num_slices
+
+    def layer_scale(self):
+        return self.info().layer_scale
+
+    def level_step(self):
+        return self.info().level_step
+
+    def variation_sigma(self):
+        return self.info().variation_sigma
+
+    def variation_seed(self):
+        return self.info().variation_seed
+
+    def master_diff(self, s: int) -> np.ndarray:
+        i = self.info()
+        u = np.zeros((i.padded_rows, i.padded_cols), order="F")
+        _check(load_library().xbs_weights_master(self._h, s, _ptr(u), max(1, i.padded_rows)))
+        return u
+
+    def set_master_diff(self, s: int, u: np.ndarray) -> None:
+        u = _fortran(u)
+        _check(load_library().xbs_weights_set_master(self._h, s, _ptr(u), max(1, u.shape[0])))
+
+    def _padded(self, fn, s, p):
+        i = self.info()
+        g = np.zeros((i.padded_rows, i.padded_cols), order="F")
+        _check(fn(self._h, s, int(p), _ptr(g), max(1, i.padded_rows)))
+        return g
+
+    def master_polarity(self, s: int, p: "Polarity") -> np.ndarray:
+        return self._padded(load_library().xbs_weights_master_polarity, s, p)
+
+    def ideal_working(self, s: int, p: "Polarity") -> np.ndarray:
+        return self._padded(load_library().xbs_weights_ideal_working, s, p)
+
+    def ideal_tile(self, s: int, p: "Polarity", tr: int, tc: int) -> np.ndarray:
+        i = self.info()
+        if not (0 <= tr < i.grid_rows and 0 <= tc < i.grid_cols):
+            raise ValueError("TiledLayerWeights: tile index out of range")
+        w = self.ideal_working(s, p)
+        return np.asfortranarray(w[tr * i.tile_rows:(tr + 1) * i.tile_rows, tc * i.tile_cols:(tc + 1) * i.tile_cols])
+
+    def implied_weights(self) -> np.ndarray:
+        i = self.info()
+        w = np.zeros((i.rows, i.cols), order="F")
+        _check(load_library().xbs_weights_implied(self._h, _ptr(w), max(1, i.rows)))
+        return w
+
+
+def map_weights(W: np.ndarray, spec: "MappingSpec", cfg: "CrossbarConfig") -> TiledLayerWeights:
+    """mapping::map_weights (mapping.cpp:83-131) on the device."""
+    o = CrossbarLayerOptions(map=spec, crossbar=cfg).to_c()
+    W = _fortran(W)
+    if W.ndim != 2:
+        raise ValueError("map_weights: W must be a matrix")
+    h = ctypes.c_void_p()
+    _check(load_library().xbs_map_weights(ctypes.byref(o), _ptr(W), W.shape[0], W.shape[1], max(1, W.shape[0]),
+                                          ctypes.byref(h)))
+    return TiledLayerWeights(h)
+
+
+def apply_variation(t: TiledLayerWeights, sigma: float, seed: int) -> TiledLayerWeights:
+    """mapping::apply_variation (mapping.cpp:133-140): a copy, new variation."""
+    h = ctypes.c_void_p()
+    _check(load_library().xbs_weights_apply_variation(t.handle, float(sigma), int(seed), ctypes.byref(h)))
+    return TiledLayerWeights(h)
+
+
+def reconstruct_output(codes_pos, codes_neg, spec: "MappingSpec", scale: float) -> np.ndarray:
+    """mapping::reconstruct_output (mapping.cpp:142-160) on the device."""
+    S = spec.num_slices()
+    if len(codes_pos) != S or len(codes_neg) != S:
+        raise ValueError("reconstruct_output: need codes for every slice")
+    n = len(codes_pos[0]) if S else 0
+    if any(len(c) != n for c in list(codes_pos) + list(codes_neg)):
+        raise ValueError("reconstruct_output: inconsistent code lengths")
+    pos = np.ascontiguousarray(np.asarray(codes_pos, dtype=np.float64).reshape(S, n))
+    neg = np.ascontiguousarray(np.asarray(codes_neg, dtype=np.float64).reshape(S, n))
+    out = np.zeros(n)
+    _check(load_library().xbs_reconstruct_output(_ptr(pos), _ptr(neg), S, n, spec.device_bits, float(scale),
+                                                 _ptr(out)))
+    return out
+
+
+def _cspec(spec: "UpdateSpec") -> CUpdateSpec:
+    return CUpdateSpec(spec.v, spec.gamma, spec.lr, spec.seed, spec.layer_scale)
+
+
+def apply_update(t: TiledLayerWeights, dW: np.ndarray, spec: "UpdateSpec", iteration: int) -> None:
+    """update::apply_update (update.cpp:43-88): the master only, on the device."""
+    dW = _fortran(dW)
+    cs = _cspec(spec)
+    _check(load_library().xbs_apply_update(t.handle, _ptr(dW), dW.shape[0], dW.shape[1], max(1, dW.shape[0]),
+                                           ctypes.byref(cs), int(iteration)))
+
+
+def scale_gradient(dW: np.ndarray, spec: "UpdateSpec", cfg: "CrossbarConfig") -> np.ndarray:
+    """update::scale_gradient (update.cpp:16-24) on the device."""
+    dW = _fortran(dW)
+    out = np.zeros_like(dW, order="F")
+    _check(load_library().xbs_scale_gradient(_ptr(dW), dW.shape[0], dW.shape[1], max(1, dW.shape[0]),
+                                             spec.layer_scale, cfg.g_min, cfg.g_max, _ptr(out), max(1, dW.shape[0])))
+    return out
+
+
+def nonlinear_update(g, dg, spec: "UpdateSpec", cfg: "CrossbarConfig"):
+    """update::nonlinear_update (update.cpp:26-33), elementwise on the device."""
+    g_, dg_ = np.ascontiguousarray(np.atleast_1d(g), np.float64), np.ascontiguousarray(np.atleast_1d(dg), np.float64)
+    g_, dg_ = np.broadcast_arrays(g_, dg_)
+    g_, dg_ = np.ascontiguousarray(g_), np.ascontiguousarray(dg_)
+    out = np.zeros(g_.size)
+    _check(load_library().xbs_nonlinear_update(_ptr(g_), _ptr(dg_), g_.size, spec.v, cfg.g_min, cfg.g_max, _ptr(out)))
+    return float(out[0]) if np.ndim(g) == 0 and np.ndim(dg) == 0 else out
+
+
+_GOLDEN = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+def _splitmix(h: int, v: int) -> int:
+    h = (h + _GOLDEN + v) & _M64
+    h = ((h ^ (h >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    h = ((h ^ (h >> 27)) * 0x94D049BB133111EB) & _M64
+    return h ^ (h >> 31)
+
+
+class CounterRng:
+    """rng.hpp:12-48: stateless keyed counter generator (host utility; the
+    update kernels draw the same stream on the device)."""
+
+    def __init__(self, seed: int, a: int, b: int = 0, c: int = 0):
+        self.key = _splitmix(_splitmix(_splitmix(_splitmix(_GOLDEN ^ (seed & _M64), a & _M64), b & _M64),
+                                       c & _M64), 0)
+        self.counter = 0
+
+    def _next(self) -> int:
+        self.counter += 1
+        return _splitmix(self.key, self.counter)
+
+    def uniform(self) -> float:
+        return float(self._next() >> 11) * 2.0 ** -53
+
+    def gaussian(self) -> float:
+        u1 = 1.0 - self.uniform()
+        u2 = self.uniform()
+        return float(np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586476925287 * u2))
+
+
+def write_noise(dg: float, spec: "UpdateSpec", cfg: "CrossbarConfig", rng: CounterRng) -> float:
+    """update::write_noise (update.cpp:35-41) on the device; advances rng by
+    the two draws of a Gaussian unless the deviation is 0."""
+    d = np.array([float(dg)])
+    key, ctr = (ctypes.c_uint64 * 1)(rng.key), (ctypes.c_uint64 * 1)(rng.counter)
+    out, drew = np.zeros(1), (ctypes.c_int32 * 1)()
+    _check(load_library().xbs_write_noise(_ptr(d), 1, spec.gamma, cfg.g_min, cfg.g_max, key, ctr, _ptr(out), drew))
+    if drew[0]:
+        rng.counter += 2
+    return float(out[0])
+
+
 class Tensor:
     """tensor.hpp:13-21"""
 
