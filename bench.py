@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "non-ideal crossbar MACs/s (fwd+bwd+update) on 1 B200; % of int8 TC / HBM roofline"
-L_LIMBS = 4  # u8 limbs per snapped conductance (radix-255 digits) -> int8 ops = 2 * L * MAC
+L_LIMBS = 3  # u8 limbs per snapped conductance (three radix-255 digits, 24-bit grid) -> int8 ops = 2 * L * MAC
 
 
 def parse():

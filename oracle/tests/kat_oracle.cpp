@@ -740,7 +740,8 @@ TEST_CASE("streaming pipeline with disabled non-idealities equals the direct mat
   // rounds (u = q * fl(2^-14/255) is not on the dyadic grid), so equality
   // depends on Eigen's summation order and cannot be verified here (the
   // reference does not build).  literal: agrees to 1e-14 relative.
-  // snapped: the 2^-e grid moves each conductance by <= 2^-(e+1) -> 1e-8.
+  // snapped: the 2^-e grid (24 bits below g_max) moves each conductance by
+  // <= 2^-(e+1), ~2e-6 relative at g_min = g_max / 64 here -> 4e-6.
   for (int snapped = 0; snapped < 2; ++snapped) {
     std::mt19937_64 rng(3);
     Matrix W = random_matrix(8, 6, rng);
@@ -752,7 +753,7 @@ TEST_CASE("streaming pipeline with disabled non-idealities equals the direct mat
     Matrix x = cabs(random_matrix(5, 8, rng, 1.0));
     Matrix a = lin_streamed.forward(make_input(x), false).values, b = lin_fast.forward(make_input(x), false).values;
     if (!snapped) CHECK(maxdiff(a, b) <= 1e-14 * max_abs(b));
-    else CHECK(maxdiff(a, b) <= 1e-8 * max_abs(b));
+    else CHECK(maxdiff(a, b) <= 4e-6 * max_abs(b));
   }
 }
 

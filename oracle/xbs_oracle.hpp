@@ -259,8 +259,9 @@ double write_noise(double dg_ideal, const UpdateSpec& spec, const CrossbarConfig
 void apply_update(TiledLayerWeights& t, const Matrix& dW, const UpdateSpec& spec, uint64_t iteration);
 
 // ------------------------------------------------------- snapped exactness grid
-// Q_MAX = 65025^2 - 1: the largest snapped level (two radix-255 digit pairs).
-constexpr double kQMax = 4228250624.0;  // 65025.0 * 65025.0 - 1
+// Q_MAX = 255^3 - 1: the largest snapped level (three radix-255 u8 digits,
+// the GPU's tensor-core limbs).
+constexpr double kQMax = 16581374.0;  // 255.0 * 255.0 * 255.0 - 1
 // Largest e with g_max * 2^e <= Q_MAX (radix-255 variant).
 int snap_exponent(double g_max);
 double snap_conductance(double g, int e);  // nearbyint(g * 2^e) * 2^-e

@@ -25,7 +25,7 @@ namespace {
 __device__ __forceinline__ uint32_t q_at(const uint8_t* digits, const Geo& g, int s, int p, int tr, int tc, int r,
                                          int c) {
   const size_t base = g.tile_digit_offset(s, p, tr, tc, 0) + size_t(r) * g.C + c, ps = g.plane_bytes();
-  return (digits[base] + 255u * digits[base + ps]) + 65025u * (digits[base + 2 * ps] + 255u * digits[base + 3 * ps]);
+  return (digits[base] + 255u * digits[base + ps]) + 65025u * digits[base + 2 * ps];
 }
 
 // Forward observations (layers.cpp:252-257): n of column c of tile (tr, tc)

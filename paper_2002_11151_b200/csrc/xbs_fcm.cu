@@ -42,8 +42,7 @@ __device__ __forceinline__ void store_q(uint8_t* digits, const Geo& g, int s, in
   const size_t off = size_t(r) * g.C + c;
   digits[g.tile_digit_offset(s, p, tr, tc, 0) + off] = uint8_t(lo % 255u);
   digits[g.tile_digit_offset(s, p, tr, tc, 1) + off] = uint8_t(lo / 255u);
-  digits[g.tile_digit_offset(s, p, tr, tc, 2) + off] = uint8_t(hi % 255u);
-  digits[g.tile_digit_offset(s, p, tr, tc, 3) + off] = uint8_t(hi / 255u);
+  digits[g.tile_digit_offset(s, p, tr, tc, 2) + off] = uint8_t(hi);
 }
 
 __device__ __forceinline__ double block_max(double v, double* red) {

@@ -3,17 +3,21 @@
 //
 // Unit = (two 128-row M-blocks of input bit-plane rows [b * TPi + k], one per
 //         CTA of the pair; 64 device output columns of one tile column).
-// For every crossbar row tile tr, slice s and polarity p the leader CTA
-// issues a K = 2 x R chain of tcgen05.mma.cta_group::2.kind::i8
-// (M = 256 = both M-blocks, N = 128, K = 32):
-//     D[:,  0: 64] = A_bits . d0 + A_255 . d1    (lo digit pair of q)
-//     D[:, 64:128] = A_bits . d2 + A_255 . d3    (hi digit pair of q)
-// i.e. the exact column current of every (row, bit plane, column) split as
-// hi * 65025 + lo in s32 TMEM accumulators (each CTA holds its 128 rows).
-// The B operand is split along N across the pair: the leader stages the lo
-// digit planes (d0, d1), the peer the hi planes (d2, d3), so each SM reads
-// 6 KB of SMEM operands per MMA instead of 8 and each loads half of the
-// conductance tile.  The accumulation K-extent is exactly one crossbar
+// For every crossbar row tile tr and slice s the leader CTA issues, per
+// 128-row k-block, tcgen05.mma.cta_group::2.kind::i8 (M = 256 = both
+// M-blocks, K = 32) in two phases into one 256-column TMEM accumulator
+// holding both polarities:
+//     A_bits phase, N = 256:  D[:, 0:64 | 64:128 | 128:192 | 192:256]
+//                               = A_bits . [d0_pos | d0_neg | d2_pos | d2_neg]
+//     A_255 phase,  N = 128:  D[:, 0:64 | 64:128] += A_255 . [d1_pos | d1_neg]
+// so lo_p = A_bits . d0 + A_255 . d1 sits at 64 p and hi_p = A_bits . d2 at
+// 128 + 64 p: the exact column current of every (row, bit plane, column)
+// as hi * 65025 + lo with q = d0 + 255 d1 + 65025 d2 (three u8 limbs, a
+// 24-bit snapped grid) in s32 (each CTA holds its 128 rows).  That is
+// 3 R int8 MACs per (row, device) instead of the 4 R of a two-pair split.
+// The B operand is split along N across the pair: the leader stages d0 of
+// both polarities and d1_pos, the peer d2 of both polarities and d1_neg
+// (24 KB per k-block each).  The accumulation K-extent is exactly one crossbar
 // (R = 128 or 256 rows, one or two k-blocks); the epilogue then applies the
 // ADC (fp32 fast path + exact threshold fix-up, xbs_tc_common.cuh) and the
 // signed shift-add P += +-2^(s db) * code.  After the last tile the TPi
@@ -24,8 +28,8 @@
 // allocator + (leader only) MMA issuer, warps 2..17 epilogue: warp w reads
 // TMEM lanes 32 (w % 4).. and device columns 16 ((w-2)/4)...
 // Pipelines per CTA: A (own M-block: {bits, 255 bits} x KB k-blocks, 32 KB
-// per k-block) x 3 stages (2 for 256-row crossbars), B (16 KB per k-block:
-// two 64-column SW64 digit boxes) x 6 (5), TMEM accumulators 4 x 128
+// per k-block) x 3 stages (2 for 256-row crossbars), B (24 KB per k-block:
+// three 64-column SW64 digit boxes) x 4, TMEM accumulators 2 x 256
 // columns.  Column blocks made only of tile padding are never scheduled.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -40,9 +44,6 @@ namespace xbs {
 namespace tc {
 
 namespace fw {
-#ifndef XBS_FWD_PIPE
-#define XBS_FWD_PIPE 1
-#endif
 #ifndef XBS_FWD_EPI_WARPS
 #define XBS_FWD_EPI_WARPS 8
 #endif
@@ -52,11 +53,11 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kCW = 64;             // device columns per unit
 constexpr int kABox = 128 * 128;    // 128 rows x 128 B (one k-block), SW128
 constexpr int kBBox = 128 * kCW;    // 128 crossbar rows x 64 columns, SW64
-constexpr int kBStage = 2 * kBBox;  // this CTA's half of one k-block: [dh]
-constexpr int kTBufs = 4;           // TMEM accumulators of 128 columns
+constexpr int kBStage = 3 * kBBox;  // this CTA's boxes of one k-block: two A_bits-phase boxes + one A_255 box
+constexpr int kTBufs = 2;           // TMEM accumulators of 256 columns (one (tr, s), both polarities)
 template <int KB> constexpr int kAStage = 2 * KB * kABox;  // [dh][kb]
 template <int KB> constexpr int kAStages = KB == 1 ? 3 : 2;
-template <int KB> constexpr int kBStages = KB == 1 ? 6 : 5;
+template <int KB> constexpr int kBStages = 4;
 template <int KB>
 constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages<KB> * kBStage + 1024 + 256;
 }  // namespace fw
@@ -180,27 +181,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           __syncwarp();
           if (++as == kAStages) { as = 0; aph ^= 1; }
           for (int s = 0; s < a.S; ++s)
-            for (int p = 0; p < 2; ++p)
 #pragma unroll
-              for (int kb = 0; kb < KB; ++kb) {
-                mbar_wait(&b_empty[bs], bph ^ 1);
-                if (elect_one()) {
-                  if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * kBStage);
-                  const uint32_t fb = mapa(smem_u32(&b_full[bs]), 0);
-                  const int row0 = ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) * a.R + kb * 128;
-                  // leader: lo planes d0 (dh 0), d1 (dh 1); peer: hi planes d2, d3
-                  tma_load_2d_pair(sB + bs * kBStage, &mapB, fb, h * kCW, row0 + (2 * int(rank) + 0) * a.R);
-                  tma_load_2d_pair(sB + bs * kBStage + kBBox, &mapB, fb, h * kCW, row0 + (2 * int(rank) + 1) * a.R);
-                }
-                __syncwarp();
-                if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            for (int kb = 0; kb < KB; ++kb) {
+              mbar_wait(&b_empty[bs], bph ^ 1);
+              if (elect_one()) {
+                if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * kBStage);
+                const uint32_t fb = mapa(smem_u32(&b_full[bs]), 0);
+                // digit plane d of polarity p: row ((((s 2 + p) GR + tr) GC + tc) L + d) R
+                auto row = [&](int p, int d) { return ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * kLimbs + d) * a.R + kb * 128; };
+                // leader: d0_pos, d0_neg, d1_pos; peer: d2_pos, d2_neg, d1_neg
+                const int dpair = rank == 0 ? 0 : 2;
+                tma_load_2d_pair(sB + bs * kBStage, &mapB, fb, h * kCW, row(0, dpair));
+                tma_load_2d_pair(sB + bs * kBStage + kBBox, &mapB, fb, h * kCW, row(1, dpair));
+                tma_load_2d_pair(sB + bs * kBStage + 2 * kBBox, &mapB, fb, h * kCW, row(int(rank), 1));
               }
+              __syncwarp();
+              if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            }
         }
       }
     }
   } else if (warp == 1) {
     if (rank == 0) {  // ------ MMA issuer (leader CTA; converged warp, one lane issues)
-      constexpr uint32_t idesc = idesc_i8(256, 2 * kCW, /*b_mn_major=*/true);
+      constexpr uint32_t idesc_a = idesc_i8(256, 4 * kCW, /*b_mn_major=*/true);  // A_bits phase, N = 256
+      constexpr uint32_t idesc_b = idesc_i8(256, 2 * kCW, /*b_mn_major=*/true);  // A_255 phase, N = 128
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
         const int usp = udiv<NARROW>(u, a.nbase, a.f_nbase);
@@ -209,25 +213,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
           const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
-          for (int sp = 0; sp < 2 * a.S; ++sp) {
+          for (int s = 0; s < a.S; ++s) {
             mbar_wait(&t_empty[ab], abph ^ 1);
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&b_full[bs], bph);
               tc_fence_after();
+              // B: each CTA's boxes MN-major SW64 (8-row K groups 512 B apart,
+              // 32 K rows per MMA = 2 KB; the A_bits phase spans two 64-column
+              // boxes, LBO = one box)
               const uint64_t b0d = sdesc(smem_u32(sB + bs * kBStage), kBBox, 512, 4);
               if (elect_one()) {
 #pragma unroll
                 for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
                   for (int ks = 0; ks < 4; ++ks) {
-                    // A: K-major SW128 (LBO 16, SBO 1024); B: each CTA's
-                    // 64-column half, MN-major SW64 (8-row K groups 512 B
-                    // apart, 32 K rows per MMA = 2 KB)
+                    // A: K-major SW128 (LBO 16, SBO 1024)
                     const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kABox + 32 * ks);
-                    const uint64_t bd = sdesc_add(b0d, dh * kBBox + 2048 * ks);
+                    const uint64_t bd = sdesc_add(b0d, dh * 2 * kBBox + 2048 * ks);
 #ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
-                    umma_i8_pair(tmem + ab * 128, ad, bd, idesc, (kb | dh | ks) != 0);
+                    umma_i8_pair(tmem + ab * 256, ad, bd, dh ? idesc_b : idesc_a, (kb | dh | ks) != 0);
 #else
                     (void)ad; (void)bd;
 #endif
@@ -250,25 +255,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     // warp -> (TMEM lane quarter lg, kCPW-column slice q of the unit's 64)
     const int lg = warp & 3, q = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
-    const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kCPW * q;
+    const uint32_t tl = tmem + (uint32_t(32 * lg) << 16) + kCPW * q;  // + 256 ab + 64 p (+ 128: hi)
     const uint32_t te0 = mapa(smem_u32(&t_empty[0]), 0);  // leader's barriers, 8 B apart
     uint32_t ab = 0, abph = 0, exact = 0;
     const AdcConst k = a.adc;
     for (int u = cid; u < a.num_units; u += ncl) {
       int mbp, nb, tr0, tr1;
       fwd_unit<NARROW>(u, a, mbp, nb, tr0, tr1);
-      const int nchain = (tr1 - tr0) * a.S * 2;
+      const int npair = (tr1 - tr0) * a.S;  // one TMEM buffer per (tr, s): both polarities
       float P[kCPW];
 #pragma unroll
       for (int j = 0; j < kCPW; ++j) P[j] = 0.f;
-      // chains run tr-major, then slice, then polarity: weight +-2^(s db)
-      // (times k.unscale), stepped without integer division
+      // (tr, s) buffers run tr-major, then slice: weight 2^(s db) k.unscale,
+      // + for the positive and - for the negative polarity, stepped without
+      // integer division
       const float wstep = float(1 << a.db);
       float wmag = k.unscale;
-      int sp = 0;
-#if XBS_FWD_PIPE
+      int sl = 0;
       // software-pipelined TMEM reads: one 16-column half is in flight while
-      // the other is converted (A: columns 0-15, B: 16-31 of this warp)
+      // the other is converted (A: columns 0-15, B: 16-31 of this warp);
+      // polarity p's lo sits at +64 p, its hi at +128 + 64 p
       static_assert(kCPW == 32, "pipelined epilogue: 32 columns per warp");
       uint32_t alo[16], ahi[16], blo[16], bhi[16];
       // logical columns in this warp's 32 (narrow layers: N or the tile
@@ -281,100 +287,94 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         nv = min(a.tile_cols, a.N - tcu * a.tile_cols) - hu * kCW - kCPW * q;
       }
       if (NARROW && nv <= 16) {
-        // at most the first 16 columns: one TMEM read and conversion per chain
+        // at most the first 16 columns: one TMEM read per polarity and buffer
         // (none when the warp holds only padding); barrier protocol unchanged
-        for (int c = 0; c < nchain; ++c) {
-          const float w = (sp & 1) == 0 ? wmag : -wmag;
-          if (++sp == 2 * a.S) {
-            sp = 0;
+        for (int c = 0; c < npair; ++c) {
+          const float w = wmag;
+          if (++sl == a.S) {
+            sl = 0;
             wmag = k.unscale;
-          } else if ((sp & 1) == 0) {
+          } else {
             wmag = __fmul_rn(wmag, wstep);
           }
           mbar_wait_hint(&t_full[ab], abph);
           tc_fence_after();
           if (nv > 0) {
-            tmem_ld16(tl + ab * 128, alo);
-            tmem_ld16(tl + ab * 128 + kCW, ahi);
+            tmem_ld16(tl + ab * 256, alo);
+            tmem_ld16(tl + ab * 256 + 128, ahi);
+            tmem_ld16(tl + ab * 256 + 64, blo);
+            tmem_ld16(tl + ab * 256 + 192, bhi);
             tmem_wait_ld();
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
           if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-          if (nv > 0) adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
+          if (nv > 0) {
+            adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
+            adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, -w, P, 0, exact);
+          }
         }
         if (nv <= 0) continue;  // no logical output columns: nothing to combine
       } else {
-      mbar_wait_hint(&t_full[ab], abph);
-      tc_fence_after();
-      tmem_ld16(tl + ab * 128, alo);
-      tmem_ld16(tl + ab * 128 + kCW, ahi);
-      tmem_wait_ld();
-      for (int c = 0; c < nchain; ++c) {
-        const float w = (sp & 1) == 0 ? wmag : -wmag;
-        if (++sp == 2 * a.S) {
-          sp = 0;
-          wmag = k.unscale;
-        } else if ((sp & 1) == 0) {
-          wmag = __fmul_rn(wmag, wstep);
-        }
-        tmem_ld16(tl + ab * 128 + 16, blo);
-        tmem_ld16(tl + ab * 128 + kCW + 16, bhi);
-        adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-        if (c + 1 < nchain) {
-          mbar_wait_hint(&t_full[ab], abph);
-          tc_fence_after();
-          tmem_ld16(tl + ab * 128, alo);
-          tmem_ld16(tl + ab * 128 + kCW, ahi);
-        }
-        adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, w, P, 16, exact);
-        tmem_wait_ld();
-      }
-      }
-#else
-      for (int c = 0; c < nchain; ++c) {
-        const float w = (sp & 1) == 0 ? wmag : -wmag;
-        if (++sp == 2 * a.S) {
-          sp = 0;
-          wmag = k.unscale;
-        } else if ((sp & 1) == 0) {
-          wmag = __fmul_rn(wmag, wstep);
-        }
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
-        uint32_t lo[kCPW], hi[kCPW];
-#pragma unroll
-        for (int h = 0; h < kCPW / 16; ++h) {
-          tmem_ld16(tl + ab * 128 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
-          tmem_ld16(tl + ab * 128 + kCW + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
-        }
+        tmem_ld16(tl + ab * 256, alo);
+        tmem_ld16(tl + ab * 256 + 128, ahi);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-        if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+        for (int c = 0; c < npair; ++c) {
+          const float w = wmag;
+          if (++sl == a.S) {
+            sl = 0;
+            wmag = k.unscale;
+          } else {
+            wmag = __fmul_rn(wmag, wstep);
+          }
+          const uint32_t tb = tl + ab * 256;
+          // positive polarity: columns 0-15 in A, 16-31 loading into B
+          tmem_ld16(tb + 16, blo);
+          tmem_ld16(tb + 128 + 16, bhi);
 #ifdef XBS_STUB_EPI  // perf experiment hook: TMEM loads and barriers only
-        if (lo[0] == 0xdeadbeef && hi[kCPW - 1] == 0x12345) P[0] += w;
-        continue;
+          if (alo[0] == 0xdeadbeef && ahi[15] == 0x12345) P[0] += w;
+#else
+          adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, w, P, 0, exact);
 #endif
-        adc_conv8<0, kCPW, kCPW, 16>(lo, hi, k, w, P, 0, exact);
-        if constexpr (kCPW >= 32) {
-          adc_conv8<16, kCPW, kCPW, 16>(lo, hi, k, w, P, 16, exact);
-        }
-        if constexpr (kCPW >= 64) {
-          adc_conv8<32>(lo, hi, k, w, P, 32, exact);
-          adc_conv8<40>(lo, hi, k, w, P, 40, exact);
-          adc_conv8<48>(lo, hi, k, w, P, 48, exact);
-          adc_conv8<56>(lo, hi, k, w, P, 56, exact);
+          tmem_wait_ld();
+          tmem_ld16(tb + 64, alo);
+          tmem_ld16(tb + 192, ahi);
+#ifdef XBS_STUB_EPI
+          if (blo[0] == 0xdeadbeef && bhi[15] == 0x12345) P[1] += w;
+#else
+          adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, w, P, 16, exact);
+#endif
+          tmem_wait_ld();
+          // negative polarity
+          tmem_ld16(tb + 64 + 16, blo);
+          tmem_ld16(tb + 192 + 16, bhi);
+#ifdef XBS_STUB_EPI
+          if (alo[0] == 0xdeadbeef && ahi[15] == 0x12345) P[2] += w;
+#else
+          adc_conv8<0, 16, kCPW, 16>(alo, ahi, k, -w, P, 0, exact);
+#endif
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          if (c + 1 < npair) {
+            mbar_wait_hint(&t_full[ab], abph);
+            tc_fence_after();
+            tmem_ld16(tl + ab * 256, alo);
+            tmem_ld16(tl + ab * 256 + 128, ahi);
+          }
+#ifdef XBS_STUB_EPI
+          if (blo[0] == 0xdeadbeef && bhi[15] == 0x12345) P[3] += w;
+#else
+          adc_conv8<0, 16, kCPW, 16>(blo, bhi, k, -w, P, 16, exact);
+#endif
+          tmem_wait_ld();
         }
       }
-#endif
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
       // (exact in int32: host-checked bound); per 16 columns, lane q ends
       // with the totals of columns q * (16 / TPi) + i

@@ -4,7 +4,7 @@
 // demand) — DESIGN.md §"Data layout in HBM":
 //   master  u[s][i][j]        fp64, S x Kp x Np, row-major (j fastest)
 //   digits  D[s][p][tr][tc][d][r][c]  u8 radix-255 digits of the snapped
-//           conductance q = (d0 + 255 d1) + 65025 (d2 + 255 d3); each digit
+//           conductance q = (d0 + 255 d1) + 65025 d2; each digit
 //           plane is an R x C row-major tile (R, C = tile dims rounded up to
 //           128; the internal pad holds 0 and never conducts)
 //   A_fwd   [dh][b*TPi + k][KI] u8 {0,1} (dh=0) / {0,255} (dh=1) input
@@ -25,8 +25,10 @@
 
 namespace xbs {
 
-// Snapped exactness grid (radix-255 variant): q <= kQMax.
-constexpr double kQMax = 4228250624.0;  // 65025^2 - 1
+// Snapped exactness grid (radix-255 variant): q <= kQMax,
+// three u8 digits (tensor-core limbs) per conductance.
+constexpr int kLimbs = 3;
+constexpr double kQMax = 16581374.0;  // 255^3 - 1
 
 // Rows of the forward / backward bit-plane operands, padded to whole
 // 256-row MMA unit pairs (rows beyond M*TP are zero).
@@ -45,9 +47,9 @@ struct Geo {
   int Te = 0, TPe = 0;              // error_bits, padded
   __host__ __device__ size_t plane_bytes() const { return size_t(R) * C; }
   __host__ __device__ size_t tile_digit_offset(int s, int p, int tr, int tc, int d) const {
-    return ((((size_t(s) * 2 + p) * GR + tr) * GC + tc) * 4 + d) * plane_bytes();
+    return ((((size_t(s) * 2 + p) * GR + tr) * GC + tc) * kLimbs + d) * plane_bytes();
   }
-  __host__ __device__ size_t digits_bytes() const { return size_t(S) * 2 * GR * GC * 4 * plane_bytes(); }
+  __host__ __device__ size_t digits_bytes() const { return size_t(S) * 2 * GR * GC * kLimbs * plane_bytes(); }
 };
 
 // Conversion / regeneration parameters (mapping.cpp:28-58, aam.cpp:5-31).

@@ -90,16 +90,15 @@ __device__ __forceinline__ void store_digits(uint8_t* digits, const Geo& g, int 
   const size_t off = size_t(r) * g.C + c;
   digits[g.tile_digit_offset(s, p, tr, tc, 0) + off] = uint8_t(lo % 255u);
   digits[g.tile_digit_offset(s, p, tr, tc, 1) + off] = uint8_t(lo / 255u);
-  digits[g.tile_digit_offset(s, p, tr, tc, 2) + off] = uint8_t(hi % 255u);
-  digits[g.tile_digit_offset(s, p, tr, tc, 3) + off] = uint8_t(hi / 255u);
+  digits[g.tile_digit_offset(s, p, tr, tc, 2) + off] = uint8_t(hi);
 }
 
 __device__ __forceinline__ uint32_t load_q(const uint8_t* digits, const Geo& g, int s, int p, int tr, int tc,
                                            int r, int c) {
   const size_t off = size_t(r) * g.C + c;
   const size_t base = g.tile_digit_offset(s, p, tr, tc, 0) + off, ps = g.plane_bytes();
-  const uint32_t d0 = digits[base], d1 = digits[base + ps], d2 = digits[base + 2 * ps], d3 = digits[base + 3 * ps];
-  return (d0 + 255u * d1) + 65025u * (d2 + 255u * d3);
+  const uint32_t d0 = digits[base], d1 = digits[base + ps], d2 = digits[base + 2 * ps];
+  return (d0 + 255u * d1) + 65025u * d2;
 }
 
 // -------------------------------------------------------------- map_weights
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
 #pragma unroll
     for (int jj = 0; jj < JPT; ++jj) rrow[jj] = rp.r_source + double(c0 + jj + 1) * rp.r_row;
     const size_t plane = g.plane_bytes();
-    const size_t sp_stride = size_t(g.GR) * g.GC * 4 * plane;
+    const size_t sp_stride = size_t(g.GR) * g.GC * kLimbs * plane;
     const size_t sstride = size_t(g.Kp) * g.Np;
     for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < g.K; i += gridDim.y * blockDim.y) {
       const int tr = i / g.tile_rows, r = i - tr * g.tile_rows;
@@ -296,7 +295,7 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
           qi[3] = reinterpret_cast<const uint4&>(t).w;
         }
       }
-      uint8_t* dbase = digits + (size_t(tr) * g.GC + tc) * 4 * plane + size_t(r) * g.C + c0;
+      uint8_t* dbase = digits + (size_t(tr) * g.GC + tc) * kLimbs * plane + size_t(r) * g.C + c0;
 #pragma unroll
       for (int s = S - 1; s >= 0; --s) {  // Horner order: most significant slice first
         const int qs = (S - 1 - s) % PRE;  // position within the current group
@@ -351,18 +350,17 @@ __global__ void __launch_bounds__(256) k_update(Geo g, RegenP rp, UpdP up, const
         if constexpr (!CONV) continue;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          typename VecT<JPT>::B w[4] = {0, 0, 0, 0};
+          typename VecT<JPT>::B w[kLimbs] = {0, 0, 0};
 #pragma unroll
           for (int jj = 0; jj < JPT; ++jj) {
             const uint32_t lo = q[p][jj] % 65025u, hi = q[p][jj] / 65025u;
             w[0] |= typename VecT<JPT>::B((lo % 255u) << (8 * jj));
             w[1] |= typename VecT<JPT>::B((lo / 255u) << (8 * jj));
-            w[2] |= typename VecT<JPT>::B((hi % 255u) << (8 * jj));
-            w[3] |= typename VecT<JPT>::B((hi / 255u) << (8 * jj));
+            w[2] |= typename VecT<JPT>::B(hi << (8 * jj));
           }
           uint8_t* d = dbase + (size_t(s) * 2 + p) * sp_stride;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) *reinterpret_cast<typename VecT<JPT>::B*>(d + k * plane) = w[k];
+          for (int k = 0; k < kLimbs; ++k) *reinterpret_cast<typename VecT<JPT>::B*>(d + k * plane) = w[k];
         }
       }
 #pragma unroll

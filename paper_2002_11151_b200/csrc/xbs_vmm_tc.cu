@@ -116,27 +116,29 @@ AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab) {
 // K2 backward (layers.cpp:339-379) on CTA pairs (cta_group::2).  Unit =
 // (two 128-row blocks of error bit-plane rows [(b * TPe + k) * 2 + phase], one
 // per CTA of the pair; 64 device rows of one crossbar row tile).  For each
-// crossbar column tile tc, slice s and polarity p the leader issues one chain
-// of K = 2 x C (tile columns, bits | 255*bits) tcgen05.mma.cta_group::2.kind::i8
-// (M = 256, N = 128, K = 32) with the transposed tiles read K-major straight
-// from the same digit planes:
-//     D_p[:, acc*64 + r] = sum_c v_phi[c] * q_acc(s, p, tr, tc; r, c)
-// i.e. the products vp.gp and vm.gp (p = 0) or vp.gn and vm.gn (p = 1) of
-// the reference (phase in M).  B is split along N across the pair: the
-// leader stages the lo digit pairs (d0, d1) and the peer the hi pairs
-// (d2, d3) of both polarities.  Four 128-column TMEM accumulators let the
-// MMAs run up to three half-chains ahead of the epilogue.  The epilogue
+// crossbar column tile tc and slice s the leader issues, per 128-column
+// k-block, tcgen05.mma.cta_group::2.kind::i8 (M = 256, K = 32) with the
+// transposed tiles read K-major straight from the same digit planes, in two
+// phases into one 256-column accumulator holding both polarities:
+//     A_bits phase, N = 256: D[:, 64 p + r]       = v_phi . d0_p,
+//                            D[:, 128 + 64 p + r] = v_phi . d2_p
+//     A_255 phase,  N = 128: D[:, 64 p + r]      += 255 v_phi . d1_p
+// i.e. lo / hi of the products vp.gp and vm.gp (p = 0) or vp.gn and vm.gn
+// (p = 1) of the reference (phase in M), q = d0 + 255 d1 + 65025 d2.  B is
+// split along N across the pair: the leader stages d0 of both polarities and
+// d1_pos, the peer d2 of both polarities and d1_neg.  Two 256-column TMEM
+// accumulators let the MMAs run one (tc, s) ahead of the epilogue.  The epilogue
 // converts every product through the ADC and accumulates +-2^(s db) * code
 // with sign +1 when phase == polarity (acc_pos) and -1 otherwise (acc_neg).
 namespace tc {
 
 namespace bw {
 constexpr int kBHalf = 64 * 128;     // one [64 rows][128 cols] digit box
-constexpr int kBStage = 4 * kBHalf;  // this CTA's digit pair acc = rank: [p][dh][64 r][128 c]
-constexpr int kTBufs = 4;            // TMEM accumulators of 128 columns (one polarity each)
+constexpr int kBStage = 3 * kBHalf;  // this CTA's boxes: two A_bits-phase boxes (pos, neg) + one A_255 box
+constexpr int kTBufs = 2;            // TMEM accumulators of 256 columns (one (tc, s), both polarities)
 template <int KB> constexpr int kAStage = 2 * KB * kPlane;  // [dh][kb]
 template <int KB> constexpr int kAStages = 2;
-template <int KB> constexpr int kBStages = KB == 1 ? 4 : 3;
+template <int KB> constexpr int kBStages = KB == 1 ? 5 : 4;
 template <int KB>
 constexpr int kSmem = kAStages<KB> * kAStage<KB> + kBStages<KB> * kBStage + 1024 + 256;
 }  // namespace bw
@@ -280,15 +282,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * kBStage);
                 const uint32_t fb = mapa(smem_u32(&b_full[bs]), 0);
                 uint8_t* dst = sB + bs * kBStage;
-                // this CTA's digit pair acc = rank; smem order [p][dh][64 r][128 c], digit d = 2*acc + dh
-#pragma unroll
-                for (int p = 0; p < 2; ++p)
-#pragma unroll
-                  for (int dh = 0; dh < 2; ++dh) {
-                    const int row =
-                        (((((s * 2 + p) * a.GR + tr) * a.GC + tc) * 4) + 2 * int(rank) + dh) * a.R + rh * 64;
-                    tma_load_2d_pair(dst + (p * 2 + dh) * kBHalf, &mapB, fb, kb * 128, row);
-                  }
+                // digit plane d of polarity p, this unit's 64 device rows
+                auto row = [&](int p, int d) {
+                  return ((((s * 2 + p) * a.GR + tr) * a.GC + tc) * kLimbs + d) * a.R + rh * 64;
+                };
+                // leader: d0_pos, d0_neg, d1_pos; peer: d2_pos, d2_neg, d1_neg
+                const int dpair = rank == 0 ? 0 : 2;
+                tma_load_2d_pair(dst, &mapB, fb, kb * 128, row(0, dpair));
+                tma_load_2d_pair(dst + kBHalf, &mapB, fb, kb * 128, row(1, dpair));
+                tma_load_2d_pair(dst + 2 * kBHalf, &mapB, fb, kb * 128, row(int(rank), 1));
               }
               __syncwarp();
               if (++bs == kBStages) { bs = 0; bph ^= 1; }
@@ -298,7 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0) {  // ------ MMA issuer (leader CTA; converged warp, one lane issues)
-      constexpr uint32_t idesc = idesc_i8(256, 128, /*b_mn_major=*/false);
+      constexpr uint32_t idesc_a = idesc_i8(256, 256, /*b_mn_major=*/false);  // A_bits phase
+      constexpr uint32_t idesc_b = idesc_i8(256, 128, /*b_mn_major=*/false);  // A_255 phase
       uint32_t as = 0, aph = 0, bs = 0, bph = 0, ab = 0, abph = 0;
       for (int u = cid; u < a.num_units; u += ncl) {
         const int tc0 = udiv<TRIM>(u, a.nbase, a.f_nbase) * a.tcs, ntc = min(a.GC, tc0 + a.tcs) - tc0;
@@ -310,43 +313,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
           for (int s = 0; s < a.S; ++s) {
-            // both polarities' accumulators, then the k-blocks of one B stage
-            mbar_wait(&t_empty[ab], abph ^ 1);
-            const uint32_t ab1 = ab + 1 == kTBufs ? 0 : ab + 1;
-            const uint32_t abph1 = ab + 1 == kTBufs ? abph ^ 1 : abph;
-            mbar_wait(&t_empty[ab1], abph1 ^ 1);
+            mbar_wait(&t_empty[ab], abph ^ 1);  // both polarities' accumulator
 #pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&b_full[bs], bph);
               tc_fence_after();
+              // B K-major SW128; the A_bits phase spans the two 64-row boxes
+              // (128 N rows per CTA, 8-row groups 1024 B apart)
               const uint64_t b0d = sdesc(smem_u32(sB + bs * kBStage), 16, 1024, 2);
               const int nks = TRIM ? min(4, (lcol - kb * 128 + 31) >> 5) : 4;  // >= 1 for kb 0
               if (elect_one()) {
+                const uint32_t td = tmem + ab * 256;
 #pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                  const uint32_t td = tmem + (p == 0 ? ab : ab1) * 128;
+                for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
-                  for (int dh = 0; dh < 2; ++dh)
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
-                      if (TRIM && ks >= nks) break;
-                      const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kPlane + 32 * ks);
-                      const uint64_t bd = sdesc_add(b0d, (p * 2 + dh) * kBHalf + 32 * ks);
+                  for (int ks = 0; ks < 4; ++ks) {
+                    if (TRIM && ks >= nks) break;
+                    const uint64_t ad = sdesc_add(a0d, (dh * KB + kb) * kPlane + 32 * ks);
+                    const uint64_t bd = sdesc_add(b0d, dh * 2 * kBHalf + 32 * ks);
 #ifndef XBS_STUB_MMA  // perf experiment hook (tools/build_variant.sh): no tensor work
-                      umma_i8_pair(td, ad, bd, idesc, (kb | dh | ks) != 0);
+                    umma_i8_pair(td, ad, bd, dh ? idesc_b : idesc_a, (kb | dh | ks) != 0);
 #else
-                      (void)ad; (void)bd; (void)td;
+                    (void)ad; (void)bd; (void)td;
 #endif
-                    }
-                  if (kb == KB - 1) umma_commit_pair(&t_full[p == 0 ? ab : ab1]);
-                }
+                  }
+                if (kb == KB - 1) umma_commit_pair(&t_full[ab]);
                 umma_commit_pair(&b_empty[bs]);
               }
               __syncwarp();
               if (++bs == kBStages) { bs = 0; bph ^= 1; }
             }
-            ab = ab1;
-            abph = abph1;
             if (++ab == kTBufs) { ab = 0; abph ^= 1; }
           }
           if (elect_one()) umma_commit_pair(&a_empty[as]);
@@ -356,8 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {  // ---------------------------------------------------- epilogue
-    // Per chain a warp converts kRows (16 or 32) device rows x 2 polarities
-    // (lo at +0, hi at +64 within each polarity's 128 columns).
+    // Per (tc, s) a warp converts kRows (16 or 32) device rows x 2 polarities
+    // (polarity p: lo at +64 p, hi at +128 + 64 p of the 256-column buffer).
     constexpr int kRows = 64 / (kEpiWarps / 4);  // output rows per epilogue warp
     const int lg = warp & 3, ch = (warp - 2) >> 2;
     const int ml = 32 * lg + lane;
@@ -395,23 +391,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float wpos = phi == 0 ? w : -w;  // polarity 0 (gp): + for the plus phase
         const float wneg = phi == 1 ? w : -w;  // polarity 1 (gn): + for the minus phase
         uint32_t lo[kRows], hi[kRows];
+        mbar_wait_hint(&t_full[ab], abph);
+        tc_fence_after();
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          mbar_wait_hint(&t_full[ab], abph);
-          tc_fence_after();
-          const uint32_t ta = tl + ab * 128;
+          const uint32_t ta = tl + ab * 256 + 64 * p;
           if (!TRIM || nvr > 0) {
 #pragma unroll
             for (int h = 0; h < kRows / 16; ++h) {
               tmem_ld16(ta + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&lo[16 * h]));
-              tmem_ld16(ta + 64 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
+              tmem_ld16(ta + 128 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&hi[16 * h]));
             }
             tmem_wait_ld();
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-          if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          if (p == 1) {  // both polarities read: the buffer goes back to the MMA issuer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+          }
           if (TRIM && nvr <= 0) continue;
           const float wp = p == 0 ? wpos : wneg;
 #ifdef XBS_STUB_EPI  // perf experiment hook: TMEM loads and barriers only

@@ -515,7 +515,8 @@ class CrossbarCore:
         return int(load_library().xbs_core_launch_count(self._h))
 
 
-@dataclasses.dataclass
+
+
 # ------------------------------------------- free functions (mapping / update)
 class TiledLayerWeights:
     """mapping::TiledLayerWeights (mapping.hpp:39-90): device-resident master.
@@ -721,6 +722,7 @@ def write_noise(dg: float, spec: "UpdateSpec", cfg: "CrossbarConfig", rng: Count
     return float(out[0])
 
 
+@dataclasses.dataclass
 class Tensor:
     """tensor.hpp:13-21"""
 

@@ -1,5 +1,6 @@
 """Generates the committed golden fixtures (tests/golden/*.npz) from the CPU
-oracle (snapped mode, the GPU's exactness contract).
+oracle (snapped mode, the GPU's exactness contract: since
+round 2 the 24-bit grid of three radix-255 limbs, q <= 255^3 - 1).
 
 The oracle itself is pinned on the reference's own known answers
 (oracle/tests/kat_oracle.cpp, restating test_nn.cpp / test_update.cpp /

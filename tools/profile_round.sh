@@ -6,7 +6,7 @@
 # 3. one --set full capture of the four per-step kernels after warm-up.
 set -u
 CFG=${1:-c2-4096}
-CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-peak"
+CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-peak --no-others"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
