@@ -419,7 +419,9 @@ def stage_work(cfg, layers, S):
         # dW: an M-deep outer product whose cost is writing K x N fp64 and
         # reading the u8 codes -- HBM-bound
         "dw": ("hbm", sum(8 * L.K * L.N + L.M * (L.K + 2 * L.N) for L in layers) / 1e9, "GB/s"),
-        "update": ("hbm", sum(L.K * L.N * (24 * S + 8) for L in layers) / 1e9, "GB/s"),
+        # fp64 master read + write, both polarities' VMM-ready digits (L bytes
+        # each), dW read once (24 S + 8 at L = 4)
+        "update": ("hbm", sum(L.K * L.N * ((16 + 2 * L_LIMBS) * S + 8) for L in layers) / 1e9, "GB/s"),
         # input / error quantisation + bit-plane emission: read fp64, write
         # codes and the two u8 plane copies (x: T_in planes; dy: 2 T_err)
         "prep_x": ("hbm", sum(L.M * L.K * (8 + 2 + 1 + 2 * 8) for L in layers) / 1e9, "GB/s"),
