@@ -580,6 +580,15 @@ def rooflines(cfg, layers, stages_ms, peak_tops, hbm, mma_only=None):
             if mma_only and mma_only.get(st):
                 mo = amount / (mma_only[st] * 1e-3)
                 roof[st].update({"mma_only_rate": mo, "frac_vs_mma_only": ach / mo})
+        if st == "update" and cfg.sigma != 0.0:
+            # sigma != 0: the kernel also streams the cached fp64 variation
+            # multipliers of both polarities (16 B per device and slice; the
+            # reference re-derives them from the counter RNG each
+            # regeneration, which costs more fp64 time on B200 than reading
+            # them -- DESIGN.md section 4)
+            moved = amount + sum(L.K * L.N * 16 * S for L in layers) / 1e9
+            roof[st].update({"bytes_moved_gb": moved, "achieved_moved": moved / (ms * 1e-3),
+                             "frac_moved": moved / (ms * 1e-3) / hbm})
     return macs, roof
 
 

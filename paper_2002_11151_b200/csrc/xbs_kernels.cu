@@ -13,9 +13,13 @@
 // reference's x86-64 code does (no contraction).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "xbs_internal.cuh"
 #include "xbs_rng.cuh"
+#include "xbs_tc_common.cuh"
 
 namespace xbs {
 
@@ -436,6 +440,318 @@ __global__ void __launch_bounds__(256) k_update_any(Geo g, RegenP rp, UpdP up, c
   }
 }
 
+// ------------------------------------------------- K3b, bulk-copy pipeline
+// Same per-weight arithmetic as k_update, restructured for HBM: a persistent
+// CTA runs one producer warp that streams "units" (rpu rows x cw columns of
+// dW, the S master slices and, sigma != 0, the 2S variation multiplier
+// planes) into a ring of shared-memory stages with cp.async.bulk (one
+// contiguous copy per array row, completion counted on the stage's full
+// mbarrier), while 8 consumer warps take one device column per thread from
+// the stage that has landed.  Loads therefore stay in flight while the fp64
+// conversion (two correctly rounded reciprocals per AAM device) runs: the
+// register-staged k_update issued the next row's loads only after the
+// current row's stores (23% warps active, 0.30-0.60 of HBM).
+namespace updp {
+constexpr int kConsumers = 256;         // one device column per consumer thread
+constexpr int kThreads = kConsumers + 32;
+constexpr int kMaxStages = 8;
+constexpr int kHdr = 2 * kMaxStages * 8;  // full[] + empty[] mbarriers
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(s_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16),
+// streamed past L2 with an evict-first policy: every byte is read once
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          s_u32(dst)),
+      "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(pol)
+      : "memory");
+}
+}  // namespace updp
+
+// AAM conversion + snap for the update kernel: q = rint(2^e / (1/gv + rpath))
+// with the reference's correctly rounded chain (aam.cpp:14-31, the 1.0 / x of
+// convert_qt).  The chain's value x_e is within 3 2^-53 x of the real
+// X = 2^e gv / (1 + gv rpath); the fast form below (one fma, one reciprocal
+// refined to ~2^-52 from MUFU.RCP64H, two products) is within 6 2^-53 X of
+// X.  With X < 2^24 the two differ by < 2^-25, so whenever the fast value is
+// farther than 2^-20 from a half-integer both round to the same integer;
+// otherwise (about 2e-6 of conversions) the exact chain decides.
+__device__ __forceinline__ uint32_t aam_snap(double gv, double rpath, double scale) {
+  const double w = __fma_rn(gv, rpath, 1.0);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(w));
+  double e = __fma_rn(-w, r, 1.0);
+  e = __fma_rn(e, e, e);
+  r = __fma_rn(r, e, r);
+  const double x = __dmul_rn(__dmul_rn(gv, scale), r);
+  const double xr = rint(x);
+  if (fabs(__dsub_rn(x, xr)) < 0.5 - 0x1p-20) return __double2uint_rn(xr);
+  return __double2uint_rn(__dmul_rn(__drcp_rn(__dadd_rn(__drcp_rn(gv), rpath)), scale));
+}
+
+struct UpdTmaP {
+  int cw_log;     // log2 of the unit width (columns), cw * rpu == 256
+  int rpu;        // rows per unit
+  int nch;        // column chunks per row block
+  int nst;        // pipeline stages
+  int nunits;     // row blocks * nch (< 2^31, host-checked)
+  tc::FDiv fd_nch, fd_tr, fd_tc;  // unit and tile decode by multiply-shift
+};
+
+template <int S, bool VAR, bool NL, bool NOISE, bool AAM, bool CONV>
+__global__ void __launch_bounds__(updp::kThreads, 2)
+    k_update_tma(Geo g, RegenP rp, UpdP up, UpdTmaP tp, const double* __restrict__ dW, double* __restrict__ master,
+                 uint8_t* __restrict__ digits, DevScalars* sc, const uint32_t* __restrict__ qmin) {
+  using namespace updp;
+  constexpr int NA = 1 + S + (VAR ? 2 * S : 0);  // double arrays per unit row: dW, master[S], varm[S][2]
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  double* stages = reinterpret_cast<double*>(smem + kHdr);
+  constexpr int kStageD = kConsumers * NA;  // doubles per stage
+  if (sc->dw_nonfinite) {  // scale_gradient throws before touching the master (update.cpp:18-19)
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&sc->err_flag, 2);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < tp.nst; ++k) {
+      bar_init(&full[k], 1);
+      bar_init(&empty[k], kConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int cw = 1 << tp.cw_log;
+  if (threadIdx.x >= kConsumers) {  // producer warp
+    if (threadIdx.x != kConsumers) return;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const size_t sstride = size_t(g.Kp) * g.Np;
+    int slot = 0;
+    uint32_t phase = 0;
+    bool wrapped = false;
+    for (int u = blockIdx.x; u < tp.nunits; u += gridDim.x) {
+      if (wrapped) bar_wait(&empty[slot], phase ^ 1);
+      const int rb = tc::fdiv(u, tp.fd_nch);
+      const int j0 = (u - rb * tp.nch) << tp.cw_log;
+      const int ncols = min(cw, g.N - j0);
+      const int i0 = rb * tp.rpu, nrows = min(tp.rpu, g.K - i0);
+      const uint32_t rbytes = uint32_t(ncols) * 8;  // N even (host-checked): a multiple of 16
+      bar_expect(&full[slot], rbytes * NA * nrows);
+      double* st = stages + size_t(slot) * kStageD;
+      for (int rr = 0; rr < nrows; ++rr) {
+        const int i = i0 + rr;
+        double* d = st + size_t(rr) * NA * cw;
+        bulk_g2s(d, dW + size_t(i) * g.N + j0, rbytes, &full[slot], pol);
+        const double* m = master + size_t(i) * g.Np + j0;
+        for (int s = 0; s < S; ++s) bulk_g2s(d + (1 + s) * cw, m + s * sstride, rbytes, &full[slot], pol);
+        if constexpr (VAR)
+          for (int sp = 0; sp < 2 * S; ++sp)
+            bulk_g2s(d + (1 + S + sp) * cw, rp.varm + sp * rp.kpnp + size_t(i) * g.Np + j0, rbytes, &full[slot],
+                     pol);
+      }
+      if (++slot == tp.nst) {
+        slot = 0;
+        phase ^= 1;
+        wrapped = true;
+      }
+    }
+    return;
+  }
+  // consumers: thread t owns column cc of unit row rr
+  const int t = threadIdx.x, rr = t >> tp.cw_log, cc = t & (cw - 1);
+  const double range = rp.range;
+  const int64_t sstride = int64_t(g.Kp) * g.Np;
+  const int64_t plane = int64_t(g.R) * g.C;
+  const int64_t sp_stride = int64_t(g.GR) * g.GC * kLimbs * plane;
+  double wmax = 0.0, dwmax = 0.0;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int u = blockIdx.x; u < tp.nunits; u += gridDim.x) {
+    const int rb = tc::fdiv(u, tp.fd_nch);
+    const int j = ((u - rb * tp.nch) << tp.cw_log) + cc;
+    const int i = rb * tp.rpu + rr;
+    bar_wait(&full[slot], phase);
+    const double* __restrict__ d = stages + slot * kStageD + rr * NA * cw + cc;
+    if (i < g.K && j < g.N) {
+      const int tr = tc::fdiv(i, tp.fd_tr), r = i - tr * g.tile_rows;
+      const int tcol = tc::fdiv(j, tp.fd_tc), c = j - tcol * g.tile_cols;
+      const double rpath = AAM ? ((rp.r_source + double(c + 1) * rp.r_row) + double(g.tile_rows - r) * rp.r_col) +
+                                     rp.r_sense
+                               : 0.0;
+      const double dw = d[0];
+      double ui[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) ui[s] = d[(1 + s) * cw];
+      dwmax = fmax(dwmax, fabs(dw));
+      const double dg = dw * up.factor;  // scale_gradient (update.cpp:16-24)
+      uint32_t qi = 0;
+      if constexpr (!VAR && CONV) qi = __ldg(qmin + r * g.tile_cols + c);
+      // slice S-1 first (Horner order); pointers step down one slice at a time
+      double* mp = master + (int64_t(S - 1) * sstride + int64_t(i) * g.Np + j);
+      uint8_t* dp = digits + (int64_t(S - 1) * 2 * sp_stride + (int64_t(tr) * g.GC + tcol) * kLimbs * plane +
+                              int64_t(r) * g.C + c);
+      double acc = 0.0;
+#pragma unroll
+      for (int s = S - 1; s >= 0; --s, mp -= sstride, dp -= 2 * sp_stride) {
+        const double u0 = ui[s];
+        double du = dg;
+        if constexpr (NL) {
+          if (dg != 0.0) {
+            const bool pos_active = u0 > 0.0 || (u0 == 0.0 && dg < 0.0);
+            const double dev_arg = pos_active ? -dg : dg;
+            const double gg = rp.g_min + fabs(u0);
+            if (gg < rp.g_min || gg > rp.g_max) atomicOr(&sc->err_flag, 1);  // update.cpp:28-29
+            const double x = dev_arg >= 0.0 ? (gg - rp.g_min) / range : (rp.g_max - gg) / range;
+            const double nl = dev_arg * exp(-up.v * x);
+            du = pos_active ? -nl : nl;
+          }
+        }
+        double noise = 0.0;
+        if constexpr (NOISE) {
+          if (dg != 0.0) {
+            const double sigma = up.gamma * sqrt(range * fabs(dg));
+            if (sigma != 0.0)
+              noise = sigma * rng_gaussian(rng_key(up.seed, up.iteration, uint64_t(s), uint64_t(int64_t(i) * g.N + j)));
+          }
+        }
+        double nu = u0 - up.lr * (du + noise);
+        nu = nu > range ? range : nu;
+        nu = nu < -range ? -range : nu;
+        *mp = nu;
+        acc = acc * double(1u << g.db) + nu;
+        if constexpr (CONV) {
+          uint32_t q[2];
+          if constexpr (VAR) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              const double up_ = p == 0 ? nu : -nu;
+              double gv = (up_ > 0.0 ? up_ : 0.0) + rp.g_min;
+              gv = fmin(gv * d[(1 + S + 2 * s + p) * cw], rp.g_max);  // mapping.cpp:39-58
+              if constexpr (AAM) q[p] = aam_snap(gv, rpath, rp.snap_scale);
+              else q[p] = __double2uint_rn(__dmul_rn(gv, rp.snap_scale));
+            }
+          } else {
+            const int pa = nu > 0.0 ? 0 : 1;
+            double gv = (nu > 0.0 ? nu : -nu) + rp.g_min;  // |nu| + g_min: the active device (nu == 0: either)
+            const uint32_t qa = AAM ? aam_snap(gv, rpath, rp.snap_scale) : __double2uint_rn(__dmul_rn(gv, rp.snap_scale));
+            q[0] = pa == 0 ? qa : qi;
+            q[1] = pa == 0 ? qi : qa;
+          }
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const uint32_t lo = q[p] % 65025u, hi = q[p] / 65025u;
+            uint8_t* o = dp + p * sp_stride;
+            o[0] = uint8_t(lo % 255u);
+            o[plane] = uint8_t(lo / 255u);
+            o[2 * plane] = uint8_t(hi);
+          }
+        }
+      }
+      wmax = fmax(wmax, fabs(up.wfactor * acc));
+    }
+    __syncwarp();
+    if ((t & 31) == 0) bar_arrive(&empty[slot]);
+    if (++slot == tp.nst) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+  wmax = warp_max(wmax);
+  dwmax = warp_max(dwmax);
+  if ((t & 31) == 0) {
+    atomic_max_pos(&sc->wmax, wmax);
+    atomic_max_pos(&sc->dwmax, dwmax);
+  }
+}
+
+template <int S>
+static bool launch_update_tma_s(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
+  const Geo& g = c->g;
+  UpdTmaP tp{};
+  int cw = 32;
+  while (cw < 256 && cw < g.N) cw *= 2;
+  tp.cw_log = __builtin_ctz(unsigned(cw));
+  tp.rpu = 256 / cw;
+  tp.nch = (g.N + cw - 1) / cw;
+  const int64_t nunits = int64_t((g.K + tp.rpu - 1) / tp.rpu) * tp.nch;
+  if (nunits >= (int64_t{1} << 31)) return false;
+  tp.nunits = int(nunits);
+  tp.fd_nch = tc::make_fdiv(uint32_t(tp.nch));
+  tp.fd_tr = tc::make_fdiv(uint32_t(g.tile_rows));
+  tp.fd_tc = tc::make_fdiv(uint32_t(g.tile_cols));
+  const bool var = !master_only && c->rp.sigma != 0.0, nl = !up.linear, noise = up.gamma != 0.0;
+  const bool aam = c->rp.aam && (c->rp.r_source + c->rp.r_row + c->rp.r_col + c->rp.r_sense) > 0.0;
+  const int na = 1 + S + (var ? 2 * S : 0);
+  const size_t stage_bytes = size_t(updp::kConsumers) * na * 8;
+  tp.nst = int(std::min<size_t>(updp::kMaxStages, std::max<size_t>(2, (100u << 10) / stage_bytes)));
+  const size_t smem = updp::kHdr + tp.nst * stage_bytes;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(tp.nunits, 2 * 148)));
+  auto go = [&](auto kern) {
+    // one attribute call per instantiation (stages never exceed 2 x 50 KB)
+    static const void* done[64];
+    static int ndone = 0;
+    bool seen = false;
+    for (int k = 0; k < ndone; ++k) seen |= done[k] == reinterpret_cast<const void*>(kern);
+    if (!seen) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(updp::kHdr + (100u << 10)));
+      if (ndone < 64) done[ndone++] = reinterpret_cast<const void*>(kern);
+    }
+    kern<<<grid, updp::kThreads, smem, st>>>(g, c->rp, up, tp, c->d_dW, c->d_master, c->d_digits, c->d_sc,
+                                             c->d_qmin);
+  };
+#define XBS_UPD(V, N, A) go(k_update_tma<S, V, N, N, A, true>)
+  if (master_only) {
+    if (!nl && !noise) go(k_update_tma<S, false, false, false, false, false>);
+    else go(k_update_tma<S, false, true, true, false, false>);
+  } else if (aam) {
+    if (!var && !nl && !noise) XBS_UPD(false, false, true);
+    else if (var && !nl && !noise) XBS_UPD(true, false, true);
+    else if (!var) XBS_UPD(false, true, true);
+    else XBS_UPD(true, true, true);
+  } else {
+    if (!var && !nl && !noise) XBS_UPD(false, false, false);
+    else if (var && !nl && !noise) XBS_UPD(true, false, false);
+    else if (!var) XBS_UPD(false, true, false);
+    else XBS_UPD(true, true, false);
+  }
+#undef XBS_UPD
+  return true;
+}
+
+// The bulk-copy kernel needs 16-byte aligned row segments: N and Np even.
+static bool launch_update_tma(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
+  if (c->g.N % 2 || c->g.Np % 2 || c->g.K == 0 || c->g.N == 0) return false;
+  switch (c->g.S) {
+    case 1: return launch_update_tma_s<1>(c, up, st, master_only);
+    case 2: return launch_update_tma_s<2>(c, up, st, master_only);
+    case 4: return launch_update_tma_s<4>(c, up, st, master_only);
+    case 8: return launch_update_tma_s<8>(c, up, st, master_only);
+    default: return false;
+  }
+}
+
 template <int S, int JPT>
 static void launch_update_s(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
   // threads per row: the row's JPT-weight groups rounded up to whole warps
@@ -480,6 +796,11 @@ static bool launch_update_j(const xbs_core* c, const UpdP& up, cudaStream_t st, 
 }
 
 void launch_update(const xbs_core* c, const UpdP& up, cudaStream_t st, bool master_only) {
+  static const bool legacy = [] {  // A/B switch for the register-staged kernel (perf experiments only)
+    const char* e = getenv("XBS_UPDATE_LEGACY");
+    return e && *e == '1';
+  }();
+  if (!legacy && launch_update_tma(c, up, st, master_only)) return;
   if (launch_update_j<4>(c, up, st, master_only)) return;
   if (launch_update_j<2>(c, up, st, master_only)) return;
   const dim3 grid((c->g.N + 255) / 256, std::min(c->g.K, 65535));
