@@ -73,6 +73,7 @@ struct FwdArgs {
   FDiv f_nbase, f_mbp, f_nnb, f_live;  // divisions of the unit decode
   int lg_tpi;                          // log2(TPi) (a power of two)
   int* acc;                 // ksplit > 1: int32 totals [N][M] (atomics), scaled by k_out in k_fwd_finalize
+  unsigned long long* acc64;  // ... int64 (two's complement) when the layer total can pass 2^31
   double k_out;
   AdcConst adc;
   double* y;
@@ -397,6 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
           const int jg = tc * a.tile_cols + cc;
           if (b < a.M && cc < a.tile_cols && jg < a.N) {
             if (a.acc) atomicAdd(&a.acc[int64_t(jg) * a.M + b], v[i]);  // split-K partial (exact)
+            else if (a.acc64) atomicAdd(&a.acc64[int64_t(jg) * a.M + b], (unsigned long long)(long long)v[i]);
             else a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
           }
         }
@@ -411,18 +413,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
 
 // Split-K: y = total * k_out (the single fp64 rounding of layers.cpp:283);
 // the partial buffer is left zero for the next call.
-__global__ void k_fwd_finalize(int64_t M, int N, double k_out, int* __restrict__ acc, double* __restrict__ y,
+template <class T>
+__global__ void k_fwd_finalize(int64_t M, int N, double k_out, T* __restrict__ acc, double* __restrict__ y,
                                int64_t ldy) {
   const int64_t n = M * N;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = t / M, b = t - j * M;
-    y[j * ldy + b] = double(acc[t]) * k_out;
+    y[j * ldy + b] = double(static_cast<long long>(acc[t])) * k_out;  // |total| < 2^53: exact
     acc[t] = 0;
   }
 }
 
 // int32 split-K buffer of at least `bytes` (kept zero between calls)
-int* acc32(xbs_core* c, size_t bytes, cudaStream_t st) {
+void* acc32(xbs_core* c, size_t bytes, cudaStream_t st) {
   if (c->acc32_bytes < bytes) {
     cudaFree(c->d_acc32);
     c->d_acc32 = nullptr;
@@ -445,11 +448,17 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   using namespace tc;
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || g.TPi > 16 || c->adc.passthrough) return false;
-  // fp32 P accumulators must stay exact: GR * maxc * sum_s 2^(s db) < 2^24
+  // Exactness bounds, per crossbar row tile a unit sums: the fp32 P
+  // accumulators hold |sum| <= tiles * maxc * sum_s 2^(s db) < 2^24, and the
+  // int32 bit-plane combine |sum_k 2^k P_k| < 2^31.  A layer with more row
+  // tiles than that is split into row-tile ranges (split-K) whose exact
+  // integer partials are added with atomics, in int64 when the layer total
+  // can pass 2^31 -- so any K stays on the tensor cores.
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
-  if (double(g.GR) * c->adc.maxc * sw >= 16777216.0) return false;
-  // int32 bit-plane combine: |sum_k 2^k P_k| < 2^31
-  if (double(g.GR) * c->adc.maxc * sw * (std::pow(2.0, g.Ti) - 1) >= 2147483648.0) return false;
+  const double per_tile = double(c->adc.maxc) * sw;
+  const int trs_cap = int(std::min(16777215.0 / per_tile, 2147483647.0 / (per_tile * (std::pow(2.0, g.Ti) - 1))));
+  if (trs_cap < 1) return false;
+  const bool wide = double(g.GR) * per_tile * (std::pow(2.0, g.Ti) - 1) >= 2147483648.0;
   const int64_t rowsF = rows_fwd(M, g.TPi);
   CUtensorMap mA, mB;
   if (!make_map_u8(&mA, c->d_Af, uint64_t(g.KI), uint64_t(2 * rowsF), 128, 128, 128)) return false;
@@ -480,15 +489,23 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   const int pairs = num_sms() / 2;
   a.ksplit = 1;
   if (2 * a.nbase <= pairs && g.GR > 1) a.ksplit = std::min(g.GR, pairs / a.nbase);
+  a.ksplit = std::max(a.ksplit, (g.GR + trs_cap - 1) / trs_cap);
   a.trs = (g.GR + a.ksplit - 1) / a.ksplit;
   a.ksplit = (g.GR + a.trs - 1) / a.trs;
+  if (int64_t(a.nbase) * a.ksplit >= (int64_t{1} << 31)) return false;
   a.num_units = a.nbase * a.ksplit;
   a.f_nbase = make_fdiv(uint32_t(a.nbase));
   a.f_mbp = make_fdiv(uint32_t(a.num_mbp));
   a.f_nnb = make_fdiv(uint32_t(a.n_nb));
   a.f_live = make_fdiv(uint32_t(a.live));
   a.acc = nullptr;
-  if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.N * 4, st))) return false;
+  a.acc64 = nullptr;
+  if (a.ksplit > 1) {
+    void* buf = acc32(c, size_t(M) * g.N * (wide ? 8 : 4), st);
+    if (!buf) return false;
+    if (wide) a.acc64 = static_cast<unsigned long long*>(buf);
+    else a.acc = static_cast<int*>(buf);
+  }
   {  // sweep the larger operand once: A (input planes) vs the conductance digits
     const double bytesA = 2.0 * double(rowsF) * g.KI, bytesB = double(g.digits_bytes()) * a.n_nb / (g.GC * (g.C / fw::kCW));
     // an operand that fits in L2 (126 MB; use half) is re-read for free
@@ -520,10 +537,11 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
     if (narrow) k_fwd_tc<2, true><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
     else k_fwd_tc<2, false><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
   }
-  if (a.acc) {
+  if (a.acc || a.acc64) {
     const int64_t n = M * g.N;
-    k_fwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * num_sms())), 256, 0, st>>>(M, g.N, a.k_out, a.acc,
-                                                                                          d_y, ldy);
+    const int fb = int(std::min<int64_t>((n + 255) / 256, 4 * num_sms()));
+    if (a.acc) k_fwd_finalize<<<fb, 256, 0, st>>>(M, g.N, a.k_out, a.acc, d_y, ldy);
+    else k_fwd_finalize<<<fb, 256, 0, st>>>(M, g.N, a.k_out, a.acc64, d_y, ldy);
     c->launches += 1;
   }
   return cudaPeekAtLastError() == cudaSuccess;

@@ -179,7 +179,7 @@ struct xbs_core {
   int KA = 0, NA = 0;
   unsigned long long* d_S64 = nullptr;  // split-batch dW: int64 partial sums [KA][NA]
   size_t S64_bytes = 0;
-  int* d_acc32 = nullptr;  // split-K VMMs of small layers: exact int32 partial totals [cols][M], kept zero
+  void* d_acc32 = nullptr;  // split-K VMMs (small or very deep / wide layers): exact int32 or int64 partial totals [cols][M], kept zero
   size_t acc32_bytes = 0;
   int64_t M_cap8 = 0;
   double* d_io_in = nullptr;   // host-API staging (M x max(K,N))

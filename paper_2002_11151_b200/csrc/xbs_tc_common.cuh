@@ -378,7 +378,7 @@ bool make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t oute
                  int swizzle_bytes = 128);
 int num_sms();
 AdcConst make_adc_const(const AdcP& a, const unsigned long long* tab);
-int* acc32(xbs_core* c, size_t bytes, cudaStream_t st);  // split-K int32 totals (xbs_fwd_tc.cu)
+void* acc32(xbs_core* c, size_t bytes, cudaStream_t st);  // split-K int32 / int64 totals (xbs_fwd_tc.cu)
 
 }  // namespace tc
 }  // namespace xbs

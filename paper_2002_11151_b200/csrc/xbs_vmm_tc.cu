@@ -154,6 +154,7 @@ struct BwdArgs {
   FDiv f_nbase, f_mbp, f_nrb, f_live;  // divisions of the unit decode
   int lg_grp;                          // log2(2 TPe) (TPe a power of two)
   int* acc;                 // ksplit > 1: int32 totals [K][M] (atomics), scaled in k_bwd_finalize
+  unsigned long long* acc64;  // ... int64 (two's complement) when the layer total can pass 2^31
   double F, vu, ifs_fac, lev_e;
   int adc_scaled;
   const DevScalars* sc;
@@ -448,6 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int ig = tr * a.tile_rows + rloc;
           if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) {
             if (a.acc) atomicAdd(&a.acc[int64_t(ig) * a.M + b], v[i]);  // split-K partial (exact)
+            else if (a.acc64) atomicAdd(&a.acc64[int64_t(ig) * a.M + b], (unsigned long long)(long long)v[i]);
             else a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
           }
         }
@@ -465,8 +467,13 @@ __global__ void k_bwd_finalize(const BwdArgs a, int64_t M, int K) {
   const int64_t n = M * K;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = t / M, b = t - i * M;
-    a.dx[i * a.ldx + b] = double(a.acc[t]) * k_out;
-    a.acc[t] = 0;
+    if (a.acc) {
+      a.dx[i * a.ldx + b] = double(a.acc[t]) * k_out;
+      a.acc[t] = 0;
+    } else {
+      a.dx[i * a.ldx + b] = double(static_cast<long long>(a.acc64[t])) * k_out;  // |total| < 2^53: exact
+      a.acc64[t] = 0;
+    }
   }
 }
 
@@ -476,10 +483,15 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   using namespace tc;
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc_b.passthrough) return false;
+  // Exactness bounds per crossbar column tile of a unit (both error-sign
+  // phases): fp32 P < 2^24, int32 (plane, phase) combine < 2^31; wider
+  // layers are split into column-tile ranges with int64 atomic totals (see
+  // launch_fwd_tc)
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
-  if (double(g.GC) * c->adc_b.maxc * sw * 2.0 >= 16777216.0) return false;
-  // int32 (plane, phase) combine: |sum| < 2^31
-  if (double(g.GC) * c->adc_b.maxc * sw * 2.0 * (std::pow(2.0, g.Te) - 1) >= 2147483648.0) return false;
+  const double per_tile = double(c->adc_b.maxc) * sw * 2.0;
+  const int tcs_cap = int(std::min(16777215.0 / per_tile, 2147483647.0 / (per_tile * (std::pow(2.0, g.Te) - 1))));
+  if (tcs_cap < 1) return false;
+  const bool wide = double(g.GC) * per_tile * (std::pow(2.0, g.Te) - 1) >= 2147483648.0;
   const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
   if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
@@ -511,15 +523,23 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   const int pairs = sm_count() / 2;
   a.ksplit = 1;
   if (2 * a.nbase <= pairs && g.GC > 1) a.ksplit = std::min(g.GC, pairs / a.nbase);
+  a.ksplit = std::max(a.ksplit, (g.GC + tcs_cap - 1) / tcs_cap);
   a.tcs = (g.GC + a.ksplit - 1) / a.ksplit;
   a.ksplit = (g.GC + a.tcs - 1) / a.tcs;
+  if (int64_t(a.nbase) * a.ksplit >= (int64_t{1} << 31)) return false;
   a.num_units = a.nbase * a.ksplit;
   a.f_nbase = make_fdiv(uint32_t(a.nbase));
   a.f_mbp = make_fdiv(uint32_t(a.num_mbp));
   a.f_nrb = make_fdiv(uint32_t(a.n_rb));
   a.f_live = make_fdiv(uint32_t(a.live));
   a.acc = nullptr;
-  if (a.ksplit > 1 && !(a.acc = acc32(c, size_t(M) * g.K * 4, st))) return false;
+  a.acc64 = nullptr;
+  if (a.ksplit > 1) {
+    void* buf = acc32(c, size_t(M) * g.K * (wide ? 8 : 4), st);
+    if (!buf) return false;
+    if (wide) a.acc64 = static_cast<unsigned long long*>(buf);
+    else a.acc = static_cast<int*>(buf);
+  }
   {  // sweep the larger operand once: A' (error planes) vs the conductance digits
     const double bytesA = 2.0 * double(rowsB) * g.NI, bytesB = double(g.digits_bytes()) / g.GR * (double(a.n_rb) / a.live);
     // an operand that fits in L2 (126 MB; use half) is re-read for free
@@ -557,7 +577,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
     if (trim) k_bwd_tc<2, true><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
     else k_bwd_tc<2, false><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
   }
-  if (a.acc) {
+  if (a.acc || a.acc64) {
     const int64_t n = M * g.K;
     k_bwd_finalize<<<int(std::min<int64_t>((n + 255) / 256, 4 * sm_count())), 256, 0, st>>>(a, M, g.K);
     c->launches += 1;
