@@ -71,6 +71,9 @@ def lib():
                                          ctypes.c_int, _D, ctypes.POINTER(ctypes.c_int)]
         L.orc_conv2d_backward.argtypes = [ctypes.c_void_p, _D, ctypes.c_long, ctypes.c_long, _D]
         L.orc_conv2d_apply_updates.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        L.orc_softmax_ce.argtypes = [_D, ctypes.c_long, ctypes.c_long, ctypes.POINTER(ctypes.c_int), ctypes.c_long, _D, _D]
+        L.orc_relu.argtypes = [_D, ctypes.c_long, ctypes.c_long, _D, _D, _D]
+        L.orc_maxpool2d.argtypes = [_D, ctypes.c_long] + [ctypes.c_int] * 5 + [_D, _D, _D]
     return _lib
 
 
@@ -255,3 +258,33 @@ def rng_gaussian(seed, a, b=0, c=0):
 def calibrate(samples, pct=0.999):
     s = np.ascontiguousarray(samples, dtype=np.float64)
     return lib().orc_calibrate(_p(s), s.size, pct)
+
+
+# ---------------------------------------------------------------- step glue
+def softmax_cross_entropy(logits, labels):
+    """train.cpp:11-33 restated in the oracle: (mean loss, dlogits)."""
+    lg = _f(logits)
+    n, c = lg.shape
+    lab = (ctypes.c_int * max(1, len(labels)))(*[int(v) for v in labels])
+    d = np.zeros((n, c), order="F")
+    loss = ctypes.c_double()
+    _check(lib().orc_softmax_ce(_p(lg), n, c, lab, len(labels), _p(d), ctypes.byref(loss)))
+    return loss.value, np.ascontiguousarray(d)
+
+
+def relu(x, dy):
+    """layers.cpp:510-522: forward of x and backward of dy through its mask."""
+    xf, dyf = _f(x), _f(dy)
+    y, dx = np.zeros(xf.shape, order="F"), np.zeros(dyf.shape, order="F")
+    _check(lib().orc_relu(_p(xf), xf.shape[0], xf.shape[1], _p(dyf), _p(y), _p(dx)))
+    return np.ascontiguousarray(y), np.ascontiguousarray(dx)
+
+
+def maxpool2d(x, c, h, w, kernel, stride, dy):
+    """layers.cpp:524-575: (y, dx) of a MaxPool2d over (c, h, w) rows."""
+    xf, dyf = _f(x), _f(dy)
+    oh, ow = (h - kernel) // stride + 1, (w - kernel) // stride + 1
+    y = np.zeros((xf.shape[0], c * oh * ow), order="F")
+    dx = np.zeros(xf.shape, order="F")
+    _check(lib().orc_maxpool2d(_p(xf), xf.shape[0], c, h, w, kernel, stride, _p(dyf), _p(y), _p(dx)))
+    return np.ascontiguousarray(y), np.ascontiguousarray(dx)

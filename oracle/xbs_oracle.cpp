@@ -822,9 +822,8 @@ Matrix apply_distortion(DistortionCache& cache, const Matrix& ideal) {
   return gn;
 }
 
-// layers.cpp:90-127 (ideal, aam, fcm, interp_fcm; the oracle engine only in
-// its zero-parasitic identity case layers.cpp:105-107 -- the nodal solve is
-// §8f row 4), then the snapped-mode grid.
+// layers.cpp:90-127 (ideal, aam, fcm, interp_fcm, and the oracle engine
+// through the nodal solve, §8f row 4: CPU-only), then the snapped-mode grid.
 Matrix CrossbarCore::convert_tile(const Matrix& tile, int slice, int pol, int tile_index) {
   const CrossbarConfig& cfg = weights_.tile_config();
   FcmOptions fo;
@@ -843,12 +842,20 @@ Matrix CrossbarCore::convert_tile(const Matrix& tile, int slice, int pol, int ti
       g = apply_distortion(cache, tile);
       break;
     }
-    case EngineKind::oracle:
+    case EngineKind::oracle: {  // layers.cpp:104-117: effective g from the nodal solve at v_fs
       if (zero_par) {
         g = tile;
         break;
       }
-      throw ConfigError("oracle: the nodal-oracle engine with parasitics is out of scope (SURVEY.md 8f-4)");
+      const NodalSolution sol = solve_nodal_oracle(cfg, tile, std::vector<double>(size_t(cfg.rows), cfg.v_fs));
+      g = Matrix(cfg.rows, cfg.cols);
+      for (int j = 0; j < cfg.cols; ++j)
+        for (int i = 0; i < cfg.rows; ++i) {
+          const double eff = tile(i, j) * (sol.v_top(i, j) - sol.v_bot(i, j)) / cfg.v_fs;
+          g(i, j) = std::min(std::max(eff, 0.0), tile(i, j));
+        }
+      break;
+    }
   }
   if (opt_.snapped)
     for (double& x : g.v) x = snap_conductance(x, snap_e_);
@@ -1263,6 +1270,60 @@ double softmax_cross_entropy(const Matrix& logits, const std::vector<int>& label
     }
   }
   return total / double(n);
+}
+
+// layers.cpp:510-522
+Matrix relu_forward(const Matrix& x, Matrix& mask) {
+  mask = Matrix(x.rows, x.cols);
+  Matrix y(x.rows, x.cols);
+  for (size_t k = 0; k < x.v.size(); ++k) {
+    mask.v[k] = x.v[k] > 0.0 ? 1.0 : 0.0;
+    y.v[k] = x.v[k] * mask.v[k];
+  }
+  return y;
+}
+Matrix relu_backward(const Matrix& dy, const Matrix& mask) {
+  Matrix dx(dy.rows, dy.cols);
+  for (size_t k = 0; k < dy.v.size(); ++k) dx.v[k] = dy.v[k] * mask.v[k];
+  return dx;
+}
+
+// layers.cpp:524-563
+Matrix maxpool2d_forward(const Matrix& x, int c, int h, int w, int kernel, int stride, std::vector<int>& arg) {
+  if (kernel < 1 || stride < 1) throw std::invalid_argument("MaxPool2d: bad kernel/stride");
+  const int oh = (h - kernel) / stride + 1, ow = (w - kernel) / stride + 1;
+  const long batch = x.rows;
+  Matrix y(batch, long(c) * oh * ow);
+  arg.assign(size_t(batch * c * oh * ow), 0);
+  for (long b = 0; b < batch; ++b)
+    for (int ch = 0; ch < c; ++ch)
+      for (int oy = 0; oy < oh; ++oy)
+        for (int ox = 0; ox < ow; ++ox) {
+          double best = -std::numeric_limits<double>::infinity();
+          int best_idx = 0;
+          for (int ky = 0; ky < kernel; ++ky)
+            for (int kx = 0; kx < kernel; ++kx) {
+              const int idx = (ch * h + oy * stride + ky) * w + ox * stride + kx;
+              const double v = x(b, idx);
+              if (v > best) {
+                best = v;
+                best_idx = idx;
+              }
+            }
+          const long o = (long(ch) * oh + oy) * ow + ox;
+          y(b, o) = best;
+          arg[size_t(b * c * oh * ow + o)] = best_idx;
+        }
+  return y;
+}
+
+// layers.cpp:565-575
+Matrix maxpool2d_backward(const Matrix& dy, int c, int h, int w, const std::vector<int>& arg) {
+  Matrix dx(dy.rows, long(c) * h * w, 0.0);
+  const long per = dy.cols;
+  for (long b = 0; b < dy.rows; ++b)
+    for (long o = 0; o < per; ++o) dx(b, arg[size_t(b * per + o)]) += dy(b, o);
+  return dx;
 }
 
 }  // namespace orc

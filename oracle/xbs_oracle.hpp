@@ -402,5 +402,12 @@ class CrossbarConv2d {  // layers.cpp:415-505 (im2col lowering onto one core)
 
 // train.cpp:11-33
 double softmax_cross_entropy(const Matrix& logits, const std::vector<int>& labels, Matrix& dlogits);
+// layers.cpp:510-522: y = x * (x > 0), dx = dy * mask (IEEE products: -0.0 kept)
+Matrix relu_forward(const Matrix& x, Matrix& mask);
+Matrix relu_backward(const Matrix& dy, const Matrix& mask);
+// layers.cpp:524-575: (c, h, w) feature order per batch row, strict '>'
+// keeps the first maximum in (ky, kx) order; arg = input feature index
+Matrix maxpool2d_forward(const Matrix& x, int c, int h, int w, int kernel, int stride, std::vector<int>& arg);
+Matrix maxpool2d_backward(const Matrix& dy, int c, int h, int w, const std::vector<int>& arg);
 
 }  // namespace orc

@@ -299,6 +299,32 @@ int orc_aam_convert(int rows, int cols, double r_row, double r_col, double r_sou
     unwrap(orc::aam_convert(cfg, wrap(g, rows, cols)), out);
   });
 }
+// Step glue of the reference's training loop (train.cpp:11-33,
+// layers.cpp:510-575), column-major batch x features like every matrix here.
+int orc_softmax_ce(const double* logits, long n, long c, const int* labels, long nlab, double* dlogits,
+                   double* loss) {
+  return guard([&] {
+    orc::Matrix d;
+    *loss = orc::softmax_cross_entropy(wrap(logits, n, c), std::vector<int>(labels, labels + nlab), d);
+    unwrap(d, dlogits);
+  });
+}
+int orc_relu(const double* x, long n, long f, const double* dy, double* y, double* dx) {
+  return guard([&] {
+    orc::Matrix mask;
+    unwrap(orc::relu_forward(wrap(x, n, f), mask), y);
+    unwrap(orc::relu_backward(wrap(dy, n, f), mask), dx);
+  });
+}
+int orc_maxpool2d(const double* x, long n, int c, int h, int w, int kernel, int stride, const double* dy, double* y,
+                  double* dx) {
+  return guard([&] {
+    std::vector<int> arg;
+    const orc::Matrix ym = orc::maxpool2d_forward(wrap(x, n, long(c) * h * w), c, h, w, kernel, stride, arg);
+    unwrap(ym, y);
+    unwrap(orc::maxpool2d_backward(wrap(dy, n, ym.cols), c, h, w, arg), dx);
+  });
+}
 // ADC-calibrator quantile over a sample (converters.cpp:96-107) -- used to
 // pick the explicit i_fs each parity config pins.
 double orc_calibrate(const double* samples, long n, double pct) {

@@ -28,11 +28,16 @@ def _net_weights(rng):
     return k1, k2, fc
 
 
-def _gpu_step(net, x, labels, it):
+def _gpu_step(net, x, labels, it, d_ref=None):
+    """d_ref: back-propagate these dlogits (the oracle's) instead of the
+    mirror's, so the crossbar backward compares bit for bit."""
     h = xb.Tensor(x, [3, H, H])
     for layer in net:
         h = layer.forward(h, True)
     loss, d = xb.softmax_cross_entropy(h.values, labels)
+    if d_ref is not None:
+        assert np.all(np.abs(d - d_ref) <= 4 * np.spacing(np.abs(d_ref)))
+        d = d_ref
     g = xb.Tensor(d, [10])
     grads = []
     for layer in reversed(net):
@@ -44,23 +49,23 @@ def _gpu_step(net, x, labels, it):
 
 
 def _orc_step(c1, c2, fc, x, labels, it):
+    """The oracle's own restatement of the digital glue (ReLU layers.cpp:510-522,
+    softmax CE train.cpp:11-33) around the oracle crossbar layers."""
     y1, d1 = c1.forward(x, 3, H, H, True)
-    m1 = (y1 > 0.0).astype(np.float64)
-    a1 = y1 * m1
+    a1 = oracle_py.relu(y1, np.zeros_like(y1))[0]
     y2, d2 = c2.forward(a1, d1[0], d1[1], d1[2], True)
-    m2 = (y2 > 0.0).astype(np.float64)
-    a2 = y2 * m2
+    a2 = oracle_py.relu(y2, np.zeros_like(y2))[0]
     logits = fc.forward(a2, True)
-    loss, d = xb.softmax_cross_entropy(logits, labels)
+    loss, d = oracle_py.softmax_cross_entropy(logits, labels)
     g_fc = fc.backward(d)
-    g_r2 = g_fc * m2
+    g_r2 = oracle_py.relu(y2, g_fc)[1]
     g_c2 = c2.backward(g_r2)
-    g_r1 = g_c2 * m1
+    g_r1 = oracle_py.relu(y1, g_c2)[1]
     g_c1 = c1.backward(g_r1)
     for layer in (c1, c2, fc):
         layer.apply_updates(it)
     # same order as the GPU stack's reversed walk (fc, flatten, relu, conv2, relu, conv1)
-    return logits, loss, [g_fc, g_fc, g_r2, g_c2, g_r1, g_c1]
+    return logits, loss, [g_fc, g_fc, g_r2, g_c2, g_r1, g_c1], d
 
 
 def test_c3_convnet_step_matches_oracle():
@@ -75,10 +80,10 @@ def test_c3_convnet_step_matches_oracle():
     c2 = oracle_py.OracleConv2d(k2, 16, 16, 3, 2, 1, opt)
     fc = oracle_py.OracleCore(wfc, opt, snapped=True)
 
-    lg, loss_g, grads_g = _gpu_step(gpu, x, labels, 0)
-    lo, loss_o, grads_o = _orc_step(c1, c2, fc, x, labels, 0)
+    lo, loss_o, grads_o, d_o = _orc_step(c1, c2, fc, x, labels, 0)
+    lg, loss_g, grads_g = _gpu_step(gpu, x, labels, 0, d_ref=d_o)
     assert np.array_equal(lg, lo)
-    assert loss_g == loss_o
+    assert abs(loss_g - loss_o) <= 4 * np.spacing(loss_o)
     for a, b in zip(grads_g, grads_o):
         assert np.array_equal(a, b)
     assert np.array_equal(gpu[5].core().gradient(), fc.gradient())
@@ -88,8 +93,8 @@ def test_c3_convnet_step_matches_oracle():
     for layer in gpu:
         h = layer.forward(h, False)
     y1, d1 = c1.forward(x, 3, H, H, False)
-    y2, d2 = c2.forward(y1 * (y1 > 0), d1[0], d1[1], d1[2], False)
-    lo2 = fc.forward(y2 * (y2 > 0), False)
+    y2, d2 = c2.forward(oracle_py.relu(y1, np.zeros_like(y1))[0], d1[0], d1[1], d1[2], False)
+    lo2 = fc.forward(oracle_py.relu(y2, np.zeros_like(y2))[0], False)
     same = np.mean(h.values == lo2)
     assert same >= 0.9, same
     assert np.all(np.isfinite(h.values))
