@@ -85,9 +85,9 @@ __global__ void k_observe_bwd(Geo g, int64_t M, const uint8_t* __restrict__ A, c
     const int64_t b = u / g.Te;
     // readout 0: plus x pos, 1: minus x neg, 2: plus x neg, 3: minus x pos
     const int phase = ro & 1, pol = (ro == 0 || ro == 3) ? 0 : 1;
-    const uint8_t* arow = A + ((b * g.TPe + k) * 2 + phase) * g.NI + size_t(tc) * g.C;
+    const uint8_t* arow = A + ((b * g.TPe + k) * 2 + phase) * g.NB + size_t(tc) * g.C;
     unsigned long long nn = 0;
-    for (int c = 0; c < g.tile_cols; ++c)
+    for (int c = 0; c < min(g.tile_cols, g.NB - int(tc) * g.C); ++c)
       if (arow[c]) nn += q_at(digits, g, s, pol, tr, tc, r, c);
     out[base + t] = nn;
   }

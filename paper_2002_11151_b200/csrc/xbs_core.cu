@@ -171,11 +171,11 @@ void ensure_batch(xbs_core* c, int64_t M) {
   const int64_t rowsF = xbs::rows_fwd(cap, c->g.TPi);
   const int64_t rowsB = xbs::rows_bwd(cap, c->g.TPe);
   ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
-  ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NI), "cudaMalloc A_bwd");
+  ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NB), "cudaMalloc A_bwd");
   // the prep kernels never write 16-column groups that hold only tile
   // padding: those plane bytes stay the zeros written here
   ck(cudaMemsetAsync(c->d_Af, 0, size_t(2 * rowsF) * c->g.KI, c->stream), "memset A_fwd");
-  ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NI, c->stream), "memset A_bwd");
+  ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NB, c->stream), "memset A_bwd");
   ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
   ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int16_t)), "cudaMalloc ecodes");
   cudaFree(c->d_xc8);
@@ -761,6 +761,10 @@ xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K,
     g.C = ((o.tile_cols + 127) / 128) * 128;
     g.KI = g.GR * g.R;
     g.NI = g.GC * g.C;
+    // narrow layers (one 128-column tile, N <= 64): the error planes keep only
+    // the 32 / 64 columns the backward MMA's K = 32 steps can touch, so the
+    // prep writes and the tcgen05 operand loads skip the padding
+    g.NB = (g.GC == 1 && g.C == 128 && g.N <= 64) ? (g.N <= 32 ? 32 : 64) : g.NI;
     g.S = o.weight_bits / o.device_bits;
     g.db = o.device_bits;
     g.wb = o.weight_bits;

@@ -9,7 +9,8 @@
 //           128; the internal pad holds 0 and never conducts)
 //   A_fwd   [dh][b*TPi + k][KI] u8 {0,1} (dh=0) / {0,255} (dh=1) input
 //           bit-planes, feature i at column (i / tile_rows) * R + i % tile_rows
-//   A_bwd   [dh][(b*TPe + k)*2 + phi][NI] u8 error bit-planes, phi = sign
+//   A_bwd   [dh][(b*TPe + k)*2 + phi][NB] u8 error bit-planes, phi = sign
+//           (NB = NI, or 32 / 64 bytes for a single narrow column tile)
 //   xcodes  [b][i] u16 activation codes; ecodes [b][j] i16 signed error codes
 //   dW      [i][j] fp64 (row-major K x N)
 #pragma once
@@ -42,6 +43,8 @@ struct Geo {
   int Kp = 0, Np = 0;               // reference padded dims
   int R = 0, C = 0;                 // device tile dims (multiples of 128)
   int KI = 0, NI = 0;               // GR*R, GC*C
+  int NB = 0;                       // A_bwd row pitch: NI, or 32 / 64 for one 128-column tile holding
+                                    // <= 32 / <= 64 logical columns (the rest of NI is zero padding)
   int S = 0, db = 0, wb = 0;        // slices, device_bits, weight_bits
   int Ti = 0, TPi = 0;              // act_bits, padded to a power of two
   int Te = 0, TPe = 0;              // error_bits, padded

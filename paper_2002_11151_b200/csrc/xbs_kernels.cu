@@ -1129,10 +1129,10 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
       ml[q4] = a2;
       mh[q4] = a3;
     }
-    uint8_t* p0 = A + (b * g.TPe * 2) * g.NI + c0 + q * 16;
+    uint8_t* p0 = A + (b * g.TPe * 2) * g.NB + c0 + q * 16;
     for (int k = 0; k < g.TPe; ++k) {
 #pragma unroll
-      for (int phi = 0; phi < 2; ++phi, p0 += g.NI) {
+      for (int phi = 0; phi < 2; ++phi, p0 += g.NB) {
         uint32_t w0[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
           w0[q4] = (k < 8 ? lo >> k : hi >> (k - 8)) & 0x01010101u;
         }
         *reinterpret_cast<uint4*>(p0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-        *reinterpret_cast<uint4*>(p0 + rowsB * g.NI) =
+        *reinterpret_cast<uint4*>(p0 + rowsB * g.NB) =
             make_uint4(w0[0] * 255u, w0[1] * 255u, w0[2] * 255u, w0[3] * 255u);
       }
     }
@@ -1158,8 +1158,8 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
   const int64_t rowsB = rows_bwd(M, c->g.TPe);
   const int64_t pad0 = M * c->g.TPe * 2;
   if (rowsB > pad0) {
-    cudaMemsetAsync(c->d_Ab + pad0 * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
-    cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NI, 0, size_t(rowsB - pad0) * c->g.NI, st);
+    cudaMemsetAsync(c->d_Ab + pad0 * c->g.NB, 0, size_t(rowsB - pad0) * c->g.NB, st);
+    cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NB, 0, size_t(rowsB - pad0) * c->g.NB, st);
   }
   if (M == 0) return;
   const int64_t plane8 = c->M_cap8 * c->NA;
@@ -1172,7 +1172,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
   }
   const int64_t nbt = (M + kPrepTB - 1) / kPrepTB;
   for (int64_t bt0 = 0; bt0 < nbt; bt0 += 65535) {
-    const dim3 grid(unsigned(c->g.NI / kPrepTI), unsigned(std::min<int64_t>(nbt - bt0, 65535)));
+    const dim3 grid(unsigned((c->g.NB + kPrepTI - 1) / kPrepTI), unsigned(std::min<int64_t>(nbt - bt0, 65535)));
     k_prep_dy<<<grid, 256, 0, st>>>(c->g, d_dy, M, rowsB, double((1 << c->opt.error_bits) - 1), c->d_sc,
                                        c->d_ecodes, c->d_Ab, c->d_e8, plane8, c->NA, bt0);
   }
@@ -1299,10 +1299,10 @@ __global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__
           for (int s = 0; s < g.S; ++s) {
             double apos = 0.0, aneg = 0.0;
             for (int k = 0; k < g.Te; ++k) {
-              const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NI + size_t(tc) * g.C;
-              const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NI + size_t(tc) * g.C;
+              const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NB + size_t(tc) * g.C;
+              const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NB + size_t(tc) * g.C;
               int64_t pp = 0, mn = 0, pn = 0, mp = 0;
-              for (int c = 0; c < g.tile_cols; ++c) {
+              for (int c = 0; c < min(g.tile_cols, g.NB - tc * g.C); ++c) {
                 const int64_t qp = load_q(digits, g, s, 0, tr, tc, r, c), qn = load_q(digits, g, s, 1, tr, tc, r, c);
                 if (ap[c]) { pp += qp; pn += qn; }
                 if (am[c]) { mn += qn; mp += qp; }
@@ -1320,12 +1320,12 @@ __global__ void k_bwd_simt(Geo g, AdcP a, int64_t M, const uint8_t* __restrict__
     int64_t total = 0;
     if (se > 0)
       for (int k = 0; k < g.Te; ++k) {
-        const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NI;
-        const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NI;
+        const uint8_t* ap = A + ((b * g.TPe + k) * 2 + 0) * g.NB;
+        const uint8_t* am = A + ((b * g.TPe + k) * 2 + 1) * g.NB;
         for (int tc = 0; tc < g.GC; ++tc)
           for (int s = 0; s < g.S; ++s) {
             int64_t pp = 0, mn = 0, pn = 0, mp = 0;
-            for (int c = 0; c < g.tile_cols; ++c) {
+            for (int c = 0; c < min(g.tile_cols, g.NB - tc * g.C); ++c) {
               const int64_t qp = load_q(digits, g, s, 0, tr, tc, r, c), qn = load_q(digits, g, s, 1, tr, tc, r, c);
               if (ap[tc * g.C + c]) { pp += qp; pn += qn; }
               if (am[tc * g.C + c]) { mn += qn; mp += qp; }

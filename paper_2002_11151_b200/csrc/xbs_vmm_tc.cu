@@ -153,6 +153,8 @@ struct BwdArgs {
   int nbase, ksplit, tcs;   // split-K (small layers): crossbar column tiles [sp * tcs, +tcs) per unit
   FDiv f_nbase, f_mbp, f_nrb, f_live;  // divisions of the unit decode
   int lg_grp;                          // log2(2 TPe) (TPe a power of two)
+  int abox;                            // bytes of one A box: 128 rows x min(NB, 128) (K-major)
+  uint32_t a_sbo, a_layout;            // its UMMA descriptor: 8-row stride, swizzle (SW128 / SW64 / SW32)
   int* acc;                 // ksplit > 1: int32 totals [K][M] (atomics), scaled in k_bwd_finalize
   unsigned long long* acc64;  // ... int64 (two's complement) when the layer total can pass 2^31
   double F, vu, ifs_fac, lev_e;
@@ -264,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int tc = tc0; tc < tc1; ++tc) {
           mbar_wait(&a_empty[as], aph ^ 1);
           if (elect_one()) {
-            if (rank == 0) mbar_expect_tx(&a_full[as], 2 * kAStage);
+            if (rank == 0) mbar_expect_tx(&a_full[as], 2 * 2 * KB * a.abox);
             const uint32_t fa = mapa(smem_u32(&a_full[as]), 0);
 #pragma unroll
             for (int dh = 0; dh < 2; ++dh)
@@ -312,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int lcol = min(a.tile_cols, a.N - (tc0 + tc) * a.tile_cols);
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
-          const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, 1024, 2);
+          const uint64_t a0d = sdesc(smem_u32(sA + as * kAStage), 16, a.a_sbo, a.a_layout);
           for (int s = 0; s < a.S; ++s) {
             mbar_wait(&t_empty[ab], abph ^ 1);  // both polarities' accumulator
 #pragma unroll
@@ -494,7 +496,13 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   const bool wide = double(g.GC) * per_tile * (std::pow(2.0, g.Te) - 1) >= 2147483648.0;
   const int64_t rowsB = rows_bwd(M, g.TPe);
   CUtensorMap mA, mB;
-  if (!make_map(&mA, c->d_Ab, uint64_t(g.NI), uint64_t(2 * rowsB), 128, 128)) return false;
+  // A: K-major error planes, row pitch NB; narrow layers load 32 / 64-byte
+  // boxes with the matching swizzle (the K = 32 steps never pass N)
+  const int awid = std::min(g.NB, 128);
+  if (!make_map(&mA, c->d_Ab, uint64_t(g.NB), uint64_t(2 * rowsB), uint32_t(awid), 128,
+                awid == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : awid == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                            : CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 64)) return false;
   const int KB = g.C / 128;
   BwdArgs a{};
@@ -503,6 +511,9 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.S = g.S;
   a.db = g.db;
   a.TPe = g.TPe;
+  a.abox = 128 * awid;
+  a.a_sbo = uint32_t(8 * awid);                                // 8 rows of awid bytes
+  a.a_layout = awid == 32 ? 6u : awid == 64 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B
   a.lg_grp = 1;
   while ((1 << a.lg_grp) < 2 * g.TPe) ++a.lg_grp;
   a.tile_rows = g.tile_rows;
@@ -541,7 +552,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
     else a.acc = static_cast<int*>(buf);
   }
   {  // sweep the larger operand once: A' (error planes) vs the conductance digits
-    const double bytesA = 2.0 * double(rowsB) * g.NI, bytesB = double(g.digits_bytes()) / g.GR * (double(a.n_rb) / a.live);
+    const double bytesA = 2.0 * double(rowsB) * g.NB, bytesB = double(g.digits_bytes()) / g.GR * (double(a.n_rb) / a.live);
     // an operand that fits in L2 (126 MB; use half) is re-read for free
     const double l2 = 64.0 * 1024 * 1024;
     const double costM = (bytesA <= l2 ? bytesA : bytesA * a.n_rb) + bytesB;  // M-blocks fastest
