@@ -102,7 +102,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
@@ -125,7 +125,7 @@ class ClockSampler:
         self.proc.terminate()
         self.proc.wait()
         self.f.close()
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, plim, reasons = [], [], None, None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [s.strip() for s in line.split(",")]
@@ -136,12 +136,29 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pw.append(float("nan"))
+            try:
+                plim = float(parts[8])
+            except (ValueError, IndexError):
+                pass
             for n, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        # "under load" = samples drawing at least half the window's peak power
+        # (an idle SM sits at its max clock, so the clock alone cannot tell)
+        pmax = max((p for p in pw if p == p), default=0.0)
+        idx = [i for i, p in enumerate(pw) if pmax > 0 and p == p and p >= 0.5 * pmax] or list(range(len(sm)))
+        loaded = [sm[i] for i in idx]
+        out = {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm), "loaded_samples": len(loaded)}
+        if pmax > 0:
+            out["power_w"] = statistics.median([pw[i] for i in idx])
+        if plim:
+            out["power_limit_w"] = plim
+        return out
 
 
 # ------------------------------------------------------------ int8 peak
