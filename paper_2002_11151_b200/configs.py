@@ -19,6 +19,70 @@ import numpy as np
 from .xbarsim import CrossbarLayerOptions, EngineKind
 
 
+# ------------------------------------------------------------ synthetic data
+# every tensor is drawn on the host with the reference's own
+# counter RNG (rng.hpp:12-48), keyed (seed, tensor id, linear row-major
+# element index): key = mix(mix(mix(mix(0x9e3779b97f4a7c15 ^ seed, id),
+# index), 0), 0), draw n = mix(key, n), uniform = (x >> 11) 2^-53, gaussian =
+# sqrt(-2 ln(1 - u_1)) cos(2 pi u_2) (Box-Muller on draws 1 and 2).  Seeds
+# per config c: data 1000 + c, weights 2000 + c, errors 3000 + c; the
+# tensor id is the layer index.  Vectorised over uint64 arrays (wrapping
+# arithmetic), in chunks to bound host memory.
+_GOLD = np.uint64(0x9E3779B97F4A7C15)
+_M1, _M2 = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+
+
+def _mix(h, v):
+    h = h + _GOLD + v
+    if not isinstance(h, np.ndarray):
+        h = (h ^ (h >> np.uint64(30))) * _M1
+        h = (h ^ (h >> np.uint64(27))) * _M2
+        return h ^ (h >> np.uint64(31))
+    t = np.empty_like(h)  # in place over the chunk: no per-step temporaries
+    for sh, mul in ((30, _M1), (27, _M2)):
+        np.right_shift(h, np.uint64(sh), out=t)
+        np.bitwise_xor(h, t, out=h)
+        np.multiply(h, mul, out=h)
+    np.right_shift(h, np.uint64(31), out=t)
+    np.bitwise_xor(h, t, out=h)
+    return h
+
+
+def _keys(seed: int, tensor_id: int, idx: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        h0 = _mix(np.uint64(0x9E3779B97F4A7C15) ^ np.uint64(seed), np.uint64(tensor_id))
+        return _mix(_mix(_mix(h0, idx), np.uint64(0)), np.uint64(0))
+
+
+def _unit(x: np.ndarray) -> np.ndarray:
+    return (x >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def _counter_fill(seed: int, tensor_id: int, shape, fn) -> np.ndarray:
+    n = int(np.prod(shape))
+    out = np.empty(n, dtype=np.float64)
+    step = 1 << 22
+    with np.errstate(over="ignore"):
+        for a in range(0, n, step):
+            key = _keys(seed, tensor_id, np.arange(a, min(n, a + step), dtype=np.uint64))
+            out[a:a + len(key)] = fn(key)
+    return out.reshape(shape)
+
+
+def counter_uniform(seed: int, tensor_id: int, shape, lo: float, hi: float) -> np.ndarray:
+    """lo + (hi - lo) * CounterRng(seed, tensor_id, index).uniform()"""
+    return _counter_fill(seed, tensor_id, shape, lambda k: lo + (hi - lo) * _unit(_mix(k, np.uint64(1))))
+
+
+def counter_normal(seed: int, tensor_id: int, shape, mean: float, sd: float) -> np.ndarray:
+    """mean + sd * CounterRng(seed, tensor_id, index).gaussian()"""
+    def g(k):
+        u1 = 1.0 - _unit(_mix(k.copy(), np.uint64(1)))
+        u2 = _unit(_mix(k, np.uint64(2)))
+        return mean + sd * (np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586476925287 * u2))
+    return _counter_fill(seed, tensor_id, shape, g)
+
+
 @dataclasses.dataclass
 class Conv:
     """Convolution behind an im2col layer (CrossbarConv2d, layers.cpp:415-505):
@@ -81,24 +145,21 @@ class Config:
         return o
 
     def weights(self, layer: Layer, idx: int = 0) -> np.ndarray:
-        rng = np.random.default_rng(2000 + 100 * self.cid + idx)
-        if self.w_dist == "kaiming":
-            return rng.normal(0.0, np.sqrt(2.0 / layer.K), (layer.K, layer.N))
-        return rng.normal(0.0, float(self.w_dist[1:]), (layer.K, layer.N))
+        sd = np.sqrt(2.0 / layer.K) if self.w_dist == "kaiming" else float(self.w_dist[1:])
+        return counter_normal(2000 + self.cid, idx, (layer.K, layer.N), 0.0, sd)
 
-    def _draw(self, dist: str, shape, seed: int) -> np.ndarray:
-        rng = np.random.default_rng(seed)
+    def _draw(self, dist: str, shape, seed: int, idx: int) -> np.ndarray:
         if dist == "u01":
-            return rng.uniform(0.0, 1.0, shape)
+            return counter_uniform(seed, idx, shape, 0.0, 1.0)
         if dist == "u-11":
-            return rng.uniform(-1.0, 1.0, shape)
-        return rng.normal(0.0, 1.0, shape)
+            return counter_uniform(seed, idx, shape, -1.0, 1.0)
+        return counter_normal(seed, idx, shape, 0.0, 1.0)
 
     def inputs(self, layer: Layer, idx: int = 0) -> np.ndarray:
-        return self._draw(self.x_dist, (layer.M, layer.K), 1000 + 100 * self.cid + idx)
+        return self._draw(self.x_dist, (layer.M, layer.K), 1000 + self.cid, idx)
 
     def errors(self, layer: Layer, idx: int = 0) -> np.ndarray:
-        return self._draw(self.dy_dist, (layer.M, layer.N), 3000 + 100 * self.cid + idx)
+        return self._draw(self.dy_dist, (layer.M, layer.N), 3000 + self.cid, idx)
 
     def macs(self, layer: Layer, T_in: int = 8, T_err: int = 8) -> dict:
         """Algorithmic work per step: logical, unpadded."""

@@ -28,3 +28,27 @@ def test_python_counter_rng_matches_oracle():
         got = [r._next() for _ in range(6)]
         assert [int(v) for v in ref] == got
         assert xb.CounterRng(*key).gaussian() == oracle_py.rng_gaussian(*key)
+
+
+def test_config_data_is_the_reference_counter_rng():
+    """configs.py draws every synthetic tensor with the reference's
+    CounterRng (rng.hpp:12-48) keyed (seed, tensor id, element index)
+    (SURVEY.md §8d); pinned against the oracle's C++ restatement: uniforms
+    bit for bit, Gaussians within 2 ulp (numpy vs glibc log / cos)."""
+    import numpy as np
+    import oracle_py
+    from paper_2002_11151_b200.configs import CONFIGS, counter_normal, counter_uniform
+
+    u = counter_uniform(1005, 0, (3, 7), -1.0, 1.0)
+    for idx in range(21):
+        x = int(oracle_py.rng_draws(1005, 0, idx, 0, 1)[0])
+        assert u.flat[idx] == -1.0 + 2.0 * ((x >> 11) * 2.0 ** -53)
+    g = counter_normal(2005, 1, (4, 5), 0.0, 0.02)
+    for idx in range(20):
+        ref = 0.0 + 0.02 * oracle_py.rng_gaussian(2005, 1, idx, 0)
+        assert abs(g.flat[idx] - ref) <= 2 * np.spacing(abs(ref))
+    cfg = CONFIGS["c1"]
+    L = cfg.layers[0]
+    x = cfg.inputs(L)
+    assert x.shape == (L.M, L.K) and 0.0 <= x.min() and x.max() < 1.0
+    assert abs(x.mean() - 0.5) < 0.01
