@@ -339,18 +339,75 @@ def run_conv(args, cfg):
             stages[k] = stages.get(k, 0.0) + t / args.steps
             core_ms += t / args.steps
     clk = clocks.stop()
+    for c in cores:
+        c.profile(False)
     macs = 0
     for L in cfg.layers:
         macs += cfg.macs(L)["total"]
+    e2e = None
+    if not args.no_e2e:
+        # the same step through the host-pointer C ABI (xbs_conv2d_forward /
+        # _backward, xbs_core_forward / _backward for the fc): every layer's
+        # images / errors copied in from pinned host memory and its outputs /
+        # input gradients copied out, inside the timed region
+        def pinned(rows, cols):  # F-ordered (rows x cols) numpy view of pinned memory
+            return torch.empty((cols, rows), dtype=torch.float64, pin_memory=True).numpy().T
+
+        hb, bi, bo = [], 0, 0
+        for m, (L, batch, x, dy, y, dx) in zip(mods, bufs):
+            hx, hdy = pinned(batch, x.shape[0]), pinned(batch, dy.shape[0])
+            hy, hdx = pinned(batch, y.shape[0]), pinned(batch, dx.shape[0])
+            hx[:] = x.cpu().numpy().T
+            hdy[:] = dy.cpu().numpy().T
+            hb.append((hx, hdy, hy, hdx))
+            bi += 8 * batch * (x.shape[0] + dy.shape[0])
+            bo += 8 * batch * (y.shape[0] + dx.shape[0])
+
+        def host_step():
+            for m, (L, batch, x, dy, y, dx), (hx, hdy, hy, hdx) in zip(mods, bufs, hb):
+                if L.conv is not None:
+                    m.forward(xb.Tensor(hx, [L.conv.in_c, L.conv.h, L.conv.w]), True, out=hy)
+                else:
+                    m.forward(hx, True, out=hy)
+            for m, (L, batch, x, dy, y, dx), (hx, hdy, hy, hdx) in reversed(list(zip(mods, bufs, hb))):
+                if L.conv is not None:
+                    m.backward(xb.Tensor(hdy, [hdy.shape[1]]), out=hdx)
+                else:
+                    m.backward(hdy, 1.0, out=hdx)
+            for m in mods:
+                m.apply_updates(it[0])
+            it[0] += 1
+
+        for _ in range(max(3, args.warmup)):
+            host_step()
+        for c in cores:
+            c.synchronize()
+        barrier(world)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        f0.record(stream)
+        for _ in range(args.steps):
+            host_step()
+        f1.record(stream)
+        f1.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps
+        e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps, world, "cuda")
+        e2e = {"value": world * macs / (e_ms * 1e-3), "unit": "MAC/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": e_ms, "wall_ms_per_step": max_over_ranks(wall * 1e3, world, "cuda"),
+               "path": "xbs_conv2d_forward/backward + xbs_core_forward/backward (fc), apply_updates "
+                       "(host pointers, pinned): images, not patch matrices, cross PCIe"}
     if rank == 0:
-        print(json.dumps({
+        line = {
             "metric": METRIC, "value": world * macs / (ms * 1e-3), "unit": "MAC/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic N(0,1) images and errors",
             "config": {"workload": cfg.name.replace("-im2col", "") + "-conv",
                        "lowering": "CrossbarConv2d: device im2col / col2im around one core per layer",
                        "layers": [[L.name, L.M, L.K, L.N] for L in cfg.layers], "parallelism": f"replicas{world}"},
-            "stage_ms": stages, "core_ms": core_ms, "glue_ms": ms - core_ms, "clocks": clk}))
+            "stage_ms": stages, "core_ms": core_ms, "glue_ms": ms - core_ms, "clocks": clk}
+        if e2e:
+            line["e2e"] = e2e
+        print(json.dumps(line))
     for c in cores[1:]:  # the first core owns the shared stream: detach before teardown
         c.set_stream(None)
     torch.cuda.synchronize()

@@ -798,7 +798,9 @@ class CrossbarConv2d(Layer):
             _lib.xbs_conv2d_destroy(h)
             self._h = None
 
-    def forward(self, x: Tensor, training: bool) -> Tensor:
+    def forward(self, x: Tensor, training: bool, out: Optional[np.ndarray] = None) -> Tensor:
+        """out: optional F-ordered (batch x out_c*oh*ow) float64 array to
+        write into (e.g. pinned host memory, as CrossbarCore.forward)."""
         if len(x.dims) != 3 or x.dims[0] != self.in_c:
             raise ValueError("CrossbarConv2d: expected (c, h, w) input")
         c, hh, ww = x.dims
@@ -806,17 +808,23 @@ class CrossbarConv2d(Layer):
         _check(load_library().xbs_conv2d_output_dims(self._h, hh, ww, ctypes.byref(oh), ctypes.byref(ow)))
         v = _fortran(x.values)
         b = v.shape[0]
-        y = np.zeros((b, self.out_c * oh.value * ow.value), order="F")
+        shape = (b, self.out_c * oh.value * ow.value)
+        if out is not None and (out.shape != shape or out.dtype != np.float64 or not out.flags.f_contiguous):
+            raise ValueError("CrossbarConv2d.forward: out must be an F-ordered float64 array of shape %s" % (shape,))
+        y = out if out is not None else np.zeros(shape, order="F")
         _check(load_library().xbs_conv2d_forward(self._h, _ptr(v), b, c, hh, ww, max(1, b), int(bool(training)), _ptr(y),
                                                  max(1, b)))
         self._in_dims = list(x.dims)
         return Tensor(y, [self.out_c, oh.value, ow.value])
 
-    def backward(self, dy: Tensor) -> Tensor:
+    def backward(self, dy: Tensor, out: Optional[np.ndarray] = None) -> Tensor:
         v = _fortran(dy.values)
         b = v.shape[0]
         c, hh, ww = self._in_dims if self._in_dims else (self.in_c, 0, 0)
-        dx = np.zeros((b, c * hh * ww), order="F")
+        shape = (b, c * hh * ww)
+        if out is not None and (out.shape != shape or out.dtype != np.float64 or not out.flags.f_contiguous):
+            raise ValueError("CrossbarConv2d.backward: out must be an F-ordered float64 array of shape %s" % (shape,))
+        dx = out if out is not None else np.zeros(shape, order="F")
         _check(load_library().xbs_conv2d_backward(self._h, _ptr(v), b, max(1, b), _ptr(dx), max(1, b)))
         return Tensor(dx, [c, hh, ww])
 
