@@ -126,6 +126,13 @@ void validate_options(const xbs_layer_options& o, const std::vector<double>& dac
   if (o.threads < 1) fail(XBS_CONFIG_ERROR, "threads must be >= 1");
 }
 
+// Converters off the tensor-core contract (1-bit DAC streams at a power-of-
+// two full scale, linear ADC of <= 16 bits): multi-bit DAC streams, DAC / ADC
+// transfer tables, wider ADCs, other DAC full scales.
+bool volts_mode(const xbs_layer_options& o, const std::vector<double>& dac_tr, const std::vector<double>& adc_tr) {
+  return !dac_tr.empty() || !adc_tr.empty() || o.adc_bits > 16 || o.dac_bits != 1 || !is_pow2_double(o.dac_v_fs);
+}
+
 // Path scope: valid reference configurations this
 // B200 path does not evaluate are refused loudly, never approximated.
 void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, const std::vector<double>& adc_tr) {
@@ -139,11 +146,13 @@ void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, 
     if (o.fcm_max_iter < 1) fail(XBS_INVALID_ARGUMENT, "fcm_convert: max_iter must be >= 1");
   }
   if (o.engine < 0 || o.engine > 4) fail(XBS_INVALID_ARGUMENT, "unknown engine");
-  if (!adc_tr.empty()) fail(XBS_UNSUPPORTED, "ADC transfer tables are not on this path");
-  if (!dac_tr.empty()) fail(XBS_UNSUPPORTED, "DAC transfer tables are not on this path");
-  if (o.adc_bits > 16) fail(XBS_UNSUPPORTED, "adc.bits > 16 is not on this path");
-  if (o.dac_bits != 1) fail(XBS_UNSUPPORTED, "only the 1-bit DAC stream is on this path");
-  if (!is_pow2_double(o.dac_v_fs)) fail(XBS_UNSUPPORTED, "dac.v_fs must be a power of two (exact currents)");
+  // general converters run the exact fp64 CUDA-core VMMs (volts mode);
+  // their ADC must have an explicit full scale or a threshold table
+  if (volts_mode(o, dac_tr, adc_tr)) {
+    if (o.dac_bits > 16) fail(XBS_UNSUPPORTED, "DAC streams wider than 16 bits are not on this path");
+    if (o.adc_bits > 0 && !(o.adc_i_fs > 0) && adc_tr.empty())
+      fail(XBS_UNSUPPORTED, "ADC auto-calibration with multi-bit / table converters is not on this path");
+  }
   if (o.act_bits > 16 || o.error_bits > 16) fail(XBS_UNSUPPORTED, "act_bits / error_bits > 16 are not on this path");
   if (o.tile_rows > 256 || o.tile_cols > 256) fail(XBS_UNSUPPORTED, "tiles larger than 256 x 256 are not on this path");
 }
@@ -444,6 +453,8 @@ void enqueue_fwd_vmm(xbs_core* c, int64_t M, const Out& out) {
   bool direct = false;
   if (c->fully_ideal) {
     xbs::launch_fwd_ideal(c, M, stage, c->stream);
+  } else if (c->volts_mode) {
+    xbs::launch_fwd_volts(c, M, stage, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
     if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;  // shape outside the tcgen05 kernel's exact bounds
     xbs::launch_fwd_simt(c, M, stage, c->stream);
@@ -457,6 +468,8 @@ void enqueue_bwd_vmm(xbs_core* c, const double* d_dy, int64_t M, const Out& out)
   bool direct = false;
   if (c->fully_ideal) {
     xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
+  } else if (c->volts_mode) {
+    xbs::launch_bwd_volts(c, M, stage, c->stream);
   } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
     if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;
     xbs::launch_bwd_simt(c, M, stage, c->stream);
@@ -818,7 +831,7 @@ xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K,
 
     xbs::AdcP& a = c->adc;
     a.passthrough = o.adc_bits == 0 || c->adc_auto;  // calibration batches pass currents through
-    a.maxc = o.adc_bits > 0 ? int((1u << o.adc_bits) - 1) : 0;
+    a.maxc = o.adc_bits > 0 && o.adc_bits <= 16 ? int((1u << o.adc_bits) - 1) : 0;
     a.maxc_d = double(a.maxc);
     a.i_fs = o.adc_i_fs;
     int lv;
@@ -843,7 +856,29 @@ xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K,
       cudaFree(d_W);
       return c.release();
     }
-    if (!a.passthrough) {
+    c->volts_mode = volts_mode(o, c->dac_tr, c->adc_tr);
+    if (c->volts_mode) {
+      // dac_encode of every digit (converters.cpp:28-35) and the ADC spec
+      const uint64_t levels = (uint64_t{1} << o.dac_bits) - 1;
+      std::vector<double> lut(size_t(levels) + 1);
+      for (uint64_t d = 0; d <= levels; ++d)
+        lut[d] = !c->dac_tr.empty() ? c->dac_tr[d] : d == 0 ? 0.0 : double(d) / double(levels) * o.dac_v_fs;
+      ck(cudaMalloc(&c->d_dac_lut, lut.size() * 8), "cudaMalloc dac lut");
+      ck(cudaMemcpy(c->d_dac_lut, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice), "H2D dac lut");
+      if (!c->adc_tr.empty()) {
+        ck(cudaMalloc(&c->d_adc_tr, c->adc_tr.size() * 8), "cudaMalloc adc table");
+        ck(cudaMemcpy(c->d_adc_tr, c->adc_tr.data(), c->adc_tr.size() * 8, cudaMemcpyHostToDevice), "H2D adc table");
+      }
+      xbs::VoltsP& v = c->volts;
+      v.lut = c->d_dac_lut;
+      v.sb = o.dac_stream_bits;
+      v.passthrough = o.adc_bits == 0;
+      v.adc_tr = c->d_adc_tr;
+      v.tr_len = int(c->adc_tr.size());
+      v.maxcode = o.adc_bits > 0 ? (uint64_t{1} << o.adc_bits) - 1 : 0;
+      v.maxc_d = double(v.maxcode);
+      v.i_fs = o.adc_i_fs;
+    } else if (!a.passthrough) {
       set_adc(c.get(), 0, o.adc_i_fs);
       set_adc(c.get(), 1, o.adc_i_fs);
     }
@@ -950,6 +985,8 @@ void xbs_core_destroy(xbs_core* c) {
   xbs::calib_release(c);
   cudaFree(c->d_obs_count);
   cudaFree(c->d_qmin);
+  cudaFree(c->d_dac_lut);
+  cudaFree(c->d_adc_tr);
   cudaFree(c->d_varm);
   cudaFree(c->d_fcm_scratch);
   cudaFree(c->d_cache_d);

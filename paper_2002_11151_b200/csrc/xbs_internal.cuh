@@ -87,6 +87,18 @@ struct AdcP {
   double maxc_d;
 };
 
+// General converters (multi-bit DAC streams, DAC / ADC transfer tables, ADC
+// above 16 bits, non-power-of-two DAC full scale): exact fp64 CUDA-core path.
+struct VoltsP {
+  const double* lut;            // dac_encode of every digit (converters.cpp:28-35), device
+  int sb;                       // dac.stream_bits
+  int passthrough;              // adc.bits == 0
+  const double* adc_tr;         // ADC thresholds (converters.cpp:76-82), device, or null
+  int tr_len;
+  unsigned long long maxcode;   // 2^bits - 1 (bits <= 32)
+  double maxc_d, i_fs;
+};
+
 // Device scalars (one struct per core, in HBM).
 struct DevScalars {
   double se;                 // max|dy|
@@ -119,6 +131,10 @@ struct xbs_core {
   xbs::RegenP rp{};
   xbs::AdcP adc{};    // forward ADC (adc_fwd_)
   xbs::AdcP adc_b{};  // backward ADC (adc_bwd_); differs from adc only after auto-calibration
+  bool volts_mode = false;  // general converters: exact fp64 CUDA-core VMMs (k_fwd_volts / k_bwd_volts)
+  xbs::VoltsP volts{};
+  double* d_dac_lut = nullptr;
+  double* d_adc_tr = nullptr;
   xbs::FcmP fcm{};
   bool tile_engine = false;     // fcm / interp_fcm with parasitics: per-tile regeneration kernels
   uint64_t update_count = 0;    // layers.cpp:389 (interp refresh schedule)
@@ -239,6 +255,8 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
 void core_forward_conv(xbs_core* c, const double* d_img, const ConvSrc& cs, bool training, double* d_y);
 void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream_t st);
 void launch_fwd_simt(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
+void launch_fwd_volts(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
+void launch_bwd_volts(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
 void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st);
 void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st);
 void launch_bwd_ideal(const xbs_core* c, const double* d_dy, int64_t M, double* d_dx, cudaStream_t st);

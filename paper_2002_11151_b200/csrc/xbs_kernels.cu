@@ -1201,6 +1201,141 @@ void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t s
   k_dw<<<blocks, 256, 0, st>>>(c->g, M, c->sx, c->lev_e, grad_divisor, c->d_xcodes, c->d_ecodes, c->d_sc, c->d_dW);
 }
 
+// ------------------------------------------------------ general converters
+// Multi-bit DAC streams, DAC / ADC transfer tables, ADC resolutions above 16
+// bits and non-power-of-two DAC full scales (layers.cpp:52-64, 236-241,
+// 316-331; converters.cpp:28-35, 70-88): the column currents are no longer
+// integers on the snapped grid, so these layers run exact CUDA-core kernels
+// that follow the reference's fp64 expression order term by term -- I =
+// sum over ascending crossbar rows (columns, backward) of volts(digit) * g
+// on the snapped conductances, the ADC as adc_quantize, then the same
+// accumulation order as layers.cpp:246-283 / 340-378 -- so the outputs are
+// bit-identical to the oracle's restatement.  No tensor-core path exists for
+// them (the radix-255 operands need 1-bit digits and power-of-two volts).
+__device__ __forceinline__ double adc_volts(const VoltsP& v, double I) {
+  if (v.passthrough) return I;
+  if (v.tr_len > 0) {  // converters.cpp:76-82: highest threshold not exceeding I
+    int lo = 0, hi = v.tr_len;  // first index with transfer[idx] > I
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v.adc_tr[mid] > I) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo == 0) return 0.0;
+    const unsigned long long code = (unsigned long long)(lo - 1);
+    return double(code < v.maxcode ? code : v.maxcode);
+  }
+  const double scaled = __dmul_rn(__ddiv_rn(I, v.i_fs), v.maxc_d);  // converters.cpp:85-87
+  if (scaled >= v.maxc_d) return v.maxc_d;
+  return double(llround(scaled));
+}
+
+__device__ __forceinline__ double g_snapped(const Geo& g, const uint8_t* digits, int e, int s, int p, int tr, int tc,
+                                            int r, int c) {
+  return ldexp(double(load_q(digits, g, s, p, tr, tc, r, c)), -e);  // exact: q 2^-e
+}
+
+__global__ void k_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint16_t* __restrict__ xc,
+                            const uint8_t* __restrict__ digits, double k_out, double* __restrict__ y) {
+  const int64_t n = M * g.N;
+  const int nx = g.Ti / v.sb, mask = (1 << v.sb) - 1;
+  const double stream_base = double(1 << v.sb);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int col = int(t / M);
+    const int tc = col / g.tile_cols, c = col % g.tile_cols;
+    double out = 0.0;
+    for (int tr = 0; tr < g.GR; ++tr) {
+      const int rows = min(g.tile_rows, g.K - tr * g.tile_rows);  // padded rows carry volts(0) = 0
+      double tile = 0.0;
+      for (int s = 0; s < g.S; ++s) {
+        const double sw = ldexp(1.0, s * g.db);  // pow(2^db, s)
+        for (int p = 0; p < 2; ++p) {
+          double acc = 0.0, wk = 1.0;
+          for (int k = 0; k < nx; ++k) {
+            double I = 0.0;
+            for (int r = 0; r < rows; ++r) {
+              const int d = (int(xc[b * g.K + tr * g.tile_rows + r]) >> (k * v.sb)) & mask;
+              if (d) I = __dadd_rn(I, __dmul_rn(v.lut[d], g_snapped(g, digits, e, s, p, tr, tc, r, c)));
+            }
+            acc = __dadd_rn(acc, __dmul_rn(wk, adc_volts(v, I)));
+            wk = __dmul_rn(wk, stream_base);
+          }
+          tile = __dadd_rn(tile, __dmul_rn(p == 0 ? sw : -sw, acc));
+        }
+      }
+      out = __dadd_rn(out, tile);
+    }
+    y[int64_t(col) * M + b] = __dmul_rn(out, k_out);
+  }
+}
+
+__global__ void k_bwd_volts(Geo g, VoltsP v, int e, int64_t M, const int16_t* __restrict__ ec,
+                            const uint8_t* __restrict__ digits, double F, double vu, double ifs_fac, int adc_scaled,
+                            double lev_e, const DevScalars* __restrict__ sc, double* __restrict__ dx) {
+  const double se = sc->se;
+  const double step_e = se > 0 ? se / lev_e : 0.0;
+  double k_out = step_e * F / vu;  // layers.cpp:375-377
+  if (adc_scaled) k_out *= ifs_fac;
+  const int64_t n = M * g.K;
+  const int ne = g.Te / v.sb, mask = (1 << v.sb) - 1;
+  const double stream_base = double(1 << v.sb);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = t % M;
+    const int i = int(t / M);
+    const int tr = i / g.tile_rows, r = i % g.tile_rows;
+    double acc_dx = 0.0;
+    if (se > 0)
+      for (int tc = 0; tc < g.GC; ++tc) {
+        const int cols = min(g.tile_cols, g.N - tc * g.tile_cols);
+        double tile = 0.0;
+        for (int s = 0; s < g.S; ++s) {
+          const double sw = ldexp(1.0, s * g.db);
+          double ap = 0.0, an = 0.0, wk = 1.0;
+          for (int k = 0; k < ne; ++k) {
+            double Ipp = 0.0, Imn = 0.0, Ipn = 0.0, Imp = 0.0;  // (vp, gp) (vm, gn) (vp, gn) (vm, gp)
+            for (int c = 0; c < cols; ++c) {
+              const int code = ec[b * g.N + tc * g.tile_cols + c];
+              const int dp = ((code > 0 ? code : 0) >> (k * v.sb)) & mask;
+              const int dm = ((code < 0 ? -code : 0) >> (k * v.sb)) & mask;
+              if (dp) {
+                const double vp = v.lut[dp];
+                Ipp = __dadd_rn(Ipp, __dmul_rn(vp, g_snapped(g, digits, e, s, 0, tr, tc, r, c)));
+                Ipn = __dadd_rn(Ipn, __dmul_rn(vp, g_snapped(g, digits, e, s, 1, tr, tc, r, c)));
+              }
+              if (dm) {
+                const double vm = v.lut[dm];
+                Imn = __dadd_rn(Imn, __dmul_rn(vm, g_snapped(g, digits, e, s, 1, tr, tc, r, c)));
+                Imp = __dadd_rn(Imp, __dmul_rn(vm, g_snapped(g, digits, e, s, 0, tr, tc, r, c)));
+              }
+            }
+            ap = __dadd_rn(ap, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipp), adc_volts(v, Imn))));
+            an = __dadd_rn(an, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipn), adc_volts(v, Imp))));
+            wk = __dmul_rn(wk, stream_base);
+          }
+          tile = __dadd_rn(tile, __dmul_rn(sw, __dsub_rn(ap, an)));
+        }
+        acc_dx = __dadd_rn(acc_dx, tile);
+      }
+    dx[int64_t(i) * M + b] = __dmul_rn(acc_dx, k_out);
+  }
+}
+
+void launch_fwd_volts(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st) {
+  const int64_t n = M * c->g.N;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  k_fwd_volts<<<blocks, 128, 0, st>>>(c->g, c->volts, c->rp.snap_e, M, c->d_xcodes, c->d_digits, c->k_out_fwd, d_y);
+}
+
+void launch_bwd_volts(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
+  const int64_t n = M * c->g.K;
+  if (n == 0) return;
+  const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
+  k_bwd_volts<<<blocks, 128, 0, st>>>(c->g, c->volts, c->rp.snap_e, M, c->d_ecodes, c->d_digits, c->F, c->vu,
+                                      c->ifs_fac_b, c->adc_scaled ? 1 : 0, c->lev_e, c->d_sc, d_dx);
+}
+
 // --------------------------------------------------------------- SIMT VMM
 __device__ __forceinline__ int64_t adc_apply(const AdcP& a, int64_t n, unsigned long long* conv) {
   if (a.passthrough) return n;

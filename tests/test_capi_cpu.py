@@ -82,7 +82,9 @@ def test_nonfinite_and_empty_weights_rejected():
     "mutate",
     [
         lambda o: setattr(o, "engine", xb.EngineKind.oracle),  # dense nodal solve with parasitics (8f-4)
-        lambda o: setattr(o.adc, "transfer", [0.0, 1e-6, 2e-6, 3e-6]),
+        # auto-calibration with a multi-bit DAC stream (the general-converter
+        # path needs an explicit full scale or a threshold table)
+        lambda o: (setattr(o.dac, "bits", 2), setattr(o.dac, "stream_bits", 2), setattr(o.adc, "i_fs", 0.0)),
     ],
 )
 def test_out_of_scope_configs_fail_loudly(mutate):
