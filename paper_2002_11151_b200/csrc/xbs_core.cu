@@ -186,7 +186,7 @@ void ensure_batch(xbs_core* c, int64_t M) {
   ck(cudaMemsetAsync(c->d_Af, 0, size_t(2 * rowsF) * c->g.KI, c->stream), "memset A_fwd");
   ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NB, c->stream), "memset A_bwd");
   ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
-  ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int16_t)), "cudaMalloc ecodes");
+  ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int32_t)), "cudaMalloc ecodes");
   cudaFree(c->d_xc8);
   cudaFree(c->d_e8);
   c->d_xc8 = c->d_e8 = nullptr;

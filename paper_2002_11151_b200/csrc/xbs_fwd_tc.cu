@@ -74,6 +74,7 @@ struct FwdArgs {
   int lg_tpi;                          // log2(TPi) (a power of two)
   int* acc;                 // ksplit > 1: int32 totals [N][M] (atomics), scaled by k_out in k_fwd_finalize
   unsigned long long* acc64;  // ... int64 (two's complement) when the layer total can pass 2^31
+  int wide;                   // bit-plane combine in int64 (a unit's total can pass 2^31)
   double k_out;
   AdcConst adc;
   double* y;
@@ -112,7 +113,7 @@ __device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int&
 // NARROW: some 64-column units hold fewer than 64 logical columns (N or the
 // tile width not a multiple of 64), so epilogue warps skip the conversions
 // of padded columns; full-width layers keep the plain pipelined loop.
-template <int KB, bool NARROW>
+template <int KB, bool NARROW, bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
   using namespace fw;
@@ -377,32 +378,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         }
       }
       // combine the TPi bit-plane lanes of each batch row: total = sum 2^k P_k
-      // (exact in int32: host-checked bound); per 16 columns, lane q ends
-      // with the totals of columns q * (16 / TPi) + i
+      // (exact in int32, or in int64 when the host bound says a total can
+      // pass 2^31); per 16 columns, lane q ends with the totals of columns
+      // q * (16 / TPi) + i
       const int kk = NARROW ? ml & (a.TPi - 1) : ml % a.TPi;
       const int64_t b = NARROW ? (int64_t(2 * mbp + int(rank)) * 128 + ml) >> a.lg_tpi
                                : (int64_t(2 * mbp + int(rank)) * 128 + ml) / a.TPi;
       int tc, hcol;
       col_unit<NARROW>(nb, a, tc, hcol);
       const int per = NARROW ? 16 >> a.lg_tpi : 16 / a.TPi;
+      auto emit = [&](auto zero) {
+        using T = decltype(zero);
 #pragma unroll
-      for (int h = 0; h < kCPW / 16; ++h) {
-        int v[16];
+        for (int h = 0; h < kCPW / 16; ++h) {
+          T v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[16 * h + j]) * (1 << kk);
-        group_reduce16(v, kk, a.TPi);
+          for (int j = 0; j < 16; ++j) v[j] = T(__float2int_rn(P[16 * h + j])) * (T(1) << kk);
+          group_reduce16(v, kk, a.TPi);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i >= per) break;
-          const int cc = hcol * kCW + kCPW * q + 16 * h + kk * per + i;
-          const int jg = tc * a.tile_cols + cc;
-          if (b < a.M && cc < a.tile_cols && jg < a.N) {
-            if (a.acc) atomicAdd(&a.acc[int64_t(jg) * a.M + b], v[i]);  // split-K partial (exact)
-            else if (a.acc64) atomicAdd(&a.acc64[int64_t(jg) * a.M + b], (unsigned long long)(long long)v[i]);
-            else a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
+          for (int i = 0; i < 16; ++i) {
+            if (i >= per) break;
+            const int cc = hcol * kCW + kCPW * q + 16 * h + kk * per + i;
+            const int jg = tc * a.tile_cols + cc;
+            if (b < a.M && cc < a.tile_cols && jg < a.N) {
+              if (a.acc) atomicAdd(&a.acc[int64_t(jg) * a.M + b], int(v[i]));  // split-K partial (exact)
+              else if (a.acc64) atomicAdd(&a.acc64[int64_t(jg) * a.M + b], (unsigned long long)(long long)v[i]);
+              else a.y[int64_t(jg) * a.ldy + b] = double(v[i]) * a.k_out;
+            }
           }
         }
-      }
+      };
+      if constexpr (WIDE) emit((long long)0);
+      else emit(0);
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
   }
@@ -449,14 +456,15 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || g.TPi > 16 || c->adc.passthrough) return false;
   // Exactness bounds, per crossbar row tile a unit sums: the fp32 P
-  // accumulators hold |sum| <= tiles * maxc * sum_s 2^(s db) < 2^24, and the
-  // int32 bit-plane combine |sum_k 2^k P_k| < 2^31.  A layer with more row
-  // tiles than that is split into row-tile ranges (split-K) whose exact
-  // integer partials are added with atomics, in int64 when the layer total
-  // can pass 2^31 -- so any K stays on the tensor cores.
+  // accumulators hold |sum| <= tiles * maxc * sum_s 2^(s db) < 2^24 (a
+  // layer with more row tiles is split into row-tile ranges, split-K, whose
+  // exact integer partials are added with atomics), and the bit-plane
+  // combine |sum_k 2^k P_k| runs in int32, or in int64 (with int64 totals:
+  // the WIDE instantiation) when it can pass 2^31 -- so any K and any
+  // activation width stay on the tensor cores.
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   const double per_tile = double(c->adc.maxc) * sw;
-  const int trs_cap = int(std::min(16777215.0 / per_tile, 2147483647.0 / (per_tile * (std::pow(2.0, g.Ti) - 1))));
+  const int trs_cap = int(16777215.0 / per_tile);
   if (trs_cap < 1) return false;
   const bool wide = double(g.GR) * per_tile * (std::pow(2.0, g.Ti) - 1) >= 2147483648.0;
   const int64_t rowsF = rows_fwd(M, g.TPi);
@@ -465,6 +473,7 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   if (!make_map_u8(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), fw::kCW, 128, 64))
     return false;
   FwdArgs a{};
+  a.wide = wide ? 1 : 0;
   a.GR = g.GR;
   a.GC = g.GC;
   a.S = g.S;
@@ -520,22 +529,29 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.y = d_y;
   a.ldy = ldy;
   a.ctr = &c->d_sc->exact_path;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_fwd_tc<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
-    cudaFuncSetAttribute(k_fwd_tc<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
-    cudaFuncSetAttribute(k_fwd_tc<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<1>);
-    cudaFuncSetAttribute(k_fwd_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fw::kSmem<2>);
-    attr = true;
-  }
-  const int grid = 2 * std::min(a.num_units, num_sms() / 2);  // CTA pairs
+  const int grid_ = 2 * std::min(a.num_units, num_sms() / 2);  // CTA pairs
+  auto launch = [&](auto kern, int smem) {
+    static const void* done[8];
+    static int ndone = 0;
+    bool seen = false;
+    for (int k = 0; k < ndone; ++k) seen |= done[k] == reinterpret_cast<const void*>(kern);
+    if (!seen) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (ndone < 8) done[ndone++] = reinterpret_cast<const void*>(kern);
+    }
+    kern<<<grid_, fw::kThreads, smem, st>>>(mA, mB, a);
+  };
   const bool narrow = (g.tile_cols % fw::kCW) != 0 || ((g.N - (g.GC - 1) * g.tile_cols) % fw::kCW) != 0;
-  if (g.R == 128) {
-    if (narrow) k_fwd_tc<1, true><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
-    else k_fwd_tc<1, false><<<grid, fw::kThreads, fw::kSmem<1>, st>>>(mA, mB, a);
-  } else {
-    if (narrow) k_fwd_tc<2, true><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
-    else k_fwd_tc<2, false><<<grid, fw::kThreads, fw::kSmem<2>, st>>>(mA, mB, a);
+  const int sel = (g.R == 256 ? 4 : 0) + (narrow ? 2 : 0) + (wide ? 1 : 0);
+  switch (sel) {
+    case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>); break;
+    case 1: launch(k_fwd_tc<1, false, true>, fw::kSmem<1>); break;
+    case 2: launch(k_fwd_tc<1, true, false>, fw::kSmem<1>); break;
+    case 3: launch(k_fwd_tc<1, true, true>, fw::kSmem<1>); break;
+    case 4: launch(k_fwd_tc<2, false, false>, fw::kSmem<2>); break;
+    case 5: launch(k_fwd_tc<2, false, true>, fw::kSmem<2>); break;
+    case 6: launch(k_fwd_tc<2, true, false>, fw::kSmem<2>); break;
+    default: launch(k_fwd_tc<2, true, true>, fw::kSmem<2>); break;
   }
   if (a.acc || a.acc64) {
     const int64_t n = M * g.N;

@@ -11,7 +11,7 @@
 //           bit-planes, feature i at column (i / tile_rows) * R + i % tile_rows
 //   A_bwd   [dh][(b*TPe + k)*2 + phi][NB] u8 error bit-planes, phi = sign
 //           (NB = NI, or 32 / 64 bytes for a single narrow column tile)
-//   xcodes  [b][i] u16 activation codes; ecodes [b][j] i16 signed error codes
+//   xcodes  [b][i] u16 activation codes; ecodes [b][j] i32 signed error codes
 //   dW      [i][j] fp64 (row-major K x N)
 #pragma once
 
@@ -189,7 +189,7 @@ struct xbs_core {
   uint8_t* d_Af = nullptr;   // 2 * rowsF * KI
   uint8_t* d_Ab = nullptr;   // 2 * rowsB * NI
   uint16_t* d_xcodes = nullptr;
-  int16_t* d_ecodes = nullptr;
+  int32_t* d_ecodes = nullptr;  // signed error codes: 16-bit magnitudes need more than int16
   // u8 operands of the tcgen05 dW GEMM (act/error bits <= 8): x codes
   // [Mcap8][KA], error magnitudes [plus | minus][Mcap8][NA]; K, N padded to
   // 128 (zero), batch padded to 128 (rows >= M zeroed per call)

@@ -1033,9 +1033,9 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
 // plus, phi=1 minus.  Tiled transpose as in k_prep_x.
 __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict__ dy, int64_t M, int64_t rowsB,
                                                  double levels, const DevScalars* __restrict__ sc,
-                                                 int16_t* __restrict__ ecodes, uint8_t* __restrict__ A,
+                                                 int32_t* __restrict__ ecodes, uint8_t* __restrict__ A,
                                                  uint8_t* __restrict__ e8, int64_t plane8, int ld8, int64_t bt0) {
-  __shared__ int16_t cs[kPrepTB][kPrepTI + 2];
+  __shared__ int32_t cs[kPrepTB][kPrepTI + 1];
   const double se = sc->se;
   const double step = se / levels;
   const double inv = 1.0 / step;
@@ -1062,7 +1062,7 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
       const int mag = int(quant_mag(fabs(v), step, inv, levels));
       sm = mag == 0 ? 0 : (v < 0 ? -mag : mag);
     }
-    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = int16_t(sm);
+    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = sm;
   }
   __syncthreads();
   // signed codes [b][N] and the u8 plus / minus dW magnitudes, 8 columns per thread
@@ -1071,11 +1071,9 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
     const int o = e % (kPrepTI / 8) * 8, r = e / (kPrepTI / 8);
     const int64_t b = b0 + r;
     if (b >= M || o >= nlive) continue;
-    const int16_t* src = &cs[r][o];
+    const int32_t* src = &cs[r][o];
     if (vec && o + 8 <= nlive) {
-      uint32_t w[4], wp[2], wm[2];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) w[h] = uint32_t(uint16_t(src[2 * h])) | (uint32_t(uint16_t(src[2 * h + 1])) << 16);
+      uint32_t wp[2], wm[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint32_t a = 0, m = 0;
@@ -1088,7 +1086,9 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
         wp[h] = a;
         wm[h] = m;
       }
-      *reinterpret_cast<uint4*>(ecodes + b * g.N + j0 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+      int4* eo = reinterpret_cast<int4*>(ecodes + b * g.N + j0 + o);
+      eo[0] = make_int4(src[0], src[1], src[2], src[3]);
+      eo[1] = make_int4(src[4], src[5], src[6], src[7]);
       if (e8) {
         *reinterpret_cast<uint2*>(e8 + b * ld8 + j0 + o) = make_uint2(wp[0], wp[1]);
         *reinterpret_cast<uint2*>(e8 + plane8 + b * ld8 + j0 + o) = make_uint2(wm[0], wm[1]);
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
     } else {
       for (int t = 0; t < 8 && o + t < nlive; ++t) {
         const int sm = src[t];
-        ecodes[b * g.N + j0 + o + t] = int16_t(sm);
+        ecodes[b * g.N + j0 + o + t] = sm;
         if (e8) {
           e8[b * ld8 + j0 + o + t] = uint8_t(sm > 0 ? sm : 0);
           e8[plane8 + b * ld8 + j0 + o + t] = uint8_t(sm < 0 ? -sm : 0);
@@ -1181,7 +1181,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
 // ---------------------------------------------------------------------- dW
 // Exact integer outer product: dW = ((S * sx) * step_e) / gd.
 __global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const uint16_t* __restrict__ xc,
-                     const int16_t* __restrict__ ec, DevScalars* __restrict__ sc, double* __restrict__ dW) {
+                     const int32_t* __restrict__ ec, DevScalars* __restrict__ sc, double* __restrict__ dW) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
   const int64_t n = int64_t(g.K) * g.N;
@@ -1270,7 +1270,7 @@ __global__ void k_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint16_t* _
   }
 }
 
-__global__ void k_bwd_volts(Geo g, VoltsP v, int e, int64_t M, const int16_t* __restrict__ ec,
+__global__ void k_bwd_volts(Geo g, VoltsP v, int e, int64_t M, const int32_t* __restrict__ ec,
                             const uint8_t* __restrict__ digits, double F, double vu, double ifs_fac, int adc_scaled,
                             double lev_e, const DevScalars* __restrict__ sc, double* __restrict__ dx) {
   const double se = sc->se;
@@ -1504,7 +1504,7 @@ void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st
 }
 
 // dx = dy_q * wimp^T (layers.cpp:307), dy_q = (sign*mag)*step_e (layers.cpp:301-302)
-__global__ void k_bwd_ideal(Geo g, int64_t M, double lev_e, const int16_t* __restrict__ ec,
+__global__ void k_bwd_ideal(Geo g, int64_t M, double lev_e, const int32_t* __restrict__ ec,
                             const DevScalars* __restrict__ sc, const double* __restrict__ w, double* __restrict__ dx) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;

@@ -344,31 +344,32 @@ __device__ __forceinline__ void adc_conv8(const uint32_t (&lo)[NL], const uint32
 // after log2(G) steps lane q (= lane % G) holds the totals of rows
 // q * (16 / G) + i (G <= 16; for G = 32, lanes q and q ^ 1 share row q >> 1).
 // 15 shuffles for 16 rows instead of 16 x log2(G) for a full butterfly.
-template <int O, int N>
-__device__ __forceinline__ void tr_step(int (&v)[16], int q) {
+template <int O, int N, class T>
+__device__ __forceinline__ void tr_step(T (&v)[16], int q) {
   if constexpr (O >= 1) {
     if constexpr (N > 1) {
       const bool up = (q & O) != 0;
 #pragma unroll
       for (int i = 0; i < N / 2; ++i) {
-        const int a = v[i], b = v[i + N / 2];
-        const int keep = up ? b : a;
+        const T a = v[i], b = v[i + N / 2];
+        const T keep = up ? b : a;
         v[i] = keep + __shfl_xor_sync(0xffffffffu, up ? a : b, O);
       }
-      tr_step<O / 2, N / 2>(v, q);
+      tr_step<O / 2, N / 2, T>(v, q);
     } else {
       v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
-      tr_step<O / 2, 1>(v, q);
+      tr_step<O / 2, 1, T>(v, q);
     }
   }
 }
-__device__ __forceinline__ void group_reduce16(int (&v)[16], int q, int G) {
+template <class T>  // int, or long long where a combined total can pass 2^31
+__device__ __forceinline__ void group_reduce16(T (&v)[16], int q, int G) {
   switch (G) {
-    case 2: tr_step<1, 16>(v, q); break;
-    case 4: tr_step<2, 16>(v, q); break;
-    case 8: tr_step<4, 16>(v, q); break;
-    case 16: tr_step<8, 16>(v, q); break;
-    case 32: tr_step<16, 16>(v, q); break;
+    case 2: tr_step<1, 16, T>(v, q); break;
+    case 4: tr_step<2, 16, T>(v, q); break;
+    case 8: tr_step<4, 16, T>(v, q); break;
+    case 16: tr_step<8, 16, T>(v, q); break;
+    case 32: tr_step<16, 16, T>(v, q); break;
     default: break;  // G == 1
   }
 }

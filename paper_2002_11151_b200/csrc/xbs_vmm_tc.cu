@@ -157,6 +157,7 @@ struct BwdArgs {
   uint32_t a_sbo, a_layout;            // its UMMA descriptor: 8-row stride, swizzle (SW128 / SW64 / SW32)
   int* acc;                 // ksplit > 1: int32 totals [K][M] (atomics), scaled in k_bwd_finalize
   unsigned long long* acc64;  // ... int64 (two's complement) when the layer total can pass 2^31
+  int wide;                   // (plane, phase) combine in int64 (a unit's total can pass 2^31)
   double F, vu, ifs_fac, lev_e;
   int adc_scaled;
   const DevScalars* sc;
@@ -208,7 +209,7 @@ __device__ __forceinline__ double bwd_k_out(const BwdArgs& a) {
 // issuer skips K = 32 steps made only of padding, or padded crossbar rows
 // inside a scheduled 64-row block, whose conversions the epilogue warps
 // skip; without padding the issue and epilogue loops are the plain ones.
-template <int KB, bool TRIM>
+template <int KB, bool TRIM, bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const BwdArgs a) {
   using namespace bw;
@@ -438,24 +439,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int per = grp <= 16 ? (TRIM ? 16 >> a.lg_grp : 16 / grp) : 1;
       const int j0 = grp <= 16 ? q * per : (q >> 1);
       const bool writer = grp <= 16 || (q & 1) == 0;
+      auto emit = [&](auto zero) {
+        using T = decltype(zero);
 #pragma unroll
-      for (int h = 0; h < kRows / 16; ++h) {
-        int v[16];
+        for (int h = 0; h < kRows / 16; ++h) {
+          T v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __float2int_rn(P[16 * h + j]) * (1 << kk);
-        group_reduce16(v, q, grp);
+          for (int j = 0; j < 16; ++j) v[j] = T(__float2int_rn(P[16 * h + j])) * (T(1) << kk);
+          group_reduce16(v, q, grp);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i >= per) break;
-          const int rloc = rh * 64 + kRows * ch + 16 * h + j0 + i;
-          const int ig = tr * a.tile_rows + rloc;
-          if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) {
-            if (a.acc) atomicAdd(&a.acc[int64_t(ig) * a.M + b], v[i]);  // split-K partial (exact)
-            else if (a.acc64) atomicAdd(&a.acc64[int64_t(ig) * a.M + b], (unsigned long long)(long long)v[i]);
-            else a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
+          for (int i = 0; i < 16; ++i) {
+            if (i >= per) break;
+            const int rloc = rh * 64 + kRows * ch + 16 * h + j0 + i;
+            const int ig = tr * a.tile_rows + rloc;
+            if (writer && b < a.M && rloc < a.tile_rows && ig < a.K) {
+              if (a.acc) atomicAdd(&a.acc[int64_t(ig) * a.M + b], int(v[i]));  // split-K partial (exact)
+              else if (a.acc64) atomicAdd(&a.acc64[int64_t(ig) * a.M + b], (unsigned long long)(long long)v[i]);
+              else a.dx[int64_t(ig) * a.ldx + b] = double(v[i]) * k_out;
+            }
           }
         }
-      }
+      };
+      if constexpr (WIDE) emit((long long)0);
+      else emit(0);
     }
     if (a.ctr) atomicAdd(&a.ctr[0], (unsigned long long)exact);
   }
@@ -486,12 +492,12 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   const Geo& g = c->g;
   if ((g.R != 128 && g.R != 256) || (g.C != 128 && g.C != 256) || g.TPe > 16 || c->adc_b.passthrough) return false;
   // Exactness bounds per crossbar column tile of a unit (both error-sign
-  // phases): fp32 P < 2^24, int32 (plane, phase) combine < 2^31; wider
-  // layers are split into column-tile ranges with int64 atomic totals (see
-  // launch_fwd_tc)
+  // phases): fp32 P < 2^24 (wider layers split into column-tile ranges),
+  // (plane, phase) combine and totals in int64 where they can pass 2^31
+  // (the WIDE instantiation; see launch_fwd_tc)
   const double sw = (std::pow(2.0, g.wb) - 1) / (std::pow(2.0, g.db) - 1);
   const double per_tile = double(c->adc_b.maxc) * sw * 2.0;
-  const int tcs_cap = int(std::min(16777215.0 / per_tile, 2147483647.0 / (per_tile * (std::pow(2.0, g.Te) - 1))));
+  const int tcs_cap = int(16777215.0 / per_tile);
   if (tcs_cap < 1) return false;
   const bool wide = double(g.GC) * per_tile * (std::pow(2.0, g.Te) - 1) >= 2147483648.0;
   const int64_t rowsB = rows_bwd(M, g.TPe);
@@ -506,6 +512,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   if (!make_map(&mB, c->d_digits, uint64_t(g.C), uint64_t(g.digits_bytes() / g.C), 128, 64)) return false;
   const int KB = g.C / 128;
   BwdArgs a{};
+  a.wide = wide ? 1 : 0;
   a.GR = g.GR;
   a.GC = g.GC;
   a.S = g.S;
@@ -570,23 +577,30 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.dx = d_dx;
   a.ldx = ldx;
   a.ctr = &c->d_sc->exact_path;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bwd_tc<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<1>);
-    cudaFuncSetAttribute(k_bwd_tc<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<2>);
-    cudaFuncSetAttribute(k_bwd_tc<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<1>);
-    cudaFuncSetAttribute(k_bwd_tc<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw::kSmem<2>);
-    attr = true;
-  }
-  const int grid = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
+  const int grid_ = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
+  auto launch = [&](auto kern, int smem) {
+    static const void* done[8];
+    static int ndone = 0;
+    bool seen = false;
+    for (int k = 0; k < ndone; ++k) seen |= done[k] == reinterpret_cast<const void*>(kern);
+    if (!seen) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (ndone < 8) done[ndone++] = reinterpret_cast<const void*>(kern);
+    }
+    kern<<<grid_, kThreads, smem, st>>>(mA, mB, a);
+  };
   const bool trim = (g.N % g.tile_cols) != 0 || g.tile_cols <= g.C - 32 || (g.tile_rows % 64) != 0 ||
                     ((g.K - (g.GR - 1) * g.tile_rows) % 64) != 0;
-  if (KB == 1) {
-    if (trim) k_bwd_tc<1, true><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
-    else k_bwd_tc<1, false><<<grid, kThreads, bw::kSmem<1>, st>>>(mA, mB, a);
-  } else {
-    if (trim) k_bwd_tc<2, true><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
-    else k_bwd_tc<2, false><<<grid, kThreads, bw::kSmem<2>, st>>>(mA, mB, a);
+  const int sel = (KB == 2 ? 4 : 0) + (trim ? 2 : 0) + (wide ? 1 : 0);
+  switch (sel) {
+    case 0: launch(k_bwd_tc<1, false, false>, bw::kSmem<1>); break;
+    case 1: launch(k_bwd_tc<1, false, true>, bw::kSmem<1>); break;
+    case 2: launch(k_bwd_tc<1, true, false>, bw::kSmem<1>); break;
+    case 3: launch(k_bwd_tc<1, true, true>, bw::kSmem<1>); break;
+    case 4: launch(k_bwd_tc<2, false, false>, bw::kSmem<2>); break;
+    case 5: launch(k_bwd_tc<2, false, true>, bw::kSmem<2>); break;
+    case 6: launch(k_bwd_tc<2, true, false>, bw::kSmem<2>); break;
+    default: launch(k_bwd_tc<2, true, true>, bw::kSmem<2>); break;
   }
   if (a.acc || a.acc64) {
     const int64_t n = M * g.K;
