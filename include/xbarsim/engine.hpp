@@ -1,7 +1,7 @@
 // xbarsim/engine.hpp — EngineKind (reference engine.hpp:15).  This path
-// evaluates ideal, aam, and zero-parasitic fcm / oracle / interp_fcm (which
-// reduce to the identity); circuit solves with parasitics are out of scope
-// and rejected with ConfigError.
+// evaluates ideal, aam, fcm and interp_fcm (either base) on the GPU, and the
+// oracle engine in its zero-parasitic identity case; the dense nodal solve
+// with parasitics is CPU-only and rejected with ConfigError.
 #pragma once
 
 namespace xbarsim {
