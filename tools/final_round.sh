@@ -18,8 +18,15 @@ echo "launch list rc=$?" >> $O/ncu_launches.log
 ncu --set full --clock-control none --import-source on -k 'regex:k_fwd_tc|k_bwd_tc|k_dw_tc|k_update' \
     -s 12 -c 4 -o $O/prof_c5 -f $CMD > $O/ncu_full.log 2>&1
 echo "full rc=$?" >> $O/ncu_full.log
+ncu -i $O/prof_c5.ncu-rep --page raw --csv > $O/prof_c5_raw.csv 2>/dev/null
+for k in k_fwd_tc k_bwd_tc k_update; do python tools/ncu_stalls.py $O/prof_c5.ncu-rep $k 25 > $O/stalls_c5_$k.txt 2>&1; done
+rm -f $O/prof_c5.ncu-rep
 CMD2="python bench.py --config c2-4096 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-peak --no-others"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv $CMD2 > $O/ncu_launches2.log 2>&1
 ncu --set full --clock-control none --import-source on -k 'regex:k_fwd_tc|k_bwd_tc|k_dw_tc|k_update' \
     -s 12 -c 4 -o $O/prof_c2 -f $CMD2 > $O/ncu_full2.log 2>&1
+ncu -i $O/prof_c2.ncu-rep --page raw --csv > $O/prof_c2_raw.csv 2>/dev/null
+for k in k_fwd_tc k_bwd_tc k_update; do python tools/ncu_stalls.py $O/prof_c2.ncu-rep $k 25 > $O/stalls_c2_$k.txt 2>&1; done
+rm -f $O/prof_c2.ncu-rep
+du -sh $O
 echo done
