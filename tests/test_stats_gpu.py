@@ -104,15 +104,19 @@ def test_set_gradient_nonfinite_refused():
 
 
 def test_tc_fallback_is_counted():
-    """A shape outside the tcgen05 kernels' exact fp32 bound (16-bit weights
-    as sixteen 1-bit slices: GR * maxc * sum 2^s >= 2^24) runs the exact SIMT
-    kernel; the C ABI counts it so callers (bench.py) can refuse it."""
+    """16-bit weights as sixteen 1-bit slices with an 8-bit ADC pass the
+    one-tile fp32 bound only per crossbar tile: the forward splits the row
+    tiles (split-K) and stays on the tensor cores.  With a 16-bit ADC a single
+    tile's shift-add total (maxc * sum 2^s >= 2^24) is outside the tcgen05
+    kernels' exact fp32 accumulators, so the exact SIMT kernel runs, and the
+    C ABI counts it so callers (bench.py) can refuse it."""
     K, N, M = 300, 40, 6
-    opt = aam_options(tile=256, wb=16, db=1, adc_bits=8, i_fs=4e-4, r_row=2.5, r_col=2.5)
-    W = normal((K, N), 9, 0.05)
-    gpu = xb.CrossbarCore(W, opt)
-    orc = oracle_py.OracleCore(W, opt, snapped=True)
-    assert gpu.info().tc_fallbacks == 0
     x = rand((M, K), 4, 0.0, 1.0)
-    assert np.array_equal(gpu.forward(x, True), orc.forward(x, True))
-    assert gpu.info().tc_fallbacks >= 1
+    W = normal((K, N), 9, 0.05)
+    for adc_bits, i_fs, fallback in ((8, 4e-4, False), (16, 4e-4, True)):
+        opt = aam_options(tile=256, wb=16, db=1, adc_bits=adc_bits, i_fs=i_fs, r_row=2.5, r_col=2.5)
+        gpu = xb.CrossbarCore(W, opt)
+        orc = oracle_py.OracleCore(W, opt, snapped=True)
+        assert gpu.info().tc_fallbacks == 0
+        assert np.array_equal(gpu.forward(x, True), orc.forward(x, True))
+        assert (gpu.info().tc_fallbacks >= 1) == fallback

@@ -17,7 +17,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = {"k_fwd_tc": "fwd_vmm", "k_bwd_tc": "bwd_vmm", "k_dw_tc": "dw", "k_dw": "dw", "k_update4": "update", "k_update": "update",
+STAGE = {"k_fwd_tc": "fwd_vmm", "k_bwd_tc": "bwd_vmm", "k_dw_tc": "dw", "k_dw": "dw", "k_update4": "update", "k_update": "update", "k_update_tma": "update",
          "k_prep_x": "prep_x", "k_prep_dy": "prep_dy"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
@@ -49,7 +49,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # an .ncu-rep, or its `ncu -i REP --page raw --csv` export
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     lines = out.splitlines()
     hdr = next(csv.reader([lines[0]]))
     units = next(csv.reader([lines[1]]))
