@@ -148,6 +148,7 @@ struct BwdArgs {
   int live, live_last;  // 64-row blocks holding logical rows per row tile / in the last row tile
   int n_rb;              // scheduled row blocks
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = row blocks fastest
+  int hint;              // TMA L2 hints: digit tiles evict-last, error planes evict-first
   int64_t M, rowsB;
   int num_mbp, num_units;  // num_units = base units (M-block pair x row block) x ksplit
   int nbase, ksplit, tcs;   // split-K (small layers): crossbar column tiles [sp * tcs, +tcs) per unit
@@ -258,6 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
       for (int u = cid; u < a.num_units; u += ncl) {
         int mbp, rb, tc0, tc1;
         bwd_unit<TRIM>(u, a, mbp, rb, tc0, tc1);
@@ -272,9 +274,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int dh = 0; dh < 2; ++dh)
 #pragma unroll
-              for (int kb = 0; kb < KB; ++kb)
-                tma_load_2d_pair(sA + as * kAStage + (dh * KB + kb) * kPlane, &mapA, fa, tc * a.C + kb * 128,
-                                 int(dh * a.rowsB) + mrow);
+              for (int kb = 0; kb < KB; ++kb) {
+                uint8_t* dst = sA + as * kAStage + (dh * KB + kb) * kPlane;
+                if (a.hint) tma_load_2d_pair_hint(dst, &mapA, fa, tc * a.C + kb * 128, int(dh * a.rowsB) + mrow, pol_a);
+                else tma_load_2d_pair(dst, &mapA, fa, tc * a.C + kb * 128, int(dh * a.rowsB) + mrow);
+              }
           }
           __syncwarp();
           if (++as == kAStages) { as = 0; aph ^= 1; }
@@ -292,9 +296,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 };
                 // leader: d0_pos, d0_neg, d1_pos; peer: d2_pos, d2_neg, d1_neg
                 const int dpair = rank == 0 ? 0 : 2;
-                tma_load_2d_pair(dst, &mapB, fb, kb * 128, row(0, dpair));
-                tma_load_2d_pair(dst + kBHalf, &mapB, fb, kb * 128, row(1, dpair));
-                tma_load_2d_pair(dst + 2 * kBHalf, &mapB, fb, kb * 128, row(int(rank), 1));
+                if (a.hint) {
+                  tma_load_2d_pair_hint(dst, &mapB, fb, kb * 128, row(0, dpair), pol_b);
+                  tma_load_2d_pair_hint(dst + kBHalf, &mapB, fb, kb * 128, row(1, dpair), pol_b);
+                  tma_load_2d_pair_hint(dst + 2 * kBHalf, &mapB, fb, kb * 128, row(int(rank), 1), pol_b);
+                } else {
+                  tma_load_2d_pair(dst, &mapB, fb, kb * 128, row(0, dpair));
+                  tma_load_2d_pair(dst + kBHalf, &mapB, fb, kb * 128, row(1, dpair));
+                  tma_load_2d_pair(dst + 2 * kBHalf, &mapB, fb, kb * 128, row(int(rank), 1));
+                }
               }
               __syncwarp();
               if (++bs == kBStages) { bs = 0; bph ^= 1; }
@@ -565,6 +575,8 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
     const double costM = (bytesA <= l2 ? bytesA : bytesA * a.n_rb) + bytesB;  // M-blocks fastest
     const double costO = bytesA + (bytesB <= l2 ? bytesB : bytesB * a.num_mbp);        // other index fastest
     a.mfast = costM <= costO ? 1 : 0;
+    a.hint = a.mfast && bytesA > l2 ? 1 : 0;  // as in launch_fwd_tc (C5 backward -5.3 %)
+    if (std::getenv("XBS_NO_L2_HINTS")) a.hint = 0;  // A/B switch (perf experiments only)
   }
   a.F = c->F;
   a.vu = c->vu;
