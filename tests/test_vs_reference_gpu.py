@@ -70,7 +70,7 @@ def test_gpu_against_the_reference_code(cfg_name, layer_idx):
           f"(max rel {g_rel:.2e}); y differs in {fy} of {y_g.size} ({conv['fwd']:.3g} conversions), dx in {fx} of "
           f"{dx_g.size} ({conv['bwd']:.3g}); max |dy| {np.max(np.abs(y_g - y_r)) / kf:.1f} LSB-weights, "
           f"max |ddx| {np.max(np.abs(dx_g - dx_r)) / kb:.1f}")
-    assert g_abs <= half_step * (1 + 1e-9)
+    assert g_abs <= half_step * (1 + 1e-6)  # + libm ulps of the variation multiplier
     assert fy <= max(2, 1e-5 * conv["fwd"]) and fx <= max(2, 1e-5 * conv["bwd"])
     assert np.max(np.abs(y_g - y_r)) <= wmax * kf * (1 + 1e-9)
     assert np.max(np.abs(dx_g - dx_r)) <= 2 * wmax * kb * (1 + 1e-9)
