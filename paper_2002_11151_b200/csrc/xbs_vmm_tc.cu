@@ -390,10 +390,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float P[kRows];
 #pragma unroll
       for (int j = 0; j < kRows; ++j) P[j] = 0.f;
+      bool nchain_done = false;
       const float wstep = float(1 << a.db);
       float wmag = k.unscale;
       int s = 0;
-      for (int c = 0; c < nchain; ++c) {
+#ifdef XBS_BWD_PIPE
+      if constexpr (kRows == 16) {
+        if (!TRIM || nvr > 0) {
+          // software-pipelined TMEM reads (as in the forward epilogue): the
+          // negative polarity's 16 rows load while the positive ones are
+          // converted, and the next chain's positive rows while the negative
+          // ones are
+          uint32_t alo[16], ahi[16], blo[16], bhi[16];
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+          tmem_ld16(tl + ab * 256, alo);
+          tmem_ld16(tl + ab * 256 + 128, ahi);
+          tmem_wait_ld();
+          for (int c = 0; c < nchain; ++c) {
+            const float w = wmag;
+            if (++s == a.S) {
+              s = 0;
+              wmag = k.unscale;
+            } else {
+              wmag = __fmul_rn(wmag, wstep);
+            }
+            const float wpos = phi == 0 ? w : -w;
+            const float wneg = phi == 1 ? w : -w;
+            const uint32_t tb = tl + ab * 256;
+            tmem_ld16(tb + 64, blo);
+            tmem_ld16(tb + 192, bhi);
+#ifdef XBS_BWD_G16
+            if (!TRIM || nvr > 8) adc_conv8<0, 16, kRows, 16>(alo, ahi, k, wpos, P, 0, exact);
+            else adc_conv8<0, 16, kRows>(alo, ahi, k, wpos, P, 0, exact);
+#else
+            adc_conv8<0, 16, kRows>(alo, ahi, k, wpos, P, 0, exact);
+            if (!TRIM || nvr > 8) adc_conv8<8, 16, kRows>(alo, ahi, k, wpos, P, 8, exact);
+#endif
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+            if (c + 1 < nchain) {
+              mbar_wait_hint(&t_full[ab], abph);
+              tc_fence_after();
+              tmem_ld16(tl + ab * 256, alo);
+              tmem_ld16(tl + ab * 256 + 128, ahi);
+            }
+#ifdef XBS_BWD_G16
+            if (!TRIM || nvr > 8) adc_conv8<0, 16, kRows, 16>(blo, bhi, k, wneg, P, 0, exact);
+            else adc_conv8<0, 16, kRows>(blo, bhi, k, wneg, P, 0, exact);
+#else
+            adc_conv8<0, 16, kRows>(blo, bhi, k, wneg, P, 0, exact);
+            if (!TRIM || nvr > 8) adc_conv8<8, 16, kRows>(blo, bhi, k, wneg, P, 8, exact);
+#endif
+            tmem_wait_ld();
+          }
+          nchain_done = true;
+        }
+      }
+#endif
+      for (int c = 0; c < nchain && !nchain_done; ++c) {
         // chains run tc-major, then slice: weight 2^(s db) k.unscale
         const float w = wmag;
         if (++s == a.S) {
@@ -430,8 +488,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lo[0] == 0xdeadbeef && hi[kRows - 1] == 0x12345) P[0] += wp;
           continue;
 #endif
+#ifdef XBS_BWD_G16
+          if (kRows == 16 && (!TRIM || nvr > 8)) {
+            adc_conv8<0, kRows, kRows, 16>(lo, hi, k, wp, P, 0, exact);
+          } else {
+            adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
+            if (!TRIM || nvr > 8) adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
+          }
+#else
           adc_conv8<0>(lo, hi, k, wp, P, 0, exact);
           if (!TRIM || nvr > 8) adc_conv8<8>(lo, hi, k, wp, P, 8, exact);
+#endif
           if constexpr (kRows >= 32) {
             if (!TRIM || nvr > 16) adc_conv8<16>(lo, hi, k, wp, P, 16, exact);
             if (!TRIM || nvr > 24) adc_conv8<24>(lo, hi, k, wp, P, 24, exact);
