@@ -93,6 +93,78 @@ __global__ void k_observe_bwd(Geo g, int64_t M, const uint8_t* __restrict__ A, c
   }
 }
 
+// General converters (volts mode: multi-bit DAC streams, DAC tables, codes
+// above 16 bits): the sensed currents are fp64 sums in the reference's order
+// (ascending crossbar rows forward, columns backward, as k_fwd_volts /
+// k_bwd_volts), recorded as their bit patterns -- non-negative doubles order
+// as u64, so the same radix select (over 64 bits) finds sorted[rank].
+__global__ void k_observe_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint32_t* __restrict__ xc,
+                                    const uint8_t* __restrict__ digits, const unsigned long long* __restrict__ count,
+                                    unsigned long long* __restrict__ out) {
+  const int nx = g.Ti / v.sb, mask = (1 << v.sb) - 1;
+  const int64_t per_b = int64_t(nx) * g.GC * g.GR * g.S * 2 * g.tile_cols;
+  const int64_t n = M * per_b;
+  const unsigned long long base = *count;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t u = t;
+    const int c = int(u % g.tile_cols);
+    u /= g.tile_cols;
+    const int p = int(u % 2);
+    u /= 2;
+    const int s = int(u % g.S);
+    u /= g.S;
+    const int tr = int(u % g.GR);
+    u /= g.GR;
+    const int tc = int(u % g.GC);
+    u /= g.GC;
+    const int k = int(u % nx);
+    const int64_t b = u / nx;
+    const int rows = min(g.tile_rows, g.K - tr * g.tile_rows);  // padded rows carry volts(0) = 0
+    double I = 0.0;
+    for (int r = 0; r < rows; ++r) {
+      const int d = int(xc[b * g.K + tr * g.tile_rows + r] >> (k * v.sb)) & mask;
+      if (d) I = __dadd_rn(I, __dmul_rn(v.lut[d], ldexp(double(q_at(digits, g, s, p, tr, tc, r, c)), -e)));
+    }
+    out[base + t] = (unsigned long long)__double_as_longlong(I);
+  }
+}
+
+__global__ void k_observe_bwd_volts(Geo g, VoltsP v, int e, int64_t M, const int32_t* __restrict__ ec,
+                                    const uint8_t* __restrict__ digits, const DevScalars* __restrict__ sc,
+                                    const unsigned long long* __restrict__ count,
+                                    unsigned long long* __restrict__ out) {
+  if (!(sc->se > 0)) return;
+  const int ne = g.Te / v.sb, mask = (1 << v.sb) - 1;
+  const int64_t per_b = int64_t(ne) * g.GR * g.GC * g.S * 4 * g.tile_rows;
+  const int64_t n = M * per_b;
+  const unsigned long long base = *count;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t u = t;
+    const int r = int(u % g.tile_rows);
+    u /= g.tile_rows;
+    const int ro = int(u % 4);
+    u /= 4;
+    const int s = int(u % g.S);
+    u /= g.S;
+    const int tc = int(u % g.GC);
+    u /= g.GC;
+    const int tr = int(u % g.GR);
+    u /= g.GR;
+    const int k = int(u % ne);
+    const int64_t b = u / ne;
+    const int phase = ro & 1, pol = (ro == 0 || ro == 3) ? 0 : 1;  // as k_observe_bwd
+    const int cols = min(g.tile_cols, g.N - tc * g.tile_cols);
+    double I = 0.0;
+    for (int c = 0; c < cols; ++c) {
+      const int code = ec[b * g.N + tc * g.tile_cols + c];
+      const int mag = phase == 0 ? (code > 0 ? code : 0) : (code < 0 ? -code : 0);
+      const int d = (mag >> (k * v.sb)) & mask;
+      if (d) I = __dadd_rn(I, __dmul_rn(v.lut[d], ldexp(double(q_at(digits, g, s, pol, tr, tc, r, c)), -e)));
+    }
+    out[base + t] = (unsigned long long)__double_as_longlong(I);
+  }
+}
+
 __global__ void k_obs_advance(unsigned long long* count, unsigned long long added, const DevScalars* sc,
                               int need_se) {
   if (need_se && !(sc->se > 0)) return;
@@ -142,10 +214,15 @@ void reserve(xbs_core* c, int dir, int64_t add, cudaStream_t st) {
 
 void calib_observe_fwd(xbs_core* c, int64_t M, cudaStream_t st) {
   const Geo& g = c->g;
-  const int64_t n = M * g.Ti * g.GC * g.GR * g.S * 2 * g.tile_cols;
+  const int streams = c->volts_mode ? g.Ti / c->volts.sb : g.Ti;
+  const int64_t n = M * streams * g.GC * g.GR * g.S * 2 * g.tile_cols;
   if (n == 0) return;
   reserve(c, 0, n, st);
-  k_observe_fwd<<<grid_for(n), 256, 0, st>>>(g, M, c->d_Af, c->d_digits, c->d_obs_count, c->d_obs[0]);
+  if (c->volts_mode)
+    k_observe_fwd_volts<<<grid_for(n), 256, 0, st>>>(g, c->volts, c->rp.snap_e, M, c->d_xcodes32, c->d_digits,
+                                                     c->d_obs_count, c->d_obs[0]);
+  else
+    k_observe_fwd<<<grid_for(n), 256, 0, st>>>(g, M, c->d_Af, c->d_digits, c->d_obs_count, c->d_obs[0]);
   k_obs_advance<<<1, 1, 0, st>>>(c->d_obs_count, (unsigned long long)n, c->d_sc, 0);
   c->obs_used[0] += n;
   c->launches += 2;
@@ -153,11 +230,16 @@ void calib_observe_fwd(xbs_core* c, int64_t M, cudaStream_t st) {
 
 void calib_observe_bwd(xbs_core* c, int64_t M, cudaStream_t st) {
   const Geo& g = c->g;
-  const int64_t n = M * g.Te * g.GR * g.GC * g.S * 4 * g.tile_rows;
+  const int streams = c->volts_mode ? g.Te / c->volts.sb : g.Te;
+  const int64_t n = M * streams * g.GR * g.GC * g.S * 4 * g.tile_rows;
   if (n == 0) return;
   reserve(c, 1, n, st);
-  k_observe_bwd<<<grid_for(n), 256, 0, st>>>(g, M, c->d_Ab, c->d_digits, c->d_sc, c->d_obs_count + 1,
-                                             c->d_obs[1]);
+  if (c->volts_mode)
+    k_observe_bwd_volts<<<grid_for(n), 256, 0, st>>>(g, c->volts, c->rp.snap_e, M, c->d_ecodes, c->d_digits, c->d_sc,
+                                                     c->d_obs_count + 1, c->d_obs[1]);
+  else
+    k_observe_bwd<<<grid_for(n), 256, 0, st>>>(g, M, c->d_Ab, c->d_digits, c->d_sc, c->d_obs_count + 1,
+                                               c->d_obs[1]);
   k_obs_advance<<<1, 1, 0, st>>>(c->d_obs_count + 1, (unsigned long long)n, c->d_sc, 1);
   c->obs_used[1] += n;  // upper bound (zero-error batches add nothing on the device)
   c->launches += 2;
@@ -177,7 +259,8 @@ bool calib_select(xbs_core* c, int dir, double pct, uint64_t* n_out) {
   ck_cuda(cudaMalloc(&d_hist, 2048 * 8), "cudaMalloc calibration histogram");
   unsigned long long h[2048];
   unsigned long long prefix = 0, mask = 0;
-  for (int shift = 33; shift >= 0; shift -= 11) {
+  // integer currents n < 2^44: 4 passes; fp64 bit patterns (volts mode): 6
+  for (int shift = c->volts_mode ? 55 : 33; shift >= 0; shift -= 11) {
     ck_cuda(cudaMemsetAsync(d_hist, 0, 2048 * 8, st), "memset histogram");
     k_obs_hist<<<grid_for(int64_t(count)), 256, 0, st>>>(c->d_obs[dir], int64_t(count), prefix, mask, shift, d_hist);
     ck_cuda(cudaMemcpyAsync(h, d_hist, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H histogram");

@@ -127,10 +127,12 @@ void validate_options(const xbs_layer_options& o, const std::vector<double>& dac
 }
 
 // Converters off the tensor-core contract (1-bit DAC streams at a power-of-
-// two full scale, linear ADC of <= 16 bits): multi-bit DAC streams, DAC / ADC
-// transfer tables, wider ADCs, other DAC full scales.
+// two full scale, linear ADC of <= 16 bits, activation / error codes of <= 16
+// bits): multi-bit DAC streams, DAC / ADC transfer tables, wider ADCs, other
+// DAC full scales, 17- to 24-bit codes (layers.cpp:28-31).
 bool volts_mode(const xbs_layer_options& o, const std::vector<double>& dac_tr, const std::vector<double>& adc_tr) {
-  return !dac_tr.empty() || !adc_tr.empty() || o.adc_bits > 16 || o.dac_bits != 1 || !is_pow2_double(o.dac_v_fs);
+  return !dac_tr.empty() || !adc_tr.empty() || o.adc_bits > 16 || o.dac_bits != 1 || !is_pow2_double(o.dac_v_fs) ||
+         o.act_bits > 16 || o.error_bits > 16;
 }
 
 // Path scope: valid reference configurations this
@@ -146,15 +148,17 @@ void check_scope(const xbs_layer_options& o, const std::vector<double>& dac_tr, 
     if (o.fcm_max_iter < 1) fail(XBS_INVALID_ARGUMENT, "fcm_convert: max_iter must be >= 1");
   }
   if (o.engine < 0 || o.engine > 4) fail(XBS_INVALID_ARGUMENT, "unknown engine");
-  // general converters run the exact fp64 CUDA-core VMMs (volts mode);
-  // their ADC must have an explicit full scale or a threshold table
-  if (volts_mode(o, dac_tr, adc_tr)) {
-    if (o.dac_bits > 16) fail(XBS_UNSUPPORTED, "DAC streams wider than 16 bits are not on this path");
-    if (o.adc_bits > 0 && !(o.adc_i_fs > 0) && adc_tr.empty())
-      fail(XBS_UNSUPPORTED, "ADC auto-calibration with multi-bit / table converters is not on this path");
-  }
-  if (o.act_bits > 16 || o.error_bits > 16) fail(XBS_UNSUPPORTED, "act_bits / error_bits > 16 are not on this path");
-  if (o.tile_rows > 256 || o.tile_cols > 256) fail(XBS_UNSUPPORTED, "tiles larger than 256 x 256 are not on this path");
+  // general converters run the exact fp64 CUDA-core VMMs (volts mode)
+  if (volts_mode(o, dac_tr, adc_tr) && o.dac_bits > 16)
+    fail(XBS_UNSUPPORTED, "DAC streams wider than 16 bits are not on this path");
+  // tiles above 256 x 256 run the exact integer CUDA-core VMMs (a 256-row
+  // crossbar is the most one TMEM accumulator pair sums exactly); the integer
+  // currents and the ADC table are sized for <= 1024 rows
+  if (o.tile_rows > 1024 || o.tile_cols > 1024)
+    fail(XBS_UNSUPPORTED, "tiles larger than 1024 x 1024 are not on this path");
+  const bool circuit_tiles = (o.engine == XBS_ENGINE_FCM || o.engine == XBS_ENGINE_INTERP_FCM) && !zero_par;
+  if (circuit_tiles && (o.tile_rows > 256 || o.tile_cols > 256))  // one thread per crossbar line, <= 256 per CTA
+    fail(XBS_UNSUPPORTED, "fcm / interp_fcm on tiles larger than 256 x 256 is not on this path");
 }
 
 int snap_exponent(double g_max) {  // largest e with g_max * 2^e <= Q_MAX
@@ -172,20 +176,28 @@ void ensure_batch(xbs_core* c, int64_t M) {
   cudaFree(c->d_Af);
   cudaFree(c->d_Ab);
   cudaFree(c->d_xcodes);
+  cudaFree(c->d_xcodes32);
   cudaFree(c->d_ecodes);
   c->d_Af = nullptr;
   c->d_Ab = nullptr;
   c->d_xcodes = nullptr;
+  c->d_xcodes32 = nullptr;
   c->d_ecodes = nullptr;
-  const int64_t rowsF = xbs::rows_fwd(cap, c->g.TPi);
-  const int64_t rowsB = xbs::rows_bwd(cap, c->g.TPe);
-  ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
-  ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NB), "cudaMalloc A_bwd");
-  // the prep kernels never write 16-column groups that hold only tile
-  // padding: those plane bytes stay the zeros written here
-  ck(cudaMemsetAsync(c->d_Af, 0, size_t(2 * rowsF) * c->g.KI, c->stream), "memset A_fwd");
-  ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NB, c->stream), "memset A_bwd");
-  ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
+  if (c->volts_mode) {
+    // the exact fp64 kernels read the codes themselves: u32 activation
+    // codes (up to 24 bits), no bit planes
+    ck(cudaMalloc(&c->d_xcodes32, size_t(cap) * c->g.K * sizeof(uint32_t)), "cudaMalloc xcodes");
+  } else {
+    const int64_t rowsF = xbs::rows_fwd(cap, c->g.TPi);
+    const int64_t rowsB = xbs::rows_bwd(cap, c->g.TPe);
+    ck(cudaMalloc(&c->d_Af, size_t(2 * rowsF) * c->g.KI), "cudaMalloc A_fwd");
+    ck(cudaMalloc(&c->d_Ab, size_t(2 * rowsB) * c->g.NB), "cudaMalloc A_bwd");
+    // the prep kernels never write 16-column groups that hold only tile
+    // padding: those plane bytes stay the zeros written here
+    ck(cudaMemsetAsync(c->d_Af, 0, size_t(2 * rowsF) * c->g.KI, c->stream), "memset A_fwd");
+    ck(cudaMemsetAsync(c->d_Ab, 0, size_t(2 * rowsB) * c->g.NB, c->stream), "memset A_bwd");
+    ck(cudaMalloc(&c->d_xcodes, size_t(cap) * c->g.K * sizeof(uint16_t)), "cudaMalloc xcodes");
+  }
   ck(cudaMalloc(&c->d_ecodes, size_t(cap) * c->g.N * sizeof(int32_t)), "cudaMalloc ecodes");
   cudaFree(c->d_xc8);
   cudaFree(c->d_e8);
@@ -405,14 +417,25 @@ void maybe_freeze_adc(xbs_core* c) {
   if (c->training_batches < c->opt.adc_cal_batches) return;
   double ifs[2] = {0.0, 0.0};  // adc.i_fs as configured (<= 0) stays "unset"
   for (int dir = 0; dir < 2; ++dir) {
-    uint64_t n = 0;
-    ifs[dir] = xbs::calib_select(c, dir, c->opt.adc_clip_percentile, &n) ? std::ldexp(double(n), c->adc.sh)
-                                                                         : c->opt.adc_i_fs;
+    uint64_t n = 0;  // the selected integer current, or (volts mode) the fp64 current's bit pattern
+    if (!xbs::calib_select(c, dir, c->opt.adc_clip_percentile, &n)) ifs[dir] = c->opt.adc_i_fs;
+    else ifs[dir] = c->volts_mode ? __builtin_bit_cast(double, n) : std::ldexp(double(n), c->adc.sh);
   }
   xbs::calib_release(c);
   c->adc_frozen = true;
-  set_adc(c, 0, ifs[0]);
-  set_adc(c, 1, ifs[1]);
+  if (c->volts_mode) {  // the fp64 kernels quantise with adc_quantize itself: no threshold table
+    ++c->gen;
+    const double maxc = std::pow(2.0, c->opt.adc_bits) - 1.0;
+    c->adc.i_fs = c->volts.i_fs = ifs[0];
+    c->adc_b.i_fs = c->volts.i_fs_b = ifs[1];
+    c->adc.passthrough = c->adc_b.passthrough = 0;
+    c->volts.passthrough = 0;
+    c->ifs_fac = ifs[0] / maxc;
+    c->ifs_fac_b = ifs[1] / maxc;
+  } else {
+    set_adc(c, 0, ifs[0]);
+    set_adc(c, 1, ifs[1]);
+  }
   c->adc_scaled = true;
   c->k_out_fwd = c->sx * c->F / c->vu * c->ifs_fac;  // layers.cpp:278-281
 }
@@ -455,8 +478,10 @@ void enqueue_fwd_vmm(xbs_core* c, int64_t M, const Out& out) {
     xbs::launch_fwd_ideal(c, M, stage, c->stream);
   } else if (c->volts_mode) {
     xbs::launch_fwd_volts(c, M, stage, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
-    if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;  // shape outside the tcgen05 kernel's exact bounds
+  } else if (c->kernel == 1 || c->big_tiles || c->adc.passthrough ||
+             !(direct = xbs::launch_fwd_tc(c, M, out.p, ld, c->stream))) {
+    // shape outside the tcgen05 kernel's exact bounds (tiles above 256 x 256 are SIMT by design)
+    if (c->kernel == 0 && !c->big_tiles && !c->adc.passthrough) ++c->tc_fallbacks;
     xbs::launch_fwd_simt(c, M, stage, c->stream);
   }
   finish_out(c, Out{out.p, ld, out.host}, M, c->g.N, direct);
@@ -470,8 +495,9 @@ void enqueue_bwd_vmm(xbs_core* c, const double* d_dy, int64_t M, const Out& out)
     xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
   } else if (c->volts_mode) {
     xbs::launch_bwd_volts(c, M, stage, c->stream);
-  } else if (c->kernel == 1 || c->adc.passthrough || !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
-    if (c->kernel == 0 && !c->adc.passthrough) ++c->tc_fallbacks;
+  } else if (c->kernel == 1 || c->big_tiles || c->adc.passthrough ||
+             !(direct = xbs::launch_bwd_tc(c, M, out.p, ld, c->stream))) {
+    if (c->kernel == 0 && !c->big_tiles && !c->adc.passthrough) ++c->tc_fallbacks;
     xbs::launch_bwd_simt(c, M, stage, c->stream);
   }
   finish_out(c, Out{out.p, ld, out.host}, M, c->g.K, direct);
@@ -857,6 +883,7 @@ xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K,
       return c.release();
     }
     c->volts_mode = volts_mode(o, c->dac_tr, c->adc_tr);
+    c->big_tiles = o.tile_rows > 256 || o.tile_cols > 256;
     if (c->volts_mode) {
       // dac_encode of every digit (converters.cpp:28-35) and the ADC spec
       const uint64_t levels = (uint64_t{1} << o.dac_bits) - 1;
@@ -872,12 +899,12 @@ xbs_core* create_core(const xbs_layer_options* opt, const double* W0, int64_t K,
       xbs::VoltsP& v = c->volts;
       v.lut = c->d_dac_lut;
       v.sb = o.dac_stream_bits;
-      v.passthrough = o.adc_bits == 0;
+      v.passthrough = o.adc_bits == 0 || c->adc_auto;  // calibration batches pass currents through
       v.adc_tr = c->d_adc_tr;
       v.tr_len = int(c->adc_tr.size());
       v.maxcode = o.adc_bits > 0 ? (uint64_t{1} << o.adc_bits) - 1 : 0;
       v.maxc_d = double(v.maxcode);
-      v.i_fs = o.adc_i_fs;
+      v.i_fs = v.i_fs_b = o.adc_i_fs;
     } else if (!a.passthrough) {
       set_adc(c.get(), 0, o.adc_i_fs);
       set_adc(c.get(), 1, o.adc_i_fs);
@@ -1000,6 +1027,7 @@ void xbs_core_destroy(xbs_core* c) {
   cudaFree(c->d_Af);
   cudaFree(c->d_Ab);
   cudaFree(c->d_xcodes);
+  cudaFree(c->d_xcodes32);
   cudaFree(c->d_ecodes);
   cudaFree(c->d_xc8);
   cudaFree(c->d_e8);

@@ -96,7 +96,8 @@ struct VoltsP {
   const double* adc_tr;         // ADC thresholds (converters.cpp:76-82), device, or null
   int tr_len;
   unsigned long long maxcode;   // 2^bits - 1 (bits <= 32)
-  double maxc_d, i_fs;
+  double maxc_d, i_fs;          // i_fs: forward full scale
+  double i_fs_b;                // backward full scale (differs after auto-calibration)
 };
 
 // Device scalars (one struct per core, in HBM).
@@ -132,6 +133,7 @@ struct xbs_core {
   xbs::AdcP adc{};    // forward ADC (adc_fwd_)
   xbs::AdcP adc_b{};  // backward ADC (adc_bwd_); differs from adc only after auto-calibration
   bool volts_mode = false;  // general converters: exact fp64 CUDA-core VMMs (k_fwd_volts / k_bwd_volts)
+  bool big_tiles = false;   // tiles above 256 x 256: exact integer CUDA-core VMMs (k_fwd_simt / k_bwd_simt)
   xbs::VoltsP volts{};
   double* d_dac_lut = nullptr;
   double* d_adc_tr = nullptr;
@@ -189,6 +191,7 @@ struct xbs_core {
   uint8_t* d_Af = nullptr;   // 2 * rowsF * KI
   uint8_t* d_Ab = nullptr;   // 2 * rowsB * NI
   uint16_t* d_xcodes = nullptr;
+  uint32_t* d_xcodes32 = nullptr;  // volts mode: u32 codes (act_bits up to 24), no bit planes
   int32_t* d_ecodes = nullptr;  // signed error codes: 16-bit magnitudes need more than int16
   // u8 operands of the tcgen05 dW GEMM (act/error bits <= 8): x codes
   // [Mcap8][KA], error magnitudes [plus | minus][Mcap8][NA]; K, N padded to

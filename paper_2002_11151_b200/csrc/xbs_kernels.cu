@@ -882,12 +882,17 @@ __device__ __forceinline__ bool plane_sector_live(int r16, int nlive) {
   return (r16 & ~31) < nlive;  // r16: first block column of the group
 }
 
-template <bool CONV>
+// CT = uint16_t: the tensor-core contract (codes of <= 16 bits and both
+// bit-plane copies).  CT = uint32_t: the general converters (volts mode),
+// whose exact fp64 kernels read the codes directly -- codes of up to 24 bits
+// (layers.cpp:28-31), no planes.
+template <bool CONV, class CT>
 __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict__ x, int64_t M, int64_t rowsF,
-                                                double step, double inv, double levels, uint16_t* __restrict__ codes,
+                                                double step, double inv, double levels, CT* __restrict__ codes,
                                                 uint8_t* __restrict__ A, uint8_t* __restrict__ c8, int ld8,
                                                 ConvSrc cv, int64_t bt0) {
-  __shared__ uint16_t cs[kPrepTB][kPrepTI + 2];
+  constexpr bool kPlanes = sizeof(CT) == 2;
+  __shared__ CT cs[kPrepTB][kPrepTI + 2];
   __shared__ int coff[kPrepTI], cky[kPrepTI], ckx[kPrepTI];  // CONV: image offset and (ky, kx) per column
   const int64_t b0 = (bt0 + blockIdx.y) * kPrepTB;
   const int c0 = blockIdx.x * kPrepTI;  // column blocks fastest: a plane row's segments are written together  // device column (0 .. KI); a block lies in one row tile (R % 64 == 0)
@@ -940,7 +945,7 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
     // llround of a non-positive quotient is <= 0: code 0 (clamped); columns
     // beyond nlive load 0 and so hold code 0
     const uint32_t code = xv[n] > 0.0 ? uint32_t(quant_mag(xv[n], step, inv, levels)) : 0u;
-    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = uint16_t(code);
+    cs[bl][il0 + n * (kPrepThreads / kPrepTB)] = CT(code);
   }
   __syncthreads();
   // codes [b][K] (u16) and the u8 dW codes [b][ld8]: one thread per (row, 8
@@ -950,16 +955,23 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
     const int o = e % (kPrepTI / 8) * 8, r = e / (kPrepTI / 8);
     const int64_t b = b0 + r;
     if (b >= M || o >= nlive) continue;
-    const uint16_t* src = &cs[r][o];
+    const CT* src = &cs[r][o];
     if (vec && o + 8 <= nlive) {
-      uint32_t w[4], w8[2];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) w[h] = uint32_t(src[2 * h]) | (uint32_t(src[2 * h + 1]) << 16);
+      uint32_t w8[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         w8[h] = (uint32_t(src[4 * h]) & 0xffu) | ((uint32_t(src[4 * h + 1]) & 0xffu) << 8) |
                 ((uint32_t(src[4 * h + 2]) & 0xffu) << 16) | (uint32_t(src[4 * h + 3]) << 24);
-      *reinterpret_cast<uint4*>(codes + b * g.K + i0 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+      if constexpr (kPlanes) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) w[h] = uint32_t(src[2 * h]) | (uint32_t(src[2 * h + 1]) << 16);
+        *reinterpret_cast<uint4*>(codes + b * g.K + i0 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        uint4* co = reinterpret_cast<uint4*>(codes + b * g.K + i0 + o);
+        co[0] = make_uint4(src[0], src[1], src[2], src[3]);
+        co[1] = make_uint4(src[4], src[5], src[6], src[7]);
+      }
       if (c8) *reinterpret_cast<uint2*>(c8 + b * ld8 + i0 + o) = make_uint2(w8[0], w8[1]);
     } else {
       for (int t = 0; t < 8 && o + t < nlive; ++t) {
@@ -970,6 +982,7 @@ __global__ void __launch_bounds__(256) k_prep_x(Geo g, const double* __restrict_
   }
   // bit planes: one thread per (batch row, 16 columns) packs the codes'
   // bytes four to a word once; plane k is then (word >> k) & 0x01010101
+  if constexpr (!kPlanes) return;
   constexpr int Q = kPrepTI / 16;
   for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
     const int q = e % Q, r = e / Q;
@@ -1004,7 +1017,7 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
   const int64_t rowsF = rows_fwd(M, c->g.TPi);
   // zero the M-padding rows once per call (rows [M*TPi, rowsF))
   const int64_t pad0 = M * c->g.TPi;
-  if (rowsF > pad0) {
+  if (c->d_Af && rowsF > pad0) {
     cudaMemsetAsync(c->d_Af + pad0 * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
     cudaMemsetAsync(c->d_Af + (rowsF + pad0) * c->g.KI, 0, size_t(rowsF - pad0) * c->g.KI, st);
   }
@@ -1018,12 +1031,19 @@ void launch_prep_x(const xbs_core* c, const double* d_x, int64_t M, cudaStream_t
   }
   for (int64_t bt0 = 0; bt0 < nbt; bt0 += 65535) {
     const dim3 grid(unsigned(c->g.KI / kPrepTI), unsigned(std::min<int64_t>(nbt - bt0, 65535)));
-    if (conv)
-      k_prep_x<true><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes, c->d_Af,
-                                            c->d_xc8, c->KA, *conv, bt0);
+    if (c->d_xcodes32) {  // volts mode: u32 codes only
+      if (conv)
+        k_prep_x<true, uint32_t><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes32,
+                                                        nullptr, c->d_xc8, c->KA, *conv, bt0);
+      else
+        k_prep_x<false, uint32_t><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels,
+                                                         c->d_xcodes32, nullptr, c->d_xc8, c->KA, ConvSrc{}, bt0);
+    } else if (conv)
+      k_prep_x<true, uint16_t><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
+                                                      c->d_Af, c->d_xc8, c->KA, *conv, bt0);
     else
-      k_prep_x<false><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes, c->d_Af,
-                                             c->d_xc8, c->KA, ConvSrc{}, bt0);
+      k_prep_x<false, uint16_t><<<grid, 256, 0, st>>>(c->g, d_x, M, rowsF, step, 1.0 / step, levels, c->d_xcodes,
+                                                       c->d_Af, c->d_xc8, c->KA, ConvSrc{}, bt0);
   }
 }
 
@@ -1105,7 +1125,9 @@ __global__ void __launch_bounds__(256) k_prep_dy(Geo g, const double* __restrict
     }
   }
   // bit planes of the plus / minus magnitudes, packed four bytes to a word
-  // once per (batch row, 16 columns) as in k_prep_x (full 32-byte sectors)
+  // once per (batch row, 16 columns) as in k_prep_x (full 32-byte sectors);
+  // none in volts mode (no plane buffer: the fp64 kernels read the codes)
+  if (A == nullptr) return;
   constexpr int Q = kPrepTI / 16;
   for (int e = threadIdx.x; e < kPrepTB * Q; e += blockDim.x) {
     const int q = e % Q, r = e / Q;
@@ -1157,7 +1179,7 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
   k_absmax_to_se<<<1, 1, 0, st>>>(c->d_sc, &c->d_sc->wmax_in);
   const int64_t rowsB = rows_bwd(M, c->g.TPe);
   const int64_t pad0 = M * c->g.TPe * 2;
-  if (rowsB > pad0) {
+  if (c->d_Ab && rowsB > pad0) {
     cudaMemsetAsync(c->d_Ab + pad0 * c->g.NB, 0, size_t(rowsB - pad0) * c->g.NB, st);
     cudaMemsetAsync(c->d_Ab + (rowsB + pad0) * c->g.NB, 0, size_t(rowsB - pad0) * c->g.NB, st);
   }
@@ -1180,7 +1202,8 @@ void launch_prep_dy(const xbs_core* c, const double* d_dy, int64_t M, cudaStream
 
 // ---------------------------------------------------------------------- dW
 // Exact integer outer product: dW = ((S * sx) * step_e) / gd.
-__global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const uint16_t* __restrict__ xc,
+template <class CT>
+__global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const CT* __restrict__ xc,
                      const int32_t* __restrict__ ec, DevScalars* __restrict__ sc, double* __restrict__ dW) {
   const double se = sc->se;
   const double step_e = se > 0 ? se / lev_e : 0.0;
@@ -1198,7 +1221,11 @@ __global__ void k_dw(Geo g, int64_t M, double sx, double lev_e, double gd, const
 void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t st) {
   const int64_t n = int64_t(c->g.K) * c->g.N;
   const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
-  k_dw<<<blocks, 256, 0, st>>>(c->g, M, c->sx, c->lev_e, grad_divisor, c->d_xcodes, c->d_ecodes, c->d_sc, c->d_dW);
+  if (c->d_xcodes32)
+    k_dw<<<blocks, 256, 0, st>>>(c->g, M, c->sx, c->lev_e, grad_divisor, c->d_xcodes32, c->d_ecodes, c->d_sc,
+                                 c->d_dW);
+  else
+    k_dw<<<blocks, 256, 0, st>>>(c->g, M, c->sx, c->lev_e, grad_divisor, c->d_xcodes, c->d_ecodes, c->d_sc, c->d_dW);
 }
 
 // ------------------------------------------------------ general converters
@@ -1212,7 +1239,7 @@ void launch_dw(const xbs_core* c, int64_t M, double grad_divisor, cudaStream_t s
 // accumulation order as layers.cpp:246-283 / 340-378 -- so the outputs are
 // bit-identical to the oracle's restatement.  No tensor-core path exists for
 // them (the radix-255 operands need 1-bit digits and power-of-two volts).
-__device__ __forceinline__ double adc_volts(const VoltsP& v, double I) {
+__device__ __forceinline__ double adc_volts(const VoltsP& v, double I, double i_fs) {
   if (v.passthrough) return I;
   if (v.tr_len > 0) {  // converters.cpp:76-82: highest threshold not exceeding I
     int lo = 0, hi = v.tr_len;  // first index with transfer[idx] > I
@@ -1225,7 +1252,7 @@ __device__ __forceinline__ double adc_volts(const VoltsP& v, double I) {
     const unsigned long long code = (unsigned long long)(lo - 1);
     return double(code < v.maxcode ? code : v.maxcode);
   }
-  const double scaled = __dmul_rn(__ddiv_rn(I, v.i_fs), v.maxc_d);  // converters.cpp:85-87
+  const double scaled = __dmul_rn(__ddiv_rn(I, i_fs), v.maxc_d);  // converters.cpp:85-87
   if (scaled >= v.maxc_d) return v.maxc_d;
   return double(llround(scaled));
 }
@@ -1235,7 +1262,7 @@ __device__ __forceinline__ double g_snapped(const Geo& g, const uint8_t* digits,
   return ldexp(double(load_q(digits, g, s, p, tr, tc, r, c)), -e);  // exact: q 2^-e
 }
 
-__global__ void k_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint16_t* __restrict__ xc,
+__global__ void k_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint32_t* __restrict__ xc,
                             const uint8_t* __restrict__ digits, double k_out, double* __restrict__ y) {
   const int64_t n = M * g.N;
   const int nx = g.Ti / v.sb, mask = (1 << v.sb) - 1;
@@ -1258,7 +1285,7 @@ __global__ void k_fwd_volts(Geo g, VoltsP v, int e, int64_t M, const uint16_t* _
               const int d = (int(xc[b * g.K + tr * g.tile_rows + r]) >> (k * v.sb)) & mask;
               if (d) I = __dadd_rn(I, __dmul_rn(v.lut[d], g_snapped(g, digits, e, s, p, tr, tc, r, c)));
             }
-            acc = __dadd_rn(acc, __dmul_rn(wk, adc_volts(v, I)));
+            acc = __dadd_rn(acc, __dmul_rn(wk, adc_volts(v, I, v.i_fs)));
             wk = __dmul_rn(wk, stream_base);
           }
           tile = __dadd_rn(tile, __dmul_rn(p == 0 ? sw : -sw, acc));
@@ -1309,8 +1336,8 @@ __global__ void k_bwd_volts(Geo g, VoltsP v, int e, int64_t M, const int32_t* __
                 Imp = __dadd_rn(Imp, __dmul_rn(vm, g_snapped(g, digits, e, s, 0, tr, tc, r, c)));
               }
             }
-            ap = __dadd_rn(ap, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipp), adc_volts(v, Imn))));
-            an = __dadd_rn(an, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipn), adc_volts(v, Imp))));
+            ap = __dadd_rn(ap, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipp, v.i_fs_b), adc_volts(v, Imn, v.i_fs_b))));
+            an = __dadd_rn(an, __dmul_rn(wk, __dadd_rn(adc_volts(v, Ipn, v.i_fs_b), adc_volts(v, Imp, v.i_fs_b))));
             wk = __dmul_rn(wk, stream_base);
           }
           tile = __dadd_rn(tile, __dmul_rn(sw, __dsub_rn(ap, an)));
@@ -1325,7 +1352,8 @@ void launch_fwd_volts(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st
   const int64_t n = M * c->g.N;
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
-  k_fwd_volts<<<blocks, 128, 0, st>>>(c->g, c->volts, c->rp.snap_e, M, c->d_xcodes, c->d_digits, c->k_out_fwd, d_y);
+  k_fwd_volts<<<blocks, 128, 0, st>>>(c->g, c->volts, c->rp.snap_e, M, c->d_xcodes32, c->d_digits, c->k_out_fwd,
+                                      d_y);
 }
 
 void launch_bwd_volts(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st) {
@@ -1484,7 +1512,8 @@ void launch_bwd_simt(const xbs_core* c, int64_t M, double* d_dx, cudaStream_t st
 
 // ------------------------------------------------------ fully-ideal path
 // y = x_values * wimp (layers.cpp:226), ascending k, unfused mul/add.
-__global__ void k_fwd_ideal(Geo g, int64_t M, double sx, const uint16_t* __restrict__ xc,
+template <class CT>
+__global__ void k_fwd_ideal(Geo g, int64_t M, double sx, const CT* __restrict__ xc,
                             const double* __restrict__ w, double* __restrict__ y) {
   const int64_t n = M * g.N;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
@@ -1500,7 +1529,8 @@ void launch_fwd_ideal(const xbs_core* c, int64_t M, double* d_y, cudaStream_t st
   const int64_t n = M * c->g.N;
   if (n == 0) return;
   const int blocks = int(std::min<int64_t>((n + 127) / 128, 148 * 64));
-  k_fwd_ideal<<<blocks, 128, 0, st>>>(c->g, M, c->sx, c->d_xcodes, c->d_wimp, d_y);
+  if (c->d_xcodes32) k_fwd_ideal<<<blocks, 128, 0, st>>>(c->g, M, c->sx, c->d_xcodes32, c->d_wimp, d_y);
+  else k_fwd_ideal<<<blocks, 128, 0, st>>>(c->g, M, c->sx, c->d_xcodes, c->d_wimp, d_y);
 }
 
 // dx = dy_q * wimp^T (layers.cpp:307), dy_q = (sign*mag)*step_e (layers.cpp:301-302)

@@ -82,9 +82,10 @@ def test_nonfinite_and_empty_weights_rejected():
     "mutate",
     [
         lambda o: setattr(o, "engine", xb.EngineKind.oracle),  # dense nodal solve with parasitics (8f-4)
-        # auto-calibration with a multi-bit DAC stream (the general-converter
-        # path needs an explicit full scale or a threshold table)
-        lambda o: (setattr(o.dac, "bits", 2), setattr(o.dac, "stream_bits", 2), setattr(o.adc, "i_fs", 0.0)),
+        # a DAC stream wider than 16 bits (the general-converter path keeps one
+        # table entry per digit)
+        lambda o: (setattr(o.dac, "bits", 20), setattr(o.dac, "stream_bits", 20), setattr(o, "act_bits", 20),
+                   setattr(o, "error_bits", 20)),
     ],
 )
 def test_out_of_scope_configs_fail_loudly(mutate):

@@ -5,7 +5,8 @@ wider than 16 bits and non-power-of-two DAC full scales.  These currents are
 not integers on the snapped grid, so the layer runs the exact fp64
 CUDA-core VMMs (k_fwd_volts / k_bwd_volts), which follow the reference's
 fp64 order term by term: y and dx bit-exact against the snapped oracle,
-before and after an update, plus dW."""
+before and after an update, plus dW; ADC auto-calibration on the same
+converters."""
 import numpy as np
 import pytest
 
@@ -71,8 +72,48 @@ def test_general_converters_bit_exact(case):
     assert gpu.info().tc_fallbacks == 0  # this path is by design, not a fallback
 
 
-def test_general_converters_refuse_auto_calibration():
-    opt, K, N = _options("dac2")
-    opt.adc.i_fs = 0.0  # auto-calibration with a multi-bit DAC
-    with pytest.raises(xb.UnsupportedConfigError):
-        xb.CrossbarCore(normal((K, N), 1, 0.05), opt)
+AUTOCAL = {
+    "dac2": dict(dac_bits=2),
+    "dac4_table": dict(dac_bits=4, dac_table=True),
+    "vfs_0.8": dict(v_fs=0.8),
+    "adc20": dict(adc_bits=20),
+    "codes20": dict(act_bits=20, error_bits=20),
+}
+
+
+@pytest.mark.parametrize("case", sorted(AUTOCAL))
+def test_general_converters_auto_calibrate(case):
+    """layers.cpp:74, 189-213 with the general converters: the calibration
+    batches pass the fp64 currents through and record them (as bit patterns:
+    non-negative doubles order as integers); the freeze picks the reference's
+    nearest-rank quantile (converters.cpp:96-107).  y, dx bit-exact at every
+    call, the frozen forward i_fs equal to the oracle's."""
+    c = AUTOCAL[case]
+    o = aam_options(tile=64, adc_bits=c.get("adc_bits", 7), i_fs=0.0, r_col=4.6, act_bits=c.get("act_bits", 8),
+                    error_bits=c.get("error_bits", 8), lr=0.2, useed=3)
+    sb = c.get("dac_bits", 1)
+    o.dac.bits = o.dac.stream_bits = sb
+    o.dac.v_fs = c.get("v_fs", 1.0)
+    if c.get("dac_table"):
+        o.dac.transfer = _dac_curve(sb)
+    o.adc.clip_percentile = 0.995
+    o.adc_cal_batches = cal = 2
+    K, N, M = 100, 80, 5
+    W = normal((K, N), 11, 0.05)
+    gpu = xb.CrossbarCore(W, o)
+    orc = oracle_py.OracleCore(W, o, snapped=True)
+    _sync_conductances(gpu, orc, o)
+    x = rand((M, K), 12, -0.1, 1.1)
+    for it in range(cal + 1):
+        y, y_o = gpu.forward(x, True), orc.forward(x, True)
+        assert np.array_equal(y, y_o), (case, it, np.max(np.abs(y - y_o)))
+        dy = rand((M, N), 13 + it)
+        dx, dx_o = gpu.backward(dy, 1.0), orc.backward(dy, 1.0)
+        assert np.array_equal(dx, dx_o), (case, it, np.max(np.abs(dx - dx_o)))
+        assert np.array_equal(gpu.gradient(), orc.gradient())
+        st = orc.stats()
+        assert gpu.forward_adc_full_scale() == st["fwd_i_fs"]
+        assert (st["fwd_i_fs"] > 0) == (it + 1 >= cal)
+        gpu.apply_updates(it)
+        orc.apply_updates(it)
+        _sync_conductances(gpu, orc, o)
