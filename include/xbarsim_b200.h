@@ -38,11 +38,12 @@ typedef enum xbs_status {
   XBS_STALE_CACHE_ERROR = 5,       /* xbarsim::StaleCacheError               */
   XBS_DEGENERATE_CIRCUIT_ERROR = 6,/* xbarsim::DegenerateCircuitError        */
   XBS_UNSUPPORTED = 7,             /* valid reference config outside this
-                                      path's scope (e.g. the oracle engine
-                                      with parasitics, transfer tables, an
-                                      auto-calibration sample larger than
-                                      the device); maps to
-                                      ConfigError in the C++ wrapper         */
+                                      path's scope (the oracle engine with
+                                      parasitics, DAC streams above 16 bits,
+                                      tiles above 1024 x 1024, fcm on tiles
+                                      above 256 x 256, an auto-calibration
+                                      sample larger than the device); maps
+                                      to ConfigError in the C++ wrapper      */
   XBS_CUDA_ERROR = 8,              /* device fault; StateError + CUDA string */
   XBS_INTERNAL = 9
 } xbs_status;

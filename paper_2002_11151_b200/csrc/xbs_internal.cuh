@@ -113,6 +113,7 @@ struct DevScalars {
   unsigned int fcm_fail;                 // FCM tiles without a fixed point in the last regeneration
   unsigned int pad2;
   unsigned long long fcm_residual;       // bits of the largest such residual (relative to v_fs)
+  unsigned int wave_sync[2];             // CTA-pair arrival counters of the forward / backward VMM (wave alignment)
 };
 
 // FCM conversion parameters (fcm.hpp:9-16, tile geometry and parasitics of

@@ -132,6 +132,19 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// Wave alignment of the persistent VMM producers (performance only, never a
+// correctness dependency: the wait is bounded).  The CTA pairs that share a
+// unit column of digit tiles read it through L2 only while they sweep it
+// within a few crossbar tiles of each other (at 2-3 TB/s of operand traffic
+// L2 turns over in ~50 us); nothing else keeps persistent CTAs in step, so
+// each producer arrives on a global counter at the start of a round of units
+// and waits (at most ~30 us) for the others.
+__device__ __forceinline__ void wave_align(unsigned int* ctr, unsigned int target) {
+  atomicAdd(ctr, 1u);
+  const long long t0 = clock64();
+  while (*reinterpret_cast<volatile unsigned int*>(ctr) < target && clock64() - t0 < 60000) __nanosleep(64);
+}
+
 // ------------------------------------------------- CTA pairs (cta_group::2)
 // Clusters of two CTAs on one TPC: the leader (rank 0) issues the M = 256
 // MMAs for both; the peer's TMA loads complete on the leader's barriers and

@@ -166,6 +166,7 @@ struct BwdArgs {
   double* dx;
   int64_t ldx;  // column stride of dx (M, or the caller's ld for a mapped host buffer)
   unsigned long long* ctr;
+  unsigned int* wsync;  // wave alignment counter (zeroed before the launch), or null
 };
 
 // Row block index -> (row tile, 64-row half); blocks made only of padding
@@ -260,7 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     {  // ------------------------------- TMA producer (converged warp, one lane issues)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
-      for (int u = cid; u < a.num_units; u += ncl) {
+      int round = 0;
+      for (int u = cid; u < a.num_units; u += ncl, ++round) {
+        if (a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
+          if (lane == 0) wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)));
+          __syncwarp();
+        }
         int mbp, rb, tc0, tc1;
         bwd_unit<TRIM>(u, a, mbp, rb, tc0, tc1);
         int tr, rh;
@@ -656,6 +662,11 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.dx = d_dx;
   a.ldx = ldx;
   a.ctr = &c->d_sc->exact_path;
+  a.wsync = nullptr;
+  if (a.hint && std::getenv("XBS_WAVE_SYNC")) {
+    a.wsync = &c->d_sc->wave_sync[1];
+    cudaMemsetAsync(a.wsync, 0, sizeof(unsigned int), st);
+  }
   const int grid_ = 2 * std::min(a.num_units, sm_count() / 2);  // CTA pairs
   auto launch = [&](auto kern, int smem) {
     static const void* done[8];
