@@ -67,6 +67,8 @@ struct FwdArgs {
   int live, live_last;  // 64-column units holding logical columns per tile column / in the last one
   int n_nb;              // scheduled column units
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = column units fastest
+  int grp;               // > 1: column units per group of the grouped order (with mfast)
+  int hinta;             // the input planes' evict-first hint (off: plane tiles shared inside a group)
   int hint;              // TMA L2 hints: digit tiles evict-last, input planes evict-first
   int64_t M, rowsF;
   int num_mbp, num_units;  // num_units = base units (M-block pair x column unit) x ksplit
@@ -101,7 +103,16 @@ __device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int&
 template <bool FAST>
 __device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int& nb, int& tr0, int& tr1) {
   const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
-  if (a.mfast) {
+  if (a.grp > 1) {
+    // groups of grp column units: inside a group the column unit runs
+    // fastest, then the M-block pair, so a round of CTA pairs covers
+    // (pairs / grp) M-block pairs x grp column units -- each bit-plane tile
+    // is read by grp pairs and each digit tile by pairs / grp of them
+    const int per = a.grp * a.num_mbp, gi = ub / per, r = ub - gi * per;
+    const int gl = min(a.grp, a.n_nb - gi * a.grp);  // the last group may be short
+    mbp = r / gl;
+    nb = gi * a.grp + (r - mbp * gl);
+  } else if (a.mfast) {
     nb = udiv<FAST>(ub, a.num_mbp, a.f_mbp);
     mbp = ub - nb * a.num_mbp;
   } else {
@@ -166,9 +177,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
       int round = 0;
+      bool wwait = true;  // (lane 0) cleared by a timed-out alignment wait
       for (int u = cid; u < a.num_units; u += ncl, ++round) {
         if (a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
-          if (lane == 0) wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)));
+          if (lane == 0) wwait = wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)), wwait);
           __syncwarp();
         }
         int mbp, nb, tr0, tr1;
@@ -186,7 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
 #pragma unroll
               for (int kb = 0; kb < KB; ++kb) {
                 uint8_t* dst = sA + as * kAStage + (dh * KB + kb) * kABox;
-                if (a.hint) tma_load_2d_pair_hint(dst, &mapA, fa, tr * a.R + kb * 128, int(dh * a.rowsF) + mrow, pol_a);
+                if (a.hinta) tma_load_2d_pair_hint(dst, &mapA, fa, tr * a.R + kb * 128, int(dh * a.rowsF) + mrow, pol_a);
                 else tma_load_2d_pair(dst, &mapA, fa, tr * a.R + kb * 128, int(dh * a.rowsF) + mrow);
               }
           }
@@ -541,7 +553,7 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
     // input planes larger than L2 stream past the digit tiles of the
     // current column unit: keep the digits resident (evict-last) and let the
     // planes go first (C5: forward DRAM reads 202 -> 142 GB, -4.6 % time;
-    // grouping column units to reuse the plane tiles measured slower)
+    // grouping column units pays only once the rounds are kept in step, below)
     a.hint = a.mfast && bytesA > l2 ? 1 : 0;
     if (std::getenv("XBS_NO_L2_HINTS")) a.hint = 0;  // A/B switch (perf experiments only)
   }
@@ -551,8 +563,18 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.y = d_y;
   a.ldy = ldy;
   a.ctr = &c->d_sc->exact_path;
+  // Both operands larger than L2 (C5): the CTA pairs of a round are kept in
+  // step (wave_align, xbs_tc_common.cuh) and a round covers 4 column units x
+  // pairs / 4 M-block pairs, so each digit tile is read through L2 by ~18
+  // pairs and each plane tile by 4 (the planes then take no evict-first
+  // hint).  C5 forward: DRAM reads 202 -> 43 GB per launch, 77.8 -> 75.4 ms
+  // (interleaved A/B, profiles/r02/wave_ab.md).  XBS_NO_WAVE_SYNC: A/B switch.
   a.wsync = nullptr;
-  if (a.hint && std::getenv("XBS_WAVE_SYNC")) {
+  a.grp = 1;
+  a.hinta = a.hint;
+  if (a.hint && !std::getenv("XBS_NO_WAVE_SYNC")) {
+    a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
+    a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[0];
     cudaMemsetAsync(a.wsync, 0, sizeof(unsigned int), st);
   }

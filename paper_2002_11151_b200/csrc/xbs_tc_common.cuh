@@ -139,10 +139,17 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // L2 turns over in ~50 us); nothing else keeps persistent CTAs in step, so
 // each producer arrives on a global counter at the start of a round of units
 // and waits (at most ~30 us) for the others.
-__device__ __forceinline__ void wave_align(unsigned int* ctr, unsigned int target) {
+// Returns false when the wait timed out (the caller then stops waiting: the
+// CTA pairs are not all resident, e.g. another kernel shares the GPU).
+__device__ __forceinline__ bool wave_align(unsigned int* ctr, unsigned int target, bool wait) {
   atomicAdd(ctr, 1u);
+  if (!wait) return false;
   const long long t0 = clock64();
-  while (*reinterpret_cast<volatile unsigned int*>(ctr) < target && clock64() - t0 < 60000) __nanosleep(64);
+  while (*reinterpret_cast<volatile unsigned int*>(ctr) < target) {
+    if (clock64() - t0 > 60000) return false;
+    __nanosleep(64);
+  }
+  return true;
 }
 
 // ------------------------------------------------- CTA pairs (cta_group::2)

@@ -148,6 +148,8 @@ struct BwdArgs {
   int live, live_last;  // 64-row blocks holding logical rows per row tile / in the last row tile
   int n_rb;              // scheduled row blocks
   int mfast;             // unit order: 1 = M-block pairs fastest (digits streamed once), 0 = row blocks fastest
+  int grp;               // > 1: row blocks per group of the grouped order (with mfast)
+  int hinta;             // the error planes' evict-first hint (off: plane tiles shared inside a group)
   int hint;              // TMA L2 hints: digit tiles evict-last, error planes evict-first
   int64_t M, rowsB;
   int num_mbp, num_units;  // num_units = base units (M-block pair x row block) x ksplit
@@ -186,7 +188,12 @@ __device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int
 template <bool FAST>
 __device__ __forceinline__ void bwd_unit(int u, const BwdArgs& a, int& mbp, int& rb, int& tc0, int& tc1) {
   const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
-  if (a.mfast) {
+  if (a.grp > 1) {  // grouped order, as fwd_unit (xbs_fwd_tc.cu)
+    const int per = a.grp * a.num_mbp, gi = ub / per, r = ub - gi * per;
+    const int gl = min(a.grp, a.n_rb - gi * a.grp);
+    mbp = r / gl;
+    rb = gi * a.grp + (r - mbp * gl);
+  } else if (a.mfast) {
     rb = udiv<FAST>(ub, a.num_mbp, a.f_mbp);
     mbp = ub - rb * a.num_mbp;
   } else {
@@ -262,9 +269,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t as = 0, aph = 0, bs = 0, bph = 0;
       const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
       int round = 0;
+      bool wwait = true;  // (lane 0) cleared by a timed-out alignment wait
       for (int u = cid; u < a.num_units; u += ncl, ++round) {
         if (a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
-          if (lane == 0) wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)));
+          if (lane == 0) wwait = wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)), wwait);
           __syncwarp();
         }
         int mbp, rb, tc0, tc1;
@@ -282,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int kb = 0; kb < KB; ++kb) {
                 uint8_t* dst = sA + as * kAStage + (dh * KB + kb) * kPlane;
-                if (a.hint) tma_load_2d_pair_hint(dst, &mapA, fa, tc * a.C + kb * 128, int(dh * a.rowsB) + mrow, pol_a);
+                if (a.hinta) tma_load_2d_pair_hint(dst, &mapA, fa, tc * a.C + kb * 128, int(dh * a.rowsB) + mrow, pol_a);
                 else tma_load_2d_pair(dst, &mapA, fa, tc * a.C + kb * 128, int(dh * a.rowsB) + mrow);
               }
           }
@@ -662,8 +670,15 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.dx = d_dx;
   a.ldx = ldx;
   a.ctr = &c->d_sc->exact_path;
+  // as launch_fwd_tc: rounds kept in step, 4 row blocks x pairs / 4 M-block
+  // pairs per round (C5 backward: DRAM reads 152 -> 83 GB per launch,
+  // 136.8 -> 131.5 ms)
   a.wsync = nullptr;
-  if (a.hint && std::getenv("XBS_WAVE_SYNC")) {
+  a.grp = 1;
+  a.hinta = a.hint;
+  if (a.hint && !std::getenv("XBS_NO_WAVE_SYNC")) {
+    a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
+    a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[1];
     cudaMemsetAsync(a.wsync, 0, sizeof(unsigned int), st);
   }
