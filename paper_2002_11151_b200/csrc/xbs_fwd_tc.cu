@@ -44,12 +44,10 @@ namespace xbs {
 namespace tc {
 
 namespace fw {
-#ifndef XBS_FWD_EPI_WARPS
-#define XBS_FWD_EPI_WARPS 8
-#endif
-constexpr int kEpiWarps = XBS_FWD_EPI_WARPS;
-constexpr int kCPW = 64 / (kEpiWarps / 4);  // unit columns per epilogue warp (16, 32 or 64)
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+// EW epilogue warps per CTA: 8 (32 unit columns each, software-pipelined TMEM
+// reads) or 16 (16 columns each, four warps per sub-partition as in the
+// backward kernel)
+template <int EW> constexpr int kThreadsFor = 64 + 32 * EW;
 constexpr int kCW = 64;             // device columns per unit
 constexpr int kABox = 128 * 128;    // 128 rows x 128 B (one k-block), SW128
 constexpr int kBBox = 128 * kCW;    // 128 crossbar rows x 64 columns, SW64
@@ -126,10 +124,12 @@ __device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int&
 // NARROW: some 64-column units hold fewer than 64 logical columns (N or the
 // tile width not a multiple of 64), so epilogue warps skip the conversions
 // of padded columns; full-width layers keep the plain pipelined loop.
-template <int KB, bool NARROW, bool WIDE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
+template <int KB, bool NARROW, bool WIDE, int EW = 8>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const FwdArgs a) {
   using namespace fw;
+  constexpr int kEpiWarps = EW;
+  constexpr int kCPW = 64 / (kEpiWarps / 4);  // unit columns per epilogue warp (32 or 16)
   constexpr int kAStage = fw::kAStage<KB>, kAStages = fw::kAStages<KB>, kBStages = fw::kBStages<KB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -305,8 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
       // software-pipelined TMEM reads: one 16-column half is in flight while
       // the other is converted (A: columns 0-15, B: 16-31 of this warp);
       // polarity p's lo sits at +64 p, its hi at +128 + 64 p
-      static_assert(kCPW == 32, "pipelined epilogue: 32 columns per warp");
-      uint32_t alo[16], ahi[16], blo[16], bhi[16];
+      static_assert(kCPW == 32 || kCPW == 16, "epilogue warps of 32 (pipelined) or 16 columns");
       // logical columns in this warp's 32 (narrow layers: N or the tile
       // width below the unit's 64 device columns); padded columns are
       // discarded (layers.cpp:283), so their conversions are skipped
@@ -316,7 +315,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         col_unit<NARROW>(nb, a, tcu, hu);
         nv = min(a.tile_cols, a.N - tcu * a.tile_cols) - hu * kCW - kCPW * q;
       }
-      if (NARROW && nv <= 16) {
+      if constexpr (kCPW == 16) {
+        // 16 columns per warp (the backward kernel's loop): both accumulator
+        // halves of a polarity are read, the buffer goes back to the MMA
+        // issuer after the second polarity's read, conversions follow
+        for (int c = 0; c < npair; ++c) {
+          const float w = wmag;
+          if (++sl == a.S) {
+            sl = 0;
+            wmag = k.unscale;
+          } else {
+            wmag = __fmul_rn(wmag, wstep);
+          }
+          uint32_t lo[16], hi[16];
+          mbar_wait_hint(&t_full[ab], abph);
+          tc_fence_after();
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            if (!NARROW || nv > 0) {
+              tmem_ld16(tl + ab * 256 + 64 * p, lo);
+              tmem_ld16(tl + ab * 256 + 64 * p + 128, hi);
+              tmem_wait_ld();
+            }
+            if (p == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+              if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+            }
+            if (NARROW && nv <= 0) continue;
+            const float wp = p == 0 ? w : -w;
+#ifdef XBS_STUB_EPI
+            if (lo[0] == 0xdeadbeef && hi[15] == 0x12345) P[p] += wp;
+#else
+            adc_conv8<0, 16, kCPW>(lo, hi, k, wp, P, 0, exact);
+            if (!NARROW || nv > 8) adc_conv8<8, 16, kCPW>(lo, hi, k, wp, P, 8, exact);
+#endif
+          }
+        }
+        if (NARROW && nv <= 0) continue;  // no logical output columns: nothing to combine
+      } else if (NARROW && nv <= 16) {
+        uint32_t alo[16], ahi[16], blo[16], bhi[16];
         // at most the first 16 columns: one TMEM read per polarity and buffer
         // (none when the warp holds only padding); barrier protocol unchanged
         for (int c = 0; c < npair; ++c) {
@@ -347,6 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreads, 1)
         }
         if (nv <= 0) continue;  // no logical output columns: nothing to combine
       } else {
+        uint32_t alo[16], ahi[16], blo[16], bhi[16];
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         tmem_ld16(tl + ab * 256, alo);
@@ -579,28 +619,40 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
     cudaMemsetAsync(a.wsync, 0, sizeof(unsigned int), st);
   }
   const int grid_ = 2 * std::min(a.num_units, num_sms() / 2);  // CTA pairs
-  auto launch = [&](auto kern, int smem) {
-    static const void* done[8];
+  auto launch = [&](auto kern, int smem, int threads) {
+    static const void* done[16];
     static int ndone = 0;
     bool seen = false;
     for (int k = 0; k < ndone; ++k) seen |= done[k] == reinterpret_cast<const void*>(kern);
     if (!seen) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (ndone < 8) done[ndone++] = reinterpret_cast<const void*>(kern);
+      if (ndone < 16) done[ndone++] = reinterpret_cast<const void*>(kern);
     }
-    kern<<<grid_, fw::kThreads, smem, st>>>(mA, mB, a);
+    kern<<<grid_, threads, smem, st>>>(mA, mB, a);
   };
   const bool narrow = (g.tile_cols % fw::kCW) != 0 || ((g.N - (g.GC - 1) * g.tile_cols) % fw::kCW) != 0;
   const int sel = (g.R == 256 ? 4 : 0) + (narrow ? 2 : 0) + (wide ? 1 : 0);
-  switch (sel) {
-    case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>); break;
-    case 1: launch(k_fwd_tc<1, false, true>, fw::kSmem<1>); break;
-    case 2: launch(k_fwd_tc<1, true, false>, fw::kSmem<1>); break;
-    case 3: launch(k_fwd_tc<1, true, true>, fw::kSmem<1>); break;
-    case 4: launch(k_fwd_tc<2, false, false>, fw::kSmem<2>); break;
-    case 5: launch(k_fwd_tc<2, false, true>, fw::kSmem<2>); break;
-    case 6: launch(k_fwd_tc<2, true, false>, fw::kSmem<2>); break;
-    default: launch(k_fwd_tc<2, true, true>, fw::kSmem<2>); break;
+  // epilogue warps per CTA (fw::kThreadsFor): XBS_FWD_EW is an A/B switch
+  static const int ew_env = std::getenv("XBS_FWD_EW") ? std::atoi(std::getenv("XBS_FWD_EW")) : 0;
+  const int ew = ew_env == 16 || ew_env == 8 ? ew_env : 8;
+  constexpr int T8 = fw::kThreadsFor<8>, T16 = fw::kThreadsFor<16>;
+  switch (sel + (ew == 16 ? 8 : 0)) {
+    case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>, T8); break;
+    case 1: launch(k_fwd_tc<1, false, true>, fw::kSmem<1>, T8); break;
+    case 2: launch(k_fwd_tc<1, true, false>, fw::kSmem<1>, T8); break;
+    case 3: launch(k_fwd_tc<1, true, true>, fw::kSmem<1>, T8); break;
+    case 4: launch(k_fwd_tc<2, false, false>, fw::kSmem<2>, T8); break;
+    case 5: launch(k_fwd_tc<2, false, true>, fw::kSmem<2>, T8); break;
+    case 6: launch(k_fwd_tc<2, true, false>, fw::kSmem<2>, T8); break;
+    case 7: launch(k_fwd_tc<2, true, true>, fw::kSmem<2>, T8); break;
+    case 8: launch(k_fwd_tc<1, false, false, 16>, fw::kSmem<1>, T16); break;
+    case 9: launch(k_fwd_tc<1, false, true, 16>, fw::kSmem<1>, T16); break;
+    case 10: launch(k_fwd_tc<1, true, false, 16>, fw::kSmem<1>, T16); break;
+    case 11: launch(k_fwd_tc<1, true, true, 16>, fw::kSmem<1>, T16); break;
+    case 12: launch(k_fwd_tc<2, false, false, 16>, fw::kSmem<2>, T16); break;
+    case 13: launch(k_fwd_tc<2, false, true, 16>, fw::kSmem<2>, T16); break;
+    case 14: launch(k_fwd_tc<2, true, false, 16>, fw::kSmem<2>, T16); break;
+    default: launch(k_fwd_tc<2, true, true, 16>, fw::kSmem<2>, T16); break;
   }
   if (a.acc || a.acc64) {
     const int64_t n = M * g.N;
