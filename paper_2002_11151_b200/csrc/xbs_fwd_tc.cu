@@ -327,6 +327,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
           } else {
             wmag = __fmul_rn(wmag, wstep);
           }
+#ifdef XBS_FWD16_EARLY  // experiment: read both polarities, release the buffer, then convert
+          {
+            uint32_t l0[16], h0[16], l1[16], h1[16];
+            mbar_wait_hint(&t_full[ab], abph);
+            tc_fence_after();
+            if (!NARROW || nv > 0) {
+              tmem_ld16(tl + ab * 256, l0);
+              tmem_ld16(tl + ab * 256 + 128, h0);
+              tmem_ld16(tl + ab * 256 + 64, l1);
+              tmem_ld16(tl + ab * 256 + 192, h1);
+              tmem_wait_ld();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
+            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
+            if (NARROW && nv <= 0) continue;
+            adc_conv8<0, 16, kCPW>(l0, h0, k, w, P, 0, exact);
+            if (!NARROW || nv > 8) adc_conv8<8, 16, kCPW>(l0, h0, k, w, P, 8, exact);
+            adc_conv8<0, 16, kCPW>(l1, h1, k, -w, P, 0, exact);
+            if (!NARROW || nv > 8) adc_conv8<8, 16, kCPW>(l1, h1, k, -w, P, 8, exact);
+            continue;
+          }
+#endif
           uint32_t lo[16], hi[16];
           mbar_wait_hint(&t_full[ab], abph);
           tc_fence_after();

@@ -104,8 +104,9 @@ def main():
             f.write(f"| {k} | " + " | ".join(cells) + " |\n")
             st = STAGE.get(k)
             if st and "dram__bytes_read.sum" in d:
-                traffic[st] = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + to_bytes(
+                t = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + to_bytes(
                     d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+                traffic[st] = t if t == t else None  # a metric ncu could not collect reads nan
     traffic["source"] = f"profiles/{rnd}_{cfg}_full.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
     with open(os.path.join(prof, f"traffic_{cfg}.json"), "w") as f:
         json.dump(traffic, f, indent=1)
