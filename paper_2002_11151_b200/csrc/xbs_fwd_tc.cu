@@ -26,7 +26,9 @@
 //
 // Roles per CTA (576 threads, 1 CTA / SM): warp 0 TMA producer, warp 1 TMEM
 // allocator + (leader only) MMA issuer, warps 2..17 epilogue: warp w reads
-// TMEM lanes 32 (w % 4).. and device columns 16 ((w-2)/4)...
+// TMEM lanes 32 (w % 4).. and device columns 16 ((w-2)/4)... (an 8-warp
+// variant with 32 columns per warp and software-pipelined TMEM reads is
+// kept behind XBS_FWD_EW=8 for A/B runs)
 // Pipelines per CTA: A (own M-block: {bits, 255 bits} x KB k-blocks, 32 KB
 // per k-block) x 3 stages (2 for 256-row crossbars), B (24 KB per k-block:
 // three 64-column SW64 digit boxes) x 4, TMEM accumulators 2 x 256
@@ -327,30 +329,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
           } else {
             wmag = __fmul_rn(wmag, wstep);
           }
-#ifdef XBS_FWD16_EARLY  // experiment: read both polarities, release the buffer, then convert
-          {
-            uint32_t l0[16], h0[16], l1[16], h1[16];
-            mbar_wait_hint(&t_full[ab], abph);
-            tc_fence_after();
-            if (!NARROW || nv > 0) {
-              tmem_ld16(tl + ab * 256, l0);
-              tmem_ld16(tl + ab * 256 + 128, h0);
-              tmem_ld16(tl + ab * 256 + 64, l1);
-              tmem_ld16(tl + ab * 256 + 192, h1);
-              tmem_wait_ld();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster_relaxed(te0 + 8 * ab);
-            if (++ab == kTBufs) { ab = 0; abph ^= 1; }
-            if (NARROW && nv <= 0) continue;
-            adc_conv8<0, 16, kCPW>(l0, h0, k, w, P, 0, exact);
-            if (!NARROW || nv > 8) adc_conv8<8, 16, kCPW>(l0, h0, k, w, P, 8, exact);
-            adc_conv8<0, 16, kCPW>(l1, h1, k, -w, P, 0, exact);
-            if (!NARROW || nv > 8) adc_conv8<8, 16, kCPW>(l1, h1, k, -w, P, 8, exact);
-            continue;
-          }
-#endif
           uint32_t lo[16], hi[16];
           mbar_wait_hint(&t_full[ab], abph);
           tc_fence_after();
@@ -656,9 +634,16 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   };
   const bool narrow = (g.tile_cols % fw::kCW) != 0 || ((g.N - (g.GC - 1) * g.tile_cols) % fw::kCW) != 0;
   const int sel = (g.R == 256 ? 4 : 0) + (narrow ? 2 : 0) + (wide ? 1 : 0);
-  // epilogue warps per CTA (fw::kThreadsFor): XBS_FWD_EW is an A/B switch
+  // Epilogue warps per CTA (fw::kThreadsFor): 16 warps of 16 columns hand an
+  // accumulator back to the MMA issuer half way through its conversions
+  // (after the second polarity's TMEM read), the 8-warp software-pipelined
+  // loop only after three quarters, and with two accumulators per CTA that
+  // slack decides whether the next chain's MMAs are done when the epilogue
+  // asks for them: C5 forward 76.0 -> 65.8 ms, C2-4096 0.841 -> 0.770 ms, C3
+  // (all layers) 3.85 -> 3.36 ms, C4 12.89 -> 12.27 ms (interleaved A/B,
+  // profiles/r02/ew_ab.md).  XBS_FWD_EW=8 keeps the old loop for A/B runs.
   static const int ew_env = std::getenv("XBS_FWD_EW") ? std::atoi(std::getenv("XBS_FWD_EW")) : 0;
-  const int ew = ew_env == 16 || ew_env == 8 ? ew_env : 8;
+  const int ew = ew_env == 8 ? 8 : 16;
   constexpr int T8 = fw::kThreadsFor<8>, T16 = fw::kThreadsFor<16>;
   switch (sel + (ew == 16 ? 8 : 0)) {
     case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>, T8); break;
