@@ -474,6 +474,7 @@ void enqueue_fwd_vmm(xbs_core* c, int64_t M, const Out& out) {
   const int64_t ld = out.ld ? out.ld : M;
   double* stage = out.host ? c->d_io_out : out.p;  // written with stride M
   bool direct = false;
+  c->out_host = out.host;
   if (c->fully_ideal) {
     xbs::launch_fwd_ideal(c, M, stage, c->stream);
   } else if (c->volts_mode) {
@@ -491,6 +492,7 @@ void enqueue_bwd_vmm(xbs_core* c, const double* d_dy, int64_t M, const Out& out)
   const int64_t ld = out.ld ? out.ld : M;
   double* stage = out.host ? c->d_io_out : out.p;
   bool direct = false;
+  c->out_host = out.host;
   if (c->fully_ideal) {
     xbs::launch_bwd_ideal(c, d_dy, M, stage, c->stream);
   } else if (c->volts_mode) {

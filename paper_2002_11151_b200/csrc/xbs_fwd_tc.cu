@@ -611,10 +611,14 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   // pairs and each plane tile by 4 (the planes then take no evict-first
   // hint).  C5 forward: DRAM reads 202 -> 43 GB per launch, 77.8 -> 75.4 ms
   // (interleaved A/B, profiles/r02/wave_ab.md).  XBS_NO_WAVE_SYNC: A/B switch.
+  // Not when the epilogues store into a mapped host buffer: pairs in step
+  // finish their units together, and the 32-byte PCIe writes of all 148 CTAs
+  // then collide instead of hiding behind the other pairs' MMAs (C5 e2e
+  // 226 -> 244 ms with the alignment, profiles/r02/wave_ab.md).
   a.wsync = nullptr;
   a.grp = 1;
   a.hinta = a.hint;
-  if (a.hint && !std::getenv("XBS_NO_WAVE_SYNC")) {
+  if (a.hint && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
     a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
     a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[0];

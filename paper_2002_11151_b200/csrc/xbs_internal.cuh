@@ -134,6 +134,7 @@ struct xbs_core {
   xbs::AdcP adc{};    // forward ADC (adc_fwd_)
   xbs::AdcP adc_b{};  // backward ADC (adc_bwd_); differs from adc only after auto-calibration
   bool volts_mode = false;  // general converters: exact fp64 CUDA-core VMMs (k_fwd_volts / k_bwd_volts)
+  bool out_host = false;    // the VMM being enqueued stores into a mapped host buffer (set per call)
   bool big_tiles = false;   // tiles above 256 x 256: exact integer CUDA-core VMMs (k_fwd_simt / k_bwd_simt)
   xbs::VoltsP volts{};
   double* d_dac_lut = nullptr;

@@ -676,7 +676,7 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.wsync = nullptr;
   a.grp = 1;
   a.hinta = a.hint;
-  if (a.hint && !std::getenv("XBS_NO_WAVE_SYNC")) {
+  if (a.hint && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
     a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
     a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[1];
