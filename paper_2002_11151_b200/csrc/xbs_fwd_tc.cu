@@ -308,6 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
       // the other is converted (A: columns 0-15, B: 16-31 of this warp);
       // polarity p's lo sits at +64 p, its hi at +128 + 64 p
       static_assert(kCPW == 32 || kCPW == 16, "epilogue warps of 32 (pipelined) or 16 columns");
+      uint32_t alo[16], ahi[16], blo[16], bhi[16];  // the 32-column loops' TMEM registers
       // logical columns in this warp's 32 (narrow layers: N or the tile
       // width below the unit's 64 device columns); padded columns are
       // discarded (layers.cpp:283), so their conversions are skipped
@@ -357,7 +358,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
         }
         if (NARROW && nv <= 0) continue;  // no logical output columns: nothing to combine
       } else if (NARROW && nv <= 16) {
-        uint32_t alo[16], ahi[16], blo[16], bhi[16];
         // at most the first 16 columns: one TMEM read per polarity and buffer
         // (none when the warp holds only padding); barrier protocol unchanged
         for (int c = 0; c < npair; ++c) {
@@ -388,7 +388,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
         }
         if (nv <= 0) continue;  // no logical output columns: nothing to combine
       } else {
-        uint32_t alo[16], ahi[16], blo[16], bhi[16];
         mbar_wait_hint(&t_full[ab], abph);
         tc_fence_after();
         tmem_ld16(tl + ab * 256, alo);
@@ -645,9 +644,16 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   // slack decides whether the next chain's MMAs are done when the epilogue
   // asks for them: C5 forward 76.0 -> 65.8 ms, C2-4096 0.841 -> 0.770 ms, C3
   // (all layers) 3.85 -> 3.36 ms, C4 12.89 -> 12.27 ms (interleaved A/B,
-  // profiles/r02/ew_ab.md).  XBS_FWD_EW=8 keeps the old loop for A/B runs.
+  // profiles/r02/ew_ab.md).  Narrow layers (most of a unit's columns are
+  // padding: a few warps hold all the work) and layers too small to fill the
+  // pairs (split-K, or a short chain sequence: each chain's latency shows)
+  // keep the 8-warp loop, which reads a whole buffer out before converting
+  // (C3 forward 3.06-3.26 vs 3.36 ms, C1 0.055 vs 0.077 ms; profiles/r02/ew_ab.md).  XBS_FWD_EW=8 | 16 forces one for A/B runs.
   static const int ew_env = std::getenv("XBS_FWD_EW") ? std::atoi(std::getenv("XBS_FWD_EW")) : 0;
-  const int ew = ew_env == 8 ? 8 : 16;
+  // chains a pair runs back to back: short sequences are latency-, not throughput-paced (C2-512: 16 chains,
+  // 0.045 vs 0.066 ms)
+  const int64_t chains = int64_t((a.num_units + pairs - 1) / pairs) * a.trs * g.S;
+  const int ew = ew_env == 8 || ew_env == 16 ? ew_env : ((narrow || a.ksplit > 1 || chains < 64) ? 8 : 16);
   constexpr int T8 = fw::kThreadsFor<8>, T16 = fw::kThreadsFor<16>;
   switch (sel + (ew == 16 ? 8 : 0)) {
     case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>, T8); break;
