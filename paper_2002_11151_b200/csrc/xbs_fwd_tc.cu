@@ -103,7 +103,7 @@ __device__ __forceinline__ void col_unit(int nb, const FwdArgs& a, int& tc, int&
 template <bool FAST>
 __device__ __forceinline__ void fwd_unit(int u, const FwdArgs& a, int& mbp, int& nb, int& tr0, int& tr1) {
   const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
-  if (a.grp > 1) {
+  if (!FAST && a.grp > 1) {  // (full-width instantiations only: the narrow ones keep their short decode)
     // groups of grp column units: inside a group the column unit runs
     // fastest, then the M-block pair, so a round of CTA pairs covers
     // (pairs / grp) M-block pairs x grp column units -- each bit-plane tile
@@ -181,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fw::kThreadsFor<EW>,
       int round = 0;
       bool wwait = true;  // (lane 0) cleared by a timed-out alignment wait
       for (int u = cid; u < a.num_units; u += ncl, ++round) {
-        if (a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
+        if (!NARROW && a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
           if (lane == 0) wwait = wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)), wwait);
           __syncwarp();
         }
@@ -617,7 +617,8 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   a.wsync = nullptr;
   a.grp = 1;
   a.hinta = a.hint;
-  if (a.hint && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
+  const bool narrow_cols = (g.tile_cols % fw::kCW) != 0 || ((g.N - (g.GC - 1) * g.tile_cols) % fw::kCW) != 0;
+  if (a.hint && !narrow_cols && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
     a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
     a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[0];

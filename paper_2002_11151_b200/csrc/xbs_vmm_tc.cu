@@ -188,7 +188,7 @@ __device__ __forceinline__ void row_block(int rb, const BwdArgs& a, int& tr, int
 template <bool FAST>
 __device__ __forceinline__ void bwd_unit(int u, const BwdArgs& a, int& mbp, int& rb, int& tc0, int& tc1) {
   const int sp = udiv<FAST>(u, a.nbase, a.f_nbase), ub = u - sp * a.nbase;
-  if (a.grp > 1) {  // grouped order, as fwd_unit (xbs_fwd_tc.cu)
+  if (!FAST && a.grp > 1) {  // grouped order, as fwd_unit (xbs_fwd_tc.cu); full-width instantiations only
     const int per = a.grp * a.num_mbp, gi = ub / per, r = ub - gi * per;
     const int gl = min(a.grp, a.n_rb - gi * a.grp);
     mbp = r / gl;
@@ -271,7 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int round = 0;
       bool wwait = true;  // (lane 0) cleared by a timed-out alignment wait
       for (int u = cid; u < a.num_units; u += ncl, ++round) {
-        if (a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
+        if (!TRIM && a.wsync) {  // all producers start a round of units together (xbs_tc_common.cuh)
           if (lane == 0) wwait = wave_align(a.wsync, 2u * uint32_t(min(a.num_units, (round + 1) * ncl)), wwait);
           __syncwarp();
         }
@@ -676,7 +676,9 @@ bool launch_bwd_tc(xbs_core* c, int64_t M, double* d_dx, int64_t ldx, cudaStream
   a.wsync = nullptr;
   a.grp = 1;
   a.hinta = a.hint;
-  if (a.hint && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
+  const bool trim_any = (g.N % g.tile_cols) != 0 || g.tile_cols <= g.C - 32 || (g.tile_rows % 64) != 0 ||
+                        ((g.K - (g.GR - 1) * g.tile_rows) % 64) != 0;  // the TRIM instantiations (below)
+  if (a.hint && !trim_any && !c->out_host && !std::getenv("XBS_NO_WAVE_SYNC")) {
     a.grp = std::getenv("XBS_WAVE_GROUP") ? std::max(1, std::atoi(std::getenv("XBS_WAVE_GROUP"))) : 4;
     a.hinta = a.grp > 1 && !std::getenv("XBS_WAVE_AHINT") ? 0 : 1;
     a.wsync = &c->d_sc->wave_sync[1];
