@@ -652,9 +652,9 @@ bool launch_fwd_tc(xbs_core* c, int64_t M, double* d_y, int64_t ldy, cudaStream_
   // (C3 forward 3.06-3.26 vs 3.36 ms, C1 0.055 vs 0.077 ms; profiles/r02/ew_ab.md).  XBS_FWD_EW=8 | 16 forces one for A/B runs.
   static const int ew_env = std::getenv("XBS_FWD_EW") ? std::atoi(std::getenv("XBS_FWD_EW")) : 0;
   // chains a pair runs back to back: short sequences are latency-, not throughput-paced (C2-512: 16 chains,
-  // 0.045 vs 0.066 ms)
+  // 0.045 vs 0.066 ms; C2-1024: 64 chains, 0.086 vs 0.099 ms; C2-2048: 256 chains, 0.259 vs 0.246 ms)
   const int64_t chains = int64_t((a.num_units + pairs - 1) / pairs) * a.trs * g.S;
-  const int ew = ew_env == 8 || ew_env == 16 ? ew_env : ((narrow || a.ksplit > 1 || chains < 64) ? 8 : 16);
+  const int ew = ew_env == 8 || ew_env == 16 ? ew_env : ((narrow || a.ksplit > 1 || chains < 128) ? 8 : 16);
   constexpr int T8 = fw::kThreadsFor<8>, T16 = fw::kThreadsFor<16>;
   switch (sel + (ew == 16 ? 8 : 0)) {
     case 0: launch(k_fwd_tc<1, false, false>, fw::kSmem<1>, T8); break;
